@@ -1,0 +1,161 @@
+/*
+ * gwgrid_cuda.h — C ABI of the B200-native GLS-grid engine (the drop-in
+ * boundary for the reference gwgrid hot path).
+ *
+ * The reference (gwgrid, arXiv 1210.7683) has no plugin/FFI layer; its seam
+ * for this path is the C++ library API in proj/include/gwgrid/grid.hpp, called
+ * from run_grid's compute phase (proj/src/grid.cpp:541-552), plus the in-memory
+ * Python contract gwgrid.solve_grid (proj/python/bindings.cpp:115-190,318-328).
+ * Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes, column-major FP64 operands, int64 dimensions.
+ *   - Every call returns a status code (0 = ok) and fills *st when non-null.
+ *   - Codes map 1:1 onto the reference error hierarchy
+ *     (proj/include/gwgrid/types.hpp:34-94); GWG_NOT_POSITIVE_DEFINITE carries
+ *     the grid coordinates (snp_index, trait_index), -1 = not applicable.
+ *   - One engine per device; calls on one engine must be serialised by the
+ *     caller (the reference's CT coordinator thread, grid.cpp:519-552).
+ *   - `where` flags say whether a pointer is host (GWG_HOST) or device
+ *     (GWG_DEVICE) memory.  Host buffers may be pageable or pinned; pinned
+ *     buffers give overlapped transfers.
+ *   - Output layouts: GWG_LAYOUT_NUMPY writes cell (i, j) at (i*t + j)*p
+ *     (the numpy (m, t, p) array of bindings.cpp:176-184); GWG_LAYOUT_STREAM
+ *     writes it at (j*m + i)*p (the GWG1 result stream, stream.hpp:31-34).
+ */
+#ifndef GWGRID_CUDA_H_
+#define GWGRID_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum gwg_code {
+  GWG_OK = 0,
+  GWG_DIMENSION = 1,               /* DimensionError          types.hpp:38-40 */
+  GWG_NON_SYMMETRIC = 2,           /* NonSymmetricError       types.hpp:43-45 */
+  GWG_BACKEND = 3,                 /* BackendError            types.hpp:48-50 */
+  GWG_NOT_POSITIVE_DEFINITE = 4,   /* NotPositiveDefiniteError types.hpp:55-63 */
+  GWG_IO = 5,                      /* IoError                 types.hpp:66-68 */
+  GWG_INFEASIBLE_BUDGET = 6,       /* InfeasibleBudgetError   types.hpp:91-93 */
+  GWG_CUDA = 7                     /* device/runtime failure (no reference analogue) */
+};
+
+enum gwg_where { GWG_HOST = 0, GWG_DEVICE = 1 };
+enum gwg_layout { GWG_LAYOUT_NUMPY = 0, GWG_LAYOUT_STREAM = 1 };
+
+typedef struct gwg_status {
+  int32_t code;
+  int64_t snp_index;
+  int64_t trait_index;
+  char msg[256];
+} gwg_status;
+
+/* Analytic counters, same buckets as RunCounters (counters.hpp:62-127), plus
+ * device-side timings. */
+typedef struct gwg_counters {
+  uint64_t preloop_flops;      /* rotations of X_L and X_R (2 n^2 cols)            */
+  uint64_t loop_flops;         /* trait contexts + cells, reference convention      */
+  uint64_t grid_flops;         /* 2 n (p+1) per cell: the DMMA contraction work     */
+  uint64_t bytes_loaded;       /* host->device bytes                                 */
+  uint64_t bytes_stored;       /* device->host bytes                                 */
+  uint64_t context_builds;     /* trait-prep launches (one per gwg_set_traits)       */
+  uint64_t kernel_launches;    /* launches of this library's own kernels            */
+  double grid_kernel_ms;       /* summed CUDA-event time of the fused grid kernel    */
+  double rotate_ms;            /* summed CUDA-event time of the SNP rotations        */
+  double wall_ms;              /* host wall time of the last run_grid                */
+} gwg_counters;
+
+typedef struct gwg_run_options {
+  int64_t mb;          /* SNP columns per streamed slab; 0 = engine default       */
+  int32_t layout;      /* gwg_layout of the host result buffer                    */
+  int32_t double_buffer; /* 1 = overlap H2D / compute / D2H (default)            */
+} gwg_run_options;
+
+typedef struct gwg_engine gwg_engine;
+
+/* Library identity: "gwgrid_cuda <version> sm_100a". */
+const char* gwg_version(void);
+
+/* Create an engine on `device` for n samples and p predictors per fit
+ * (p-1 shared covariates + 1 variant column).  Replaces the construction of
+ * GridPrecompute (grid.hpp:81-87).  Returns NULL and fills *st on failure. */
+gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* st);
+void gwg_engine_destroy(gwg_engine* e);
+
+/* Install the kinship eigensystem Phi = Z diag(lambda) Z^T (Z: n x n col-major,
+ * lambda ascending).  The eigendecomposition itself stays on the CPU
+ * (eigendecompose_kinship, gls.cpp:16-46); this replaces its storage in
+ * GridPrecompute::spectrum (grid.hpp:81-87). */
+int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambda,
+                         int32_t where, gwg_status* st);
+
+/* Install X_L (n x (p-1), col-major, raw) and rotate it on the device:
+ * X_L' = Z^T X_L.  Replaces rotate_columns(Z, X_L) inside precompute_grid
+ * (grid.cpp:83-101). */
+int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_status* st);
+
+/* Install t traits Y (n x t col-major; raw unless is_rotated) with per-trait
+ * h2[t], sigma2[t]; rotates Y on the device and builds every trait context
+ * (weights d, D = 1/d, D.Y', D.X_L', S_TL, chol(S_TL), z_T) in one kernel.
+ * Replaces transform_trait_slab + build_trait_contexts (grid.cpp:135-175) and
+ * the per-pass load_pass (grid.cpp:501-517).  A trait whose rotated weights
+ * fail the relative floor (gls.cpp:59-75) fails with
+ * GWG_NOT_POSITIVE_DEFINITE, snp_index = -1, trait_index = the first such j. */
+int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* h2,
+                       const double* sigma2, int32_t where, int32_t is_rotated,
+                       gwg_status* st);
+
+/* Solve the cells of one SNP slab against every installed trait:
+ * rows = mb SNP columns starting at global SNP index i0, x_r = n x mb
+ * col-major (raw unless is_rotated; rotated on the device when raw).
+ * Results for cell (il, j) go to b_out at
+ *   layout NUMPY : (il * t + j) * p           (slab-local numpy order)
+ *   layout STREAM: (j * ldo + il) * p         (result-stream order, ldo >= mb)
+ * b_out may be host or device memory (out_where).  Replaces
+ * transform_snp_slab + compute_tile (grid.cpp:125-133, 220-273); the first
+ * failing cell in trait-major order (j*m_total + i) is reported with its
+ * global coordinates like compute_block (grid.cpp:206-212). */
+int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* x_r,
+                           int32_t where, int32_t is_rotated, double* b_out,
+                           int32_t out_where, int32_t layout, int64_t ldo,
+                           gwg_status* st);
+
+/* Stream the whole m x t grid from host memory: X_R (n x m, raw, col-major)
+ * in mb-column slabs through double-buffered H2D / rotate+grid / D2H on three
+ * CUDA streams, into the host result buffer b (m*t*p doubles, `layout`).
+ * Replaces preloop_stream_transform + run_grid (grid.cpp:378-641) for
+ * in-memory operands (the GWG1 file legs are out of scope). */
+int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
+                     const gwg_run_options* opts, gwg_counters* counters,
+                     gwg_status* st);
+
+/* Counters accumulated since the last reset. */
+int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out);
+void gwg_reset_counters(gwg_engine* e);
+
+/* Wait for all work queued by this engine. */
+int32_t gwg_synchronize(gwg_engine* e, gwg_status* st);
+
+/* The engine's compute stream (cudaStream_t as void*), so callers can order
+ * their own device work (timing events, torch streams) against it. */
+void* gwg_compute_stream(gwg_engine* e);
+
+/* Seeded synthetic inputs with BASELINE.json's generators (counter-based
+ * splitmix64 per (seed, matrix, column, row), so any column range is
+ * reproducible independently).  matrix ids: 1 = kinship genotypes G,
+ * 2 = covariates, 3 = SNPs X_R, 4 = traits Y, 5 = h2.  Host-side, threaded. */
+void gwg_gen_genotypes(uint64_t seed, int32_t matrix, int64_t rows, int64_t col0,
+                       int64_t ncols, int32_t standardize, double* out, int64_t ld);
+void gwg_gen_normals(uint64_t seed, int32_t matrix, int64_t rows, int64_t col0,
+                     int64_t ncols, double* out, int64_t ld);
+void gwg_gen_uniform(uint64_t seed, int32_t matrix, int64_t count, double lo, double hi,
+                     double* out);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* GWGRID_CUDA_H_ */

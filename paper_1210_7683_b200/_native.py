@@ -1,0 +1,123 @@
+"""ctypes binding of libgwgrid_cuda.so (the C ABI in include/gwgrid_cuda.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_1210_7683_b200/csrc``).  There is no fallback: if the library is
+missing, importing the engine raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgwgrid_cuda.so")
+
+GWG_OK = 0
+GWG_DIMENSION = 1
+GWG_NON_SYMMETRIC = 2
+GWG_BACKEND = 3
+GWG_NOT_POSITIVE_DEFINITE = 4
+GWG_IO = 5
+GWG_INFEASIBLE_BUDGET = 6
+GWG_CUDA = 7
+
+GWG_HOST = 0
+GWG_DEVICE = 1
+GWG_LAYOUT_NUMPY = 0
+GWG_LAYOUT_STREAM = 1
+
+# Every symbol include/gwgrid_cuda.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "gwg_version",
+    "gwg_engine_create",
+    "gwg_engine_destroy",
+    "gwg_set_spectrum",
+    "gwg_set_covariates",
+    "gwg_set_traits",
+    "gwg_solve_snp_slab",
+    "gwg_run_grid",
+    "gwg_get_counters",
+    "gwg_reset_counters",
+    "gwg_synchronize",
+    "gwg_compute_stream",
+    "gwg_gen_genotypes",
+    "gwg_gen_normals",
+    "gwg_gen_uniform",
+)
+
+
+class Status(ctypes.Structure):
+    _fields_ = [
+        ("code", ctypes.c_int32),
+        ("snp_index", ctypes.c_int64),
+        ("trait_index", ctypes.c_int64),
+        ("msg", ctypes.c_char * 256),
+    ]
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [
+        ("preloop_flops", ctypes.c_uint64),
+        ("loop_flops", ctypes.c_uint64),
+        ("grid_flops", ctypes.c_uint64),
+        ("bytes_loaded", ctypes.c_uint64),
+        ("bytes_stored", ctypes.c_uint64),
+        ("context_builds", ctypes.c_uint64),
+        ("kernel_launches", ctypes.c_uint64),
+        ("grid_kernel_ms", ctypes.c_double),
+        ("rotate_ms", ctypes.c_double),
+        ("wall_ms", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class RunOptions(ctypes.Structure):
+    _fields_ = [
+        ("mb", ctypes.c_int64),
+        ("layout", ctypes.c_int32),
+        ("double_buffer", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the native library once; raise loudly when it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    I32, I64, U64, D = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    S = ctypes.POINTER(Status)
+    sig = {
+        "gwg_version": (ctypes.c_char_p, []),
+        "gwg_engine_create": (P, [I32, I64, I64, S]),
+        "gwg_engine_destroy": (None, [P]),
+        "gwg_set_spectrum": (I32, [P, P, P, I32, S]),
+        "gwg_set_covariates": (I32, [P, P, I32, S]),
+        "gwg_set_traits": (I32, [P, I64, P, P, P, I32, I32, S]),
+        "gwg_solve_snp_slab": (I32, [P, I64, I64, P, I32, I32, P, I32, I32, I64, S]),
+        "gwg_run_grid": (I32, [P, I64, P, P, ctypes.POINTER(RunOptions),
+                               ctypes.POINTER(Counters), S]),
+        "gwg_get_counters": (I32, [P, ctypes.POINTER(Counters)]),
+        "gwg_reset_counters": (None, [P]),
+        "gwg_synchronize": (I32, [P, S]),
+        "gwg_compute_stream": (P, [P]),
+        "gwg_gen_genotypes": (None, [U64, I32, I64, I64, I64, I32, P, I64]),
+        "gwg_gen_normals": (None, [U64, I32, I64, I64, I64, P, I64]),
+        "gwg_gen_uniform": (None, [U64, I32, I64, D, D, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,673 @@
+// engine.cu — host engine + C ABI (include/gwgrid_cuda.h) of the B200 GLS grid.
+//
+// Reference seams replaced here (proj/include/gwgrid/grid.hpp):
+//   precompute_grid / GridPrecompute        -> gwg_set_spectrum + gwg_set_covariates
+//   transform_trait_slab + build_trait_contexts + load_pass -> gwg_set_traits
+//   transform_snp_slab + compute_tile        -> gwg_solve_snp_slab
+//   preloop_stream_transform + run_grid (CT, double-buffered pipeline_run,
+//   pipeline.hpp:78-137)                     -> gwg_run_grid
+// Rotations are cuBLAS DGEMMs (plain library GEMMs); the per-trait context
+// and the fused grid kernel are this library's own sm_100a kernels.
+#include <cublas_v2.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/gwgrid_cuda.h"
+#include "kernel_table.cuh"
+
+namespace {
+
+using gwg::kBK;
+using gwg::KernelOps;
+
+int set_status(gwg_status* st, int code, int64_t snp, int64_t trait, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    st->snp_index = snp;
+    st->trait_index = trait;
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(st->msg, sizeof(st->msg), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+void clear_status(gwg_status* st) {
+  if (st) {
+    st->code = GWG_OK;
+    st->snp_index = -1;
+    st->trait_index = -1;
+    st->msg[0] = 0;
+  }
+}
+
+#define GWG_CUDA_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cudaError_t err_ = (expr);                                                             \
+    if (err_ != cudaSuccess)                                                               \
+      return set_status(st, GWG_CUDA, -1, -1, "%s failed: %s (%s:%d)", #expr,              \
+                        cudaGetErrorString(err_), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define GWG_BLAS_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cublasStatus_t err_ = (expr);                                                          \
+    if (err_ != CUBLAS_STATUS_SUCCESS)                                                     \
+      return set_status(st, GWG_BACKEND, -1, -1, "%s failed: cublas status %d", #expr,     \
+                        int(err_));                                                        \
+  } while (0)
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(ptr); }
+};
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+struct gwg_engine {
+  int device = 0;
+  int sms = 148;
+  int64_t n = 0, p = 0, np = 0;
+  KernelOps ops;
+  cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
+  cublasHandle_t blas = nullptr;
+
+  DevBuf basis, lambda, xl_raw, xl_rot;
+  bool have_spectrum = false, have_covariates = false;
+
+  int64_t t = 0;
+  bool have_traits = false;
+  DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
+
+  DevBuf raw[2], rot, out[2];
+  DevBuf err;  // [0] trait error key, [1] cell error key
+  unsigned long long* err_host = nullptr;
+
+  cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
+  cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
+  std::vector<cudaEvent_t> slab_events;
+
+  gwg_counters counters{};
+};
+
+namespace {
+
+int check_engine(gwg_engine* e, gwg_status* st) {
+  if (!e) return set_status(st, GWG_DIMENSION, -1, -1, "null engine");
+  cudaError_t err = cudaSetDevice(e->device);
+  if (err != cudaSuccess)
+    return set_status(st, GWG_CUDA, -1, -1, "cudaSetDevice: %s", cudaGetErrorString(err));
+  return GWG_OK;
+}
+
+int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int where,
+           gwg_status* st) {
+  GWG_CUDA_TRY(dst.ensure(std::max<size_t>(count, 1) * sizeof(double)));
+  if (count == 0) return GWG_OK;
+  GWG_CUDA_TRY(cudaMemcpyAsync(dst.ptr, src, count * sizeof(double),
+                               where == GWG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyHostToDevice,
+                               e->comp));
+  if (where != GWG_DEVICE) e->counters.bytes_loaded += count * sizeof(double);
+  return GWG_OK;
+}
+
+// dst (ld ldc) = Z^T src (n x cols, ld lds)
+int rotate(gwg_engine* e, const double* src, int64_t lds, int64_t cols, double* dst,
+           int64_t ldc, gwg_status* st) {
+  if (cols <= 0) return GWG_OK;
+  const double one = 1.0, zero = 0.0;
+  GWG_BLAS_TRY(cublasDgemm(e->blas, CUBLAS_OP_T, CUBLAS_OP_N, int(e->n), int(cols), int(e->n),
+                           &one, e->basis.d(), int(e->n), src, int(lds), &zero, dst, int(ldc)));
+  e->counters.preloop_flops += 2ull * uint64_t(e->n) * uint64_t(e->n) * uint64_t(cols);
+  return GWG_OK;
+}
+
+int read_errors(gwg_engine* e, gwg_status* st, bool trait_only) {
+  GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, e->comp));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  (void)trait_only;
+  return GWG_OK;
+}
+
+int reset_errors(gwg_engine* e, gwg_status* st) {
+  GWG_CUDA_TRY(cudaMemsetAsync(e->err.ptr, 0xff, 2 * sizeof(unsigned long long), e->comp));
+  return GWG_OK;
+}
+
+// Grid kernel over one rotated slab (rot: ld np, `rows` SNPs) into dev_out.
+int launch_slab(gwg_engine* e, const double* rot, int64_t rows, int64_t i0, int64_t m_total,
+                double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
+  auto encode = get_encode();
+  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {cuuint64_t(e->n), cuuint64_t(rows)};
+  const cuuint64_t gstride[1] = {cuuint64_t(e->np) * sizeof(double)};
+  const cuuint32_t box[2] = {8, cuuint32_t(e->ops.bm)};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(rot), gdim,
+                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  gwg::GridArgs a;
+  a.bops = e->bops.d();
+  a.ctx = e->ctx.d();
+  a.out = dev_out;
+  a.out_si = out_si;
+  a.out_sj = out_sj;
+  a.rows = rows;
+  a.i0 = i0;
+  a.m_total = m_total;
+  a.t = int32_t(e->t);
+  a.tiles_m = int32_t(ceil_div(rows, e->ops.bm));
+  a.tiles_t = int32_t(ceil_div(e->t, e->ops.bt));
+  a.kchunks = int32_t(e->np / kBK);
+  a.np = e->np;
+  a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_t;
+  const int ctas = int(std::min<int64_t>(tiles, e->sms));
+  GWG_CUDA_TRY(e->ops.grid(map, a, ctas, e->comp));
+  e->counters.kernel_launches += 1;
+  const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
+  e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
+  e->counters.loop_flops += cells * uint64_t(e->n) * (5 + 2 * uint64_t(e->p - 1));
+  return GWG_OK;
+}
+
+int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
+  const unsigned long long key = e->err_host[1];
+  if (key == ~0ull) return GWG_OK;
+  const int64_t j = int64_t(key / uint64_t(m_total));
+  const int64_t i = int64_t(key % uint64_t(m_total));
+  return set_status(st, GWG_NOT_POSITIVE_DEFINITE, i, j,
+                    "normal equations are not positive definite at cell (variant %lld, trait "
+                    "%lld)",
+                    (long long)i, (long long)j);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gwg_version(void) { return "gwgrid_cuda 0.1.0 sm_100a"; }
+
+gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* st) {
+  clear_status(st);
+  if (n < 1 || p < 1 || p > n) {
+    set_status(st, GWG_DIMENSION, -1, -1, "bad dimensions n=%lld p=%lld", (long long)n,
+               (long long)p);
+    return nullptr;
+  }
+  if (n > (int64_t(1) << 30)) {
+    set_status(st, GWG_DIMENSION, -1, -1, "n too large");
+    return nullptr;
+  }
+  KernelOps ops;
+  if (!gwg::ops_for(p, &ops)) {
+    set_status(st, GWG_DIMENSION, -1, -1,
+               "p=%lld is outside the compiled predictor range 1..24", (long long)p);
+    return nullptr;
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+    cudaGetLastError();
+    set_status(st, GWG_CUDA, -1, -1, "CUDA device %d not available", device);
+    return nullptr;
+  }
+  auto* e = new gwg_engine();
+  e->device = device;
+  e->n = n;
+  e->p = p;
+  e->np = round_up(n, kBK);
+  e->ops = ops;
+  auto bail = [&](const char* what, cudaError_t err) {
+    set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
+    gwg_engine_destroy(e);
+    return nullptr;
+  };
+  cudaError_t err;
+  if ((err = cudaSetDevice(device)) != cudaSuccess) return bail("cudaSetDevice", err);
+  cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device);
+  int cc_major = 0;
+  cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  if (cc_major != 10) {
+    set_status(st, GWG_CUDA, -1, -1, "device %d has compute capability %d.x; sm_100a required",
+               device, cc_major);
+    gwg_engine_destroy(e);
+    return nullptr;
+  }
+  if ((err = cudaStreamCreateWithFlags(&e->comp, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail("stream", err);
+  if ((err = cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail("stream", err);
+  if ((err = cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail("stream", err);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventCreateWithFlags(&e->ev_h2d[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e->ev_rot_done[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e->ev_comp[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&e->ev_d2h_done[b], cudaEventDisableTiming);
+  }
+  cudaEventCreate(&e->ev_k0);
+  cudaEventCreate(&e->ev_k1);
+  cudaEventCreate(&e->ev_r0);
+  cudaEventCreate(&e->ev_r1);
+  if (cublasCreate(&e->blas) != CUBLAS_STATUS_SUCCESS) {
+    set_status(st, GWG_BACKEND, -1, -1, "cublasCreate failed");
+    gwg_engine_destroy(e);
+    return nullptr;
+  }
+  cublasSetStream(e->blas, e->comp);
+  cublasSetMathMode(e->blas, CUBLAS_PEDANTIC_MATH);  // true FP64, no emulation
+  if ((err = e->err.ensure(2 * sizeof(unsigned long long))) != cudaSuccess)
+    return bail("cudaMalloc", err);
+  if ((err = cudaMallocHost(&e->err_host, 2 * sizeof(unsigned long long))) != cudaSuccess)
+    return bail("cudaMallocHost", err);
+  return e;
+}
+
+void gwg_engine_destroy(gwg_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->comp) cudaStreamSynchronize(e->comp);
+  if (e->h2d) cudaStreamSynchronize(e->h2d);
+  if (e->d2h) cudaStreamSynchronize(e->d2h);
+  for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
+                    &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->out[0],
+                    &e->out[1], &e->err})
+    b->release();
+  if (e->err_host) cudaFreeHost(e->err_host);
+  if (e->blas) cublasDestroy(e->blas);
+  for (int b = 0; b < 2; ++b) {
+    if (e->ev_h2d[b]) cudaEventDestroy(e->ev_h2d[b]);
+    if (e->ev_rot_done[b]) cudaEventDestroy(e->ev_rot_done[b]);
+    if (e->ev_comp[b]) cudaEventDestroy(e->ev_comp[b]);
+    if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
+  }
+  for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
+  if (e->comp) cudaStreamDestroy(e->comp);
+  if (e->h2d) cudaStreamDestroy(e->h2d);
+  if (e->d2h) cudaStreamDestroy(e->d2h);
+  delete e;
+}
+
+int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambda, int32_t where,
+                         gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!basis || !lambda) return set_status(st, GWG_DIMENSION, -1, -1, "null spectrum operand");
+  if (int rc = upload(e, e->basis, basis, size_t(e->n) * e->n, where, st)) return rc;
+  if (int rc = upload(e, e->lambda, lambda, size_t(e->n), where, st)) return rc;
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  e->have_spectrum = true;
+  e->have_covariates = false;
+  e->have_traits = false;
+  return GWG_OK;
+}
+
+int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!e->have_spectrum)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_spectrum must come first");
+  const int64_t pm1 = e->p - 1;
+  GWG_CUDA_TRY(e->xl_rot.ensure(std::max<int64_t>(pm1, 1) * e->n * sizeof(double)));
+  if (pm1 > 0) {
+    if (!xl) return set_status(st, GWG_DIMENSION, -1, -1, "null covariate block");
+    if (int rc = upload(e, e->xl_raw, xl, size_t(e->n) * pm1, where, st)) return rc;
+    if (int rc = rotate(e, e->xl_raw.d(), e->n, pm1, e->xl_rot.d(), e->n, st)) return rc;
+  }
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  e->have_covariates = true;
+  e->have_traits = false;
+  return GWG_OK;
+}
+
+int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* h2,
+                       const double* sigma2, int32_t where, int32_t is_rotated, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!e->have_covariates)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_covariates must come first");
+  if (t < 1 || t > (int64_t(1) << 31) - 1)
+    return set_status(st, GWG_DIMENSION, -1, -1, "trait count out of range (got %lld)",
+                      (long long)t);
+  if (!y || !h2 || !sigma2) return set_status(st, GWG_DIMENSION, -1, -1, "null trait operand");
+  e->have_traits = false;
+  const int64_t n = e->n;
+  const double* y_rot = nullptr;
+  if (is_rotated) {
+    if (where == GWG_DEVICE) {
+      y_rot = y;
+    } else {
+      if (int rc = upload(e, e->y_rot, y, size_t(n) * t, where, st)) return rc;
+      y_rot = e->y_rot.d();
+    }
+  } else {
+    const double* src = y;
+    if (where != GWG_DEVICE) {
+      if (int rc = upload(e, e->y_raw, y, size_t(n) * t, where, st)) return rc;
+      src = e->y_raw.d();
+    }
+    GWG_CUDA_TRY(e->y_rot.ensure(size_t(n) * t * sizeof(double)));
+    if (int rc = rotate(e, src, n, t, e->y_rot.d(), n, st)) return rc;
+    y_rot = e->y_rot.d();
+  }
+  if (int rc = upload(e, e->h2, h2, size_t(t), where, st)) return rc;
+  if (int rc = upload(e, e->sigma2, sigma2, size_t(t), where, st)) return rc;
+  const int64_t tiles_t = ceil_div(t, e->ops.bt);
+  const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
+  GWG_CUDA_TRY(e->bops.ensure(bops_doubles * sizeof(double)));
+  GWG_CUDA_TRY(e->ctx.ensure(size_t(t) * e->ops.ctx_stride * sizeof(double)));
+  GWG_CUDA_TRY(cudaMemsetAsync(e->bops.ptr, 0, bops_doubles * sizeof(double), e->comp));
+  if (int rc = reset_errors(e, st)) return rc;
+  gwg::PrepArgs a;
+  a.n = n;
+  a.np = e->np;
+  a.t = int32_t(t);
+  a.lambda = e->lambda.d();
+  a.y = y_rot;
+  a.ldy = n;
+  a.xl = e->xl_rot.d();
+  a.ldxl = n;
+  a.h2 = e->h2.d();
+  a.sigma2 = e->sigma2.d();
+  a.bops = e->bops.d();
+  a.ctx = e->ctx.d();
+  a.trait_err = static_cast<unsigned long long*>(e->err.ptr);
+  GWG_CUDA_TRY(e->ops.prep(a, e->comp));
+  e->counters.kernel_launches += 1;
+  e->counters.context_builds += 1;
+  const uint64_t pm1 = uint64_t(e->p - 1);
+  e->counters.loop_flops += uint64_t(t) * uint64_t(n) * (5 + 3 * pm1 + pm1 * pm1);
+  if (int rc = read_errors(e, st, true)) return rc;
+  if (e->err_host[0] != ~0ull) {
+    const int64_t j = int64_t(e->err_host[0]);
+    return set_status(st, GWG_NOT_POSITIVE_DEFINITE, -1, j,
+                      "trait covariance is not positive definite in the rotated basis: a "
+                      "weight entry is below the relative floor (trait %lld)",
+                      (long long)j);
+  }
+  e->t = t;
+  e->have_traits = true;
+  return GWG_OK;
+}
+
+int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* x_r,
+                           int32_t where, int32_t is_rotated, double* b_out, int32_t out_where,
+                           int32_t layout, int64_t ldo, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!e->have_traits)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_traits must come first");
+  if (mb < 1 || i0 < 0 || !x_r || !b_out)
+    return set_status(st, GWG_DIMENSION, -1, -1, "bad slab arguments (i0=%lld mb=%lld)",
+                      (long long)i0, (long long)mb);
+  if (layout != GWG_LAYOUT_NUMPY && layout != GWG_LAYOUT_STREAM)
+    return set_status(st, GWG_DIMENSION, -1, -1, "unknown layout %d", layout);
+  if (layout == GWG_LAYOUT_STREAM && ldo < mb)
+    return set_status(st, GWG_DIMENSION, -1, -1, "ldo (%lld) < mb (%lld)", (long long)ldo,
+                      (long long)mb);
+  const int64_t n = e->n, t = e->t, p = e->p;
+  if (layout == GWG_LAYOUT_NUMPY) ldo = mb;
+  // Rotated slab in the kernel's layout (ld = np).
+  GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
+  if (is_rotated) {
+    GWG_CUDA_TRY(cudaMemcpy2DAsync(e->rot.ptr, e->np * sizeof(double), x_r, n * sizeof(double),
+                                   n * sizeof(double), mb,
+                                   where == GWG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                       : cudaMemcpyHostToDevice,
+                                   e->comp));
+    if (where != GWG_DEVICE) e->counters.bytes_loaded += uint64_t(n) * mb * 8;
+  } else {
+    const double* src = x_r;
+    if (where != GWG_DEVICE) {
+      if (int rc = upload(e, e->raw[0], x_r, size_t(n) * mb, where, st)) return rc;
+      src = e->raw[0].d();
+    }
+    if (int rc = rotate(e, src, n, mb, e->rot.d(), e->np, st)) return rc;
+  }
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_r1, e->comp));
+  double* dev_out = b_out;
+  const size_t out_cells = layout == GWG_LAYOUT_NUMPY ? size_t(mb) * t : size_t(ldo) * t;
+  if (out_where != GWG_DEVICE) {
+    GWG_CUDA_TRY(e->out[0].ensure(size_t(mb) * t * p * sizeof(double)));
+    dev_out = e->out[0].d();
+  }
+  (void)out_cells;
+  const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
+  const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : (out_where == GWG_DEVICE ? ldo : mb);
+  if (int rc = reset_errors(e, st)) return rc;
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
+  if (int rc = launch_slab(e, e->rot.d(), mb, i0, std::max<int64_t>(i0 + mb, 1), dev_out, si,
+                           sj, st))
+    return rc;
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_k1, e->comp));
+  if (out_where != GWG_DEVICE) {
+    if (layout == GWG_LAYOUT_NUMPY) {
+      GWG_CUDA_TRY(cudaMemcpyAsync(b_out, dev_out, size_t(mb) * t * p * sizeof(double),
+                                   cudaMemcpyDeviceToHost, e->comp));
+    } else {
+      GWG_CUDA_TRY(cudaMemcpy2DAsync(b_out, ldo * p * sizeof(double), dev_out,
+                                     mb * p * sizeof(double), mb * p * sizeof(double), t,
+                                     cudaMemcpyDeviceToHost, e->comp));
+    }
+    e->counters.bytes_stored += uint64_t(mb) * t * p * 8;
+  }
+  if (int rc = read_errors(e, st, false)) return rc;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
+  if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
+  // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
+  return raise_cell_error(e, std::max<int64_t>(i0 + mb, 1), st);
+}
+
+int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
+                     const gwg_run_options* opts, gwg_counters* counters, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!e->have_traits)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_traits must come first");
+  if (m < 1 || !x_r_host || !b_host)
+    return set_status(st, GWG_DIMENSION, -1, -1, "bad run_grid arguments (m=%lld)",
+                      (long long)m);
+  const auto wall0 = std::chrono::steady_clock::now();
+  const int64_t n = e->n, t = e->t, p = e->p;
+  const int layout = opts ? opts->layout : GWG_LAYOUT_NUMPY;
+  if (layout != GWG_LAYOUT_NUMPY && layout != GWG_LAYOUT_STREAM)
+    return set_status(st, GWG_DIMENSION, -1, -1, "unknown layout %d", layout);
+  const bool dbuf = opts ? opts->double_buffer != 0 : true;
+  // Default slab: whole waves of the persistent grid (tiles_m * tiles_t a
+  // multiple of the SM count) and ~64-128 MB of results per slab.
+  int64_t mb = opts && opts->mb > 0 ? opts->mb : 0;
+  if (mb == 0) {
+    const int64_t tiles_t = ceil_div(t, e->ops.bt);
+    const int64_t unit_tiles = e->sms / std::gcd<int64_t>(tiles_t, e->sms);
+    int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
+    const int64_t target = std::max<int64_t>(1, (96ll << 20) / (t * p * 8));
+    mb = std::max<int64_t>(1, target / unit) * unit;
+  }
+  mb = std::min(mb, m);
+  const int nbuf = dbuf ? 2 : 1;
+
+  const bool x_pinned = is_pinned_host(x_r_host);
+  const bool b_pinned = is_pinned_host(b_host);
+  const size_t x_bytes = size_t(n) * m * sizeof(double);
+  const size_t b_bytes = size_t(m) * t * p * sizeof(double);
+  bool x_reg = false, b_reg = false;
+  if (!x_pinned && cudaHostRegister(const_cast<double*>(x_r_host), x_bytes,
+                                    cudaHostRegisterReadOnly) == cudaSuccess)
+    x_reg = true;
+  cudaGetLastError();
+  if (!b_pinned && cudaHostRegister(b_host, b_bytes, cudaHostRegisterDefault) == cudaSuccess)
+    b_reg = true;
+  cudaGetLastError();
+  struct Unreg {
+    const void* x;
+    void* b;
+    ~Unreg() {
+      if (x) cudaHostUnregister(const_cast<void*>(x));
+      if (b) cudaHostUnregister(b);
+    }
+  } unreg{x_reg ? x_r_host : nullptr, b_reg ? b_host : nullptr};
+
+  for (int b = 0; b < nbuf; ++b) {
+    GWG_CUDA_TRY(e->raw[b].ensure(size_t(n) * mb * sizeof(double)));
+    GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
+  }
+  GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  const int64_t slabs = ceil_div(m, mb);
+  while (int64_t(e->slab_events.size()) < 2 * slabs) {
+    cudaEvent_t ev;
+    GWG_CUDA_TRY(cudaEventCreate(&ev));
+    e->slab_events.push_back(ev);
+  }
+  if (int rc = reset_errors(e, st)) return rc;
+  // Fresh pipeline: make the side streams wait for everything already queued.
+  for (int b = 0; b < 2; ++b) {
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], e->comp));
+  }
+  for (int64_t s = 0; s < slabs; ++s) {
+    const int b = int(s % nbuf);
+    const int64_t i0 = s * mb;
+    const int64_t rows = std::min(mb, m - i0);
+    // H2D of the raw slab once the rotation of slab s - nbuf released raw[b].
+    cudaStream_t up = dbuf ? e->h2d : e->comp;
+    cudaStream_t down = dbuf ? e->d2h : e->comp;
+    GWG_CUDA_TRY(cudaStreamWaitEvent(up, e->ev_rot_done[b], 0));
+    GWG_CUDA_TRY(cudaMemcpyAsync(e->raw[b].ptr, x_r_host + size_t(i0) * n,
+                                 size_t(rows) * n * sizeof(double), cudaMemcpyHostToDevice, up));
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_h2d[b], up));
+    e->counters.bytes_loaded += uint64_t(rows) * n * 8;
+    // Compute: rotate + fused grid once the slab landed and out[b] drained.
+    GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
+    GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
+    if (int rc = rotate(e, e->raw[b].d(), n, rows, e->rot.d(), e->np, st)) return rc;
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
+    GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
+    const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
+    const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : rows;
+    if (int rc = launch_slab(e, e->rot.d(), rows, i0, m, e->out[b].d(), si, sj, st)) return rc;
+    GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s + 1], e->comp));
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_comp[b], e->comp));
+    // D2H of the slab's results.
+    GWG_CUDA_TRY(cudaStreamWaitEvent(down, e->ev_comp[b], 0));
+    if (layout == GWG_LAYOUT_NUMPY) {
+      GWG_CUDA_TRY(cudaMemcpyAsync(b_host + size_t(i0) * t * p, e->out[b].ptr,
+                                   size_t(rows) * t * p * sizeof(double),
+                                   cudaMemcpyDeviceToHost, down));
+    } else {
+      GWG_CUDA_TRY(cudaMemcpy2DAsync(b_host + size_t(i0) * p, size_t(m) * p * sizeof(double),
+                                     e->out[b].ptr, size_t(rows) * p * sizeof(double),
+                                     size_t(rows) * p * sizeof(double), t,
+                                     cudaMemcpyDeviceToHost, down));
+    }
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], down));
+    e->counters.bytes_stored += uint64_t(rows) * t * p * 8;
+  }
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
+  if (int rc = read_errors(e, st, false)) return rc;
+  for (int64_t s = 0; s < slabs; ++s) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e->slab_events[2 * s], e->slab_events[2 * s + 1]) ==
+        cudaSuccess)
+      e->counters.grid_kernel_ms += ms;
+  }
+  e->counters.wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+  if (counters) *counters = e->counters;
+  return raise_cell_error(e, m, st);
+}
+
+int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out) {
+  if (!e || !out) return GWG_DIMENSION;
+  *out = e->counters;
+  return GWG_OK;
+}
+
+void gwg_reset_counters(gwg_engine* e) {
+  if (e) e->counters = gwg_counters{};
+}
+
+int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
+  return GWG_OK;
+}
+
+void* gwg_compute_stream(gwg_engine* e) { return e ? static_cast<void*>(e->comp) : nullptr; }
+
+}  // extern "C"

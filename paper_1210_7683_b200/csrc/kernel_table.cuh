@@ -1,0 +1,81 @@
+// kernel_table.cuh — per-p kernel instantiation table shared by the
+// kernels_*.cu translation units (split so nvcc compiles them in parallel).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "grid_kernel.cuh"
+#include "trait_prep.cuh"
+
+namespace gwg {
+
+constexpr int kBK = 32;  // k per pipeline stage; n is padded to a multiple of it
+
+// ---------------------------------------------------------------------------
+// Per-p kernel table.  Tile shapes keep p+1 accumulators per cell in
+// registers and 3 smem stages under 227 KB:
+//   p <= 6 : 64 SNPs x 32 traits per CTA, warp tile 32 x 8
+//   p <= 12: 64 x 16, warp tile 16 x 8
+//   p <= 32: 64 x 8,  warp tile 8 x 8
+// ---------------------------------------------------------------------------
+struct KernelOps {
+  int bm = 0, bt = 0, threads = 0;
+  size_t smem = 0;
+  int ctx_stride = 0;
+  cudaError_t (*prep)(const PrepArgs&, cudaStream_t) = nullptr;
+  cudaError_t (*grid)(const CUtensorMap&, const GridArgs&, int, cudaStream_t) = nullptr;
+};
+
+template <class Cfg>
+cudaError_t launch_grid(const CUtensorMap& map, const GridArgs& a, int ctas,
+                        cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gls_grid_kernel<Cfg>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(Cfg::SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gls_grid_kernel<Cfg><<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int P>
+struct CfgFor {
+  static constexpr int stage_bytes(int bm, int bt) { return kBK * (bm + (P + 1) * bt) * 8; }
+  static constexpr int WM_OCT = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
+  static constexpr int WARPS_T = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
+  static constexpr int WARPS_M = 8 / WARPS_T;
+  static constexpr int BM = 8 * WM_OCT * WARPS_M;
+  static constexpr int BT = 8 * WARPS_T;
+  static constexpr int STAGES = 3 * stage_bytes(BM, BT) + 2048 <= 227 * 1024 ? 3 : 2;
+  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, kBK, STAGES>;
+};
+
+template <int P>
+KernelOps make_ops() {
+  using Cfg = typename CfgFor<P>::type;
+  static_assert(Cfg::SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  KernelOps k;
+  k.bm = Cfg::BM;
+  k.bt = Cfg::BT;
+  k.threads = Cfg::THREADS;
+  k.smem = Cfg::SMEM_BYTES;
+  k.ctx_stride = CtxLayout<P>::STRIDE;
+  k.prep = &launch_trait_prep<P, Cfg::BT>;
+  k.grid = &launch_grid<Cfg>;
+  return k;
+}
+
+// One per translation unit (kernels_a.cu / kernels_b.cu / kernels_c.cu).
+bool ops_for_a(int64_t p, KernelOps* out);
+bool ops_for_b(int64_t p, KernelOps* out);
+bool ops_for_c(int64_t p, KernelOps* out);
+
+inline bool ops_for(int64_t p, KernelOps* out) {
+  return ops_for_a(p, out) || ops_for_b(p, out) || ops_for_c(p, out);
+}
+
+}  // namespace gwg

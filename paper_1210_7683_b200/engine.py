@@ -1,0 +1,332 @@
+"""Host-side mirror of the reference gwgrid API over the device engine.
+
+Python face of include/gwgrid_cuda.h.  Names, argument meaning and error
+behaviour follow the reference's Python module (proj/python/bindings.cpp and
+proj/python/gwgrid/__init__.py):
+
+* ``eigendecompose(phi)``          -> eigendecompose_kinship (gls.cpp:16-46), CPU/LAPACK
+* ``solve_grid(kinship, xl, snps, traits, h2, sigma2, ...)``
+                                   -> solve_grid_py (bindings.cpp:115-190)
+* ``solve_cell(phi, xl, xr, y, h2, sigma2)``
+                                   -> solve_partitioned_gls (gls.cpp:162-186)
+* ``Engine``                       -> GridPrecompute + build_trait_contexts +
+                                      compute_tile / run_grid (grid.hpp:81-237)
+
+Everything after the one-off eigendecomposition runs on the B200 through the
+native library; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Any
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DimensionError, InfeasibleBudgetError, NonSymmetricError, raise_for
+
+
+def _is_torch(x: Any) -> bool:
+    return type(x).__module__.split(".")[0] == "torch"
+
+
+class _Operand:
+    """A column-major FP64 operand: host (numpy) or device (torch CUDA)."""
+
+    def __init__(self, x: Any, shape: tuple, name: str):
+        self.keep = None
+        if _is_torch(x):
+            import torch
+
+            if x.dtype != torch.float64:
+                raise DimensionError(f"{name} must be float64, got {x.dtype}")
+            if tuple(x.shape) != tuple(shape):
+                raise DimensionError(f"{name} has shape {tuple(x.shape)}, expected {shape}")
+            if x.dim() == 2 and x.shape[0] > 1 and x.shape[1] > 1 and not (
+                    x.stride(0) == 1 and x.stride(1) == x.shape[0]):
+                x = x.t().contiguous().t()
+            elif x.dim() <= 1 or x.shape[0] <= 1 or x.shape[1] <= 1:
+                x = x.contiguous()
+            self.keep = x
+            self.ptr = x.data_ptr()
+            self.where = nat.GWG_DEVICE if x.is_cuda else nat.GWG_HOST
+        else:
+            a = np.asarray(x, dtype=np.float64)
+            if a.shape != tuple(shape):
+                raise DimensionError(f"{name} has shape {a.shape}, expected {shape}")
+            a = np.asfortranarray(a)
+            self.keep = a
+            self.ptr = a.ctypes.data
+            self.where = nat.GWG_HOST
+
+
+def eigendecompose(phi: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Kinship eigensystem with the reference's contract (gls.cpp:16-46).
+
+    Symmetry gate max|Phi - Phi^T| <= 1e-12 max|Phi|; ascending eigenvalues;
+    each eigenvector's largest-magnitude entry (first on ties) made positive.
+    Runs on the CPU (LAPACK dsyevd via numpy), as the north star keeps it.
+    """
+    phi = np.asarray(phi, dtype=np.float64)
+    if phi.ndim != 2 or phi.shape[0] != phi.shape[1] or phi.shape[0] < 1:
+        raise DimensionError("relatedness matrix must be square and non-empty")
+    scale = float(np.max(np.abs(phi)))
+    asym = float(np.max(np.abs(phi - phi.T)))
+    if asym > 1e-12 * scale:
+        raise NonSymmetricError(
+            f"relatedness matrix is not symmetric: max|A-A'|={asym:g} exceeds "
+            f"1e-12*max|A|={1e-12 * scale:g}")
+    values, basis = np.linalg.eigh(phi, UPLO="L")
+    idx = np.argmax(np.abs(basis), axis=0)
+    signs = np.where(basis[idx, np.arange(basis.shape[1])] < 0.0, -1.0, 1.0)
+    basis = np.asfortranarray(basis * signs)
+    return basis, values
+
+
+class Engine:
+    """One device engine: spectrum + covariates + traits resident in HBM.
+
+    Calls on one Engine must be serialised (one host thread per GPU), like the
+    reference's CT coordinator (grid.cpp:519-552).
+    """
+
+    def __init__(self, n: int, p: int, device: int = 0):
+        self._lib = nat.load()
+        self.n, self.p, self.t = int(n), int(p), 0
+        st = nat.Status()
+        self._h = self._lib.gwg_engine_create(int(device), self.n, self.p, ctypes.byref(st))
+        if not self._h:
+            raise_for(st)
+            raise DimensionError("engine creation failed")
+        self._keep: list = []
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.gwg_engine_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _call(self, fn, *args) -> None:
+        st = nat.Status()
+        rc = fn(self._h, *args, ctypes.byref(st))
+        if rc != nat.GWG_OK:
+            raise_for(st)
+
+    # -- operands ----------------------------------------------------------
+    def set_spectrum(self, basis, values) -> None:
+        b = _Operand(basis, (self.n, self.n), "basis")
+        v = _Operand(values, (self.n,), "values")
+        if b.where != v.where:
+            raise DimensionError("basis and values must live on the same side")
+        self._call(self._lib.gwg_set_spectrum, b.ptr, v.ptr, b.where)
+
+    def set_covariates(self, xl) -> None:
+        if self.p == 1:
+            self._call(self._lib.gwg_set_covariates, None, nat.GWG_HOST)
+            return
+        x = _Operand(xl, (self.n, self.p - 1), "xl")
+        self._call(self._lib.gwg_set_covariates, x.ptr, x.where)
+
+    def set_traits(self, traits, h2, sigma2, rotated: bool = False) -> None:
+        t = int(np.shape(traits)[1]) if np.ndim(traits) == 2 else 1
+        y = _Operand(traits if np.ndim(traits) == 2 else np.reshape(traits, (-1, 1)),
+                     (self.n, t), "traits")
+        h = _Operand(h2, (t,), "h2")
+        s = _Operand(sigma2, (t,), "sigma2")
+        if not (y.where == h.where == s.where):
+            raise DimensionError("traits, h2 and sigma2 must live on the same side")
+        self._call(self._lib.gwg_set_traits, t, y.ptr, h.ptr, s.ptr, y.where, int(rotated))
+        self.t = t
+
+    # -- grid --------------------------------------------------------------
+    def solve_snp_slab(self, x_r, out=None, i0: int = 0, rotated: bool = False,
+                       layout: str = "numpy"):
+        """compute_tile for one SNP slab against every installed trait.
+
+        Returns ``out``: (mb, t, p) for layout "numpy"; (t, mb, p) for
+        "stream" (the GWG1 result order (j*m + i)*p).  A torch CUDA ``out``
+        keeps the results on the device.
+        """
+        mb = int(np.shape(x_r)[1])
+        x = _Operand(x_r, (self.n, mb), "snps")
+        lay = nat.GWG_LAYOUT_NUMPY if layout == "numpy" else nat.GWG_LAYOUT_STREAM
+        shape = (mb, self.t, self.p) if lay == nat.GWG_LAYOUT_NUMPY else (self.t, mb, self.p)
+        if out is None:
+            out = np.empty(shape, dtype=np.float64)
+        if _is_torch(out):
+            if tuple(out.shape) != shape or not out.is_contiguous():
+                raise DimensionError(f"out must be a contiguous tensor of shape {shape}")
+            optr, owhere = out.data_ptr(), nat.GWG_DEVICE if out.is_cuda else nat.GWG_HOST
+        else:
+            if out.shape != shape or not out.flags.c_contiguous or out.dtype != np.float64:
+                raise DimensionError(f"out must be a C-contiguous float64 array of shape {shape}")
+            optr, owhere = out.ctypes.data, nat.GWG_HOST
+        self._call(self._lib.gwg_solve_snp_slab, int(i0), mb, x.ptr, x.where, int(rotated),
+                   optr, owhere, lay, mb)
+        return out
+
+    def run_grid(self, snps, out=None, layout: str = "numpy", mb: int = 0,
+                 double_buffer: bool = True):
+        """Stream the whole grid from host memory (run_grid, grid.cpp:454-641)."""
+        snps = np.asfortranarray(np.asarray(snps, dtype=np.float64))
+        if snps.ndim != 2 or snps.shape[0] != self.n:
+            raise DimensionError(f"snps must be (n={self.n}, m), got {snps.shape}")
+        m = snps.shape[1]
+        lay = nat.GWG_LAYOUT_NUMPY if layout == "numpy" else nat.GWG_LAYOUT_STREAM
+        shape = (m, self.t, self.p) if lay == nat.GWG_LAYOUT_NUMPY else (self.t, m, self.p)
+        if out is None:
+            out = np.empty(shape, dtype=np.float64)
+        if out.shape != shape or not out.flags.c_contiguous or out.dtype != np.float64:
+            raise DimensionError(f"out must be a C-contiguous float64 array of shape {shape}")
+        opts = nat.RunOptions(int(mb), lay, int(bool(double_buffer)))
+        cnt = nat.Counters()
+        st = nat.Status()
+        rc = self._lib.gwg_run_grid(self._h, m, snps.ctypes.data, out.ctypes.data,
+                                    ctypes.byref(opts), ctypes.byref(cnt), ctypes.byref(st))
+        if rc != nat.GWG_OK:
+            raise_for(st)
+        return out
+
+    def counters(self) -> dict:
+        c = nat.Counters()
+        self._lib.gwg_get_counters(self._h, ctypes.byref(c))
+        return c.as_dict()
+
+    def reset_counters(self) -> None:
+        self._lib.gwg_reset_counters(self._h)
+
+    def synchronize(self) -> None:
+        self._call(self._lib.gwg_synchronize)
+
+    @property
+    def compute_stream(self) -> int:
+        return int(self._lib.gwg_compute_stream(self._h) or 0)
+
+
+def _dims_of(kinship, xl, snps, traits, h2, sigma2):
+    """ProblemDims checks of bindings.cpp:100-113 + types.cpp:7-17."""
+    kinship = np.asarray(kinship, dtype=np.float64)
+    xl = np.asarray(xl, dtype=np.float64)
+    snps = np.asarray(snps, dtype=np.float64)
+    traits = np.asarray(traits, dtype=np.float64)
+    h2 = np.asarray(h2, dtype=np.float64).reshape(-1)
+    sigma2 = np.asarray(sigma2, dtype=np.float64).reshape(-1)
+    if xl.ndim == 1:
+        xl = xl.reshape(-1, 1)
+    n = kinship.shape[0]
+    p = xl.shape[1] + 1
+    m, t = snps.shape[1], traits.shape[1]
+    if kinship.ndim != 2 or kinship.shape[1] != n or xl.shape[0] != n or snps.shape[0] != n \
+            or traits.shape[0] != n:
+        raise DimensionError("operand row counts disagree")
+    if h2.shape[0] != t or sigma2.shape[0] != t:
+        raise DimensionError("h2 and sigma2 must have one entry per trait")
+    if n < 1:
+        raise DimensionError(f"n must be >= 1, got {n}")
+    if p > n:
+        raise DimensionError(f"p ({p}) must not exceed n ({n}): each cell system is p x p "
+                             "built from n samples")
+    if m < 1:
+        raise DimensionError(f"m must be >= 1, got {m}")
+    if t < 1:
+        raise DimensionError(f"t must be >= 1, got {t}")
+    return kinship, xl, snps, traits, h2, sigma2, (n, p, m, t)
+
+
+def device_working_set_bytes(n: int, p: int, t: int, mb: int) -> int:
+    """Resident HBM bytes of a run_grid with mb-column slabs (the device
+    analogue of working_set_bytes, grid.cpp:279-297): spectrum, covariates,
+    trait operands + contexts, two raw slabs, one rotated slab, two result
+    slabs."""
+    np_ = -(-n // 32) * 32
+    fixed = (n * n + n) * 8 + 2 * n * max(p - 1, 1) * 8
+    traits = (2 * n * t + 2 * t) * 8 + (-(-t // 8) * 8) * np_ * (p + 1) * 8 + t * (2 * p + p * p // 2) * 8
+    per_snp = (2 * n + np_) * 8 + 2 * t * p * 8
+    return fixed + traits + mb * per_snp
+
+
+def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,
+               nb: int = 0, mb: int = 0, tb: int = 0, mbb: int = 0, tbb: int = 0,
+               double_buffer: bool = True, memory_budget: int | None = None,
+               device: int = 0) -> dict:
+    """Solve the whole m x t grid; returns {'b': (m, t, p), 'counters': dict}.
+
+    Same signature and semantics as gwgrid.solve_grid (bindings.cpp:115-190,
+    318-328).  ``scheduler``/``workers``/``nb``/``tb``/``mbb``/``tbb`` are the
+    reference's CPU tiling knobs: they are validated with the reference's
+    rules (grid.cpp:64-77) and have no effect on the result, which is bitwise
+    independent of tiling here as well.  ``mb`` is the streamed SNP slab
+    width.  ``memory_budget`` bounds the device working set.
+    """
+    kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
+        kinship, xl, snps, traits, h2, sigma2)
+    if scheduler not in ("ct", "it", "naive"):
+        raise DimensionError("scheduler must be ct, it, or naive")
+    for name, val, hi in (("nb", nb, m), ("mb", mb, m), ("tb", tb, t)):
+        if val and not 1 <= val <= hi:
+            raise DimensionError(f"tile parameter {name} out of range (got {val})")
+    if mbb and not 1 <= mbb <= (mb or m):
+        raise DimensionError(f"tile parameter mbb (must be in [1, mb]) out of range (got {mbb})")
+    if tbb and not 1 <= tbb <= (tb or t):
+        raise DimensionError(f"tile parameter tbb (must be in [1, tb]) out of range (got {tbb})")
+    if memory_budget is not None:
+        need1 = device_working_set_bytes(n, p, t, 1)
+        if need1 > memory_budget:
+            raise InfeasibleBudgetError(
+                f"memory budget of {memory_budget} bytes cannot hold even a 1-column slab "
+                f"(working set {need1} bytes)")
+        if not mb:
+            per = device_working_set_bytes(n, p, t, 2) - device_working_set_bytes(n, p, t, 1)
+            mb = max(1, min(m, (memory_budget - device_working_set_bytes(n, p, t, 0)) // per))
+        elif device_working_set_bytes(n, p, t, mb) > memory_budget:
+            raise InfeasibleBudgetError(
+                f"working set of {device_working_set_bytes(n, p, t, mb)} bytes exceeds the "
+                f"memory budget of {memory_budget} bytes")
+    basis, values = eigendecompose(kinship)
+    with Engine(n, p, device) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(xl)
+        eng.set_traits(traits, h2, sigma2)
+        b = np.empty((m, t, p), dtype=np.float64)
+        eng.run_grid(snps, b, mb=mb, double_buffer=double_buffer)
+        c = eng.counters()
+    counters = {
+        "preloop_flops": int(c["preloop_flops"]),
+        "loop_flops": int(c["loop_flops"]),
+        "loop_transform_flops": 0,
+        "context_builds": int(c["context_builds"]),
+        "bytes_loaded": int(c["bytes_loaded"]),
+        "bytes_stored": int(c["bytes_stored"]),
+        "io_stall_seconds": 0.0,
+        "loops_wall_seconds": c["wall_ms"] * 1e-3,
+        "preloop_wall_seconds": 0.0,
+        "stall_fraction": 0.0,
+        "grid_flops": int(c["grid_flops"]),
+        "grid_kernel_seconds": c["grid_kernel_ms"] * 1e-3,
+        "kernel_launches": int(c["kernel_launches"]),
+    }
+    return {"b": b, "counters": counters}
+
+
+def solve_cell(phi, xl, xr, y, h2: float, sigma2: float, device: int = 0) -> np.ndarray:
+    """One fit via the eigendecomposition route (gwgrid.solve_cell,
+    bindings.cpp:293-305), computed by the device engine."""
+    phi = np.asarray(phi, dtype=np.float64)
+    n = phi.shape[0]
+    xl = np.asarray(xl, dtype=np.float64).reshape(n, -1)
+    res = solve_grid(phi, xl, np.asarray(xr, dtype=np.float64).reshape(n, 1),
+                     np.asarray(y, dtype=np.float64).reshape(n, 1), [h2], [sigma2],
+                     device=device)
+    return res["b"][0, 0].copy()
