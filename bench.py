@@ -1,0 +1,389 @@
+"""Benchmark: GLS problems solved/sec on BASELINE.json configs[1] (c1).
+
+c1: n=1000, p=4, m=100,000 SNPs per GPU, t=1,000 traits, FP64, synthetic
+inputs from BASELINE.json's generators (one seed).  A step is one pass of the
+hot path over one batch: rotate Y' = Z^T Y and X_R' = Z^T X_R on the device,
+build every trait context, and solve all m x t cells with the fused grid
+kernel (the eigendecomposition is the one-off CPU preloop, outside the step,
+as in the paper).
+
+  value : inputs already resident in HBM (device pointers through the C ABI)
+  e2e   : the same step through gwg_run_grid / gwg_set_traits with pinned HOST
+          buffers: H2D of X_R and Y and D2H of every b_ij inside the timed region
+  --impl reference : the reference's CPU path (the oracle restatement of
+          gwgrid's compute_tile CT scheduler + OpenBLAS rotation, oracle/) on the
+          host cores, bounded sample of the same workload.
+
+Multi-GPU (torchrun): the SNP axis is sharded (weak scaling: m SNPs per rank);
+Z, lambda, X_L, Y, h2 are broadcast once from rank 0 over NCCL; no data-path
+collective; timing is max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GLS problems solved/sec (m·t/s) at n=1000,p=4; FP64 TFLOP/s vs B200 peak"
+PEAK_FP64_TFLOPS = 37.15  # measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.txt
+PEAK_SOURCE = ("measured: DMMA.8x8x4 issue loop on this pool's B200 at 1965 MHz "
+               "(profiles/r01_fp64_peak.txt; = 148 SM x 128 flop/clk x 1.965 GHz; "
+               "MEASURED_PEAKS.json holds no FP64 figure)")
+SEED = 20261019
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=100_000, help="SNPs per GPU")
+    ap.add_argument("--t", type=int, default=1000)
+    ap.add_argument("--n", type=int, default=1000)
+    ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """Samples SM clock and throttle reasons through NVML (pynvml) on a
+    background thread for the duration of the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+
+    def _run(self):
+        import pynvml
+
+        h = self.handle
+        while not self.stop.is_set():
+            try:
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop.wait(self.period)
+
+    def __enter__(self):
+        import threading
+
+        self.stop = threading.Event()
+        self.thread = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.thread = None
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+
+    def summary(self) -> dict:
+        sm = self.samples
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(args, rank: int, world: int, dev_index: int):
+    """Rank 0 builds the shared operands (kinship eig on the CPU); they are
+    broadcast over NCCL.  Each rank generates its own SNP shard."""
+    import torch
+
+    from paper_1210_7683_b200 import datagen, eigendecompose
+
+    n, p, m, t = args.n, args.p, args.m, args.t
+    dev = torch.device("cuda", dev_index)
+    shared = {}
+    if rank == 0:
+        phi = datagen.kinship(SEED, n, 2 * n)
+        t0 = time.perf_counter()
+        basis, values = eigendecompose(phi)
+        shared["eig_s"] = time.perf_counter() - t0
+        shared["basis"] = torch.from_numpy(np.ascontiguousarray(basis.T)).to(dev).t()
+        shared["values"] = torch.from_numpy(values).to(dev)
+        shared["xl"] = torch.from_numpy(np.ascontiguousarray(datagen.covariates(SEED, n, p).T)).to(dev).t()
+        shared["y"] = torch.from_numpy(np.ascontiguousarray(
+            datagen.normals(SEED, datagen.M_TRAITS, n, 0, t).T)).to(dev).t()
+        shared["h2"] = torch.from_numpy(datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95)).to(dev)
+    else:
+        shared["basis"] = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+        shared["values"] = torch.empty(n, dtype=torch.float64, device=dev)
+        shared["xl"] = torch.empty((p - 1, n), dtype=torch.float64, device=dev).t()
+        shared["y"] = torch.empty((t, n), dtype=torch.float64, device=dev).t()
+        shared["h2"] = torch.empty(t, dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        for key in ("basis", "values", "xl", "y", "h2"):
+            buf = shared[key]
+            base = buf.t() if buf.dim() == 2 else buf
+            dist.broadcast(base, src=0)
+    shared["sigma2"] = torch.ones(t, dtype=torch.float64, device=dev)
+    # this rank's SNP shard: global columns [rank*m, (rank+1)*m), pinned host
+    x_host = torch.empty((m, n), dtype=torch.float64).pin_memory()
+    xh = x_host.numpy().T  # (n, m) column-major view
+    datagen.genotypes(SEED, datagen.M_SNPS, n, rank * m, m, out=xh)
+    return shared, x_host, xh
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1210_7683_b200 as gw
+
+    world, rank, local = dist_setup(args.gpus)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    n, p, m, t = args.n, args.p, args.m, args.t
+    shared, x_host_t, x_host = make_inputs(args, rank, world, local)
+    dev = torch.device("cuda", local)
+
+    eng = gw.Engine(n, p, device=local)
+    eng.set_spectrum(shared["basis"], shared["values"])
+    eng.set_covariates(shared["xl"])
+    x_dev = x_host_t.to(dev, non_blocking=False).t()  # (n, m) column-major on device
+    b_dev = torch.empty((m, t, p), dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
+
+    def step():
+        eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
+        eng.solve_snp_slab(x_dev, out=b_dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    eng.reset_counters()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    cnt = eng.counters()
+    ms_max = ms_total
+    if world > 1:
+        import torch.distributed as dist
+
+        tm = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms_max = float(tm.item())
+    ms_step = ms_max / args.steps
+    cells = m * t * world
+    value = cells / (ms_step * 1e-3)
+    grid_flops_step = m * t * 2 * n * (p + 1)
+    kernel_ms = cnt["grid_kernel_ms"] / args.steps
+    achieved = grid_flops_step / (kernel_ms * 1e-3) / 1e12
+    rotate_ms = cnt["rotate_ms"] / args.steps
+
+    # sanity: no NaN, finite results
+    bad = int(torch.isnan(b_dev).sum().item())
+
+    # ---- e2e through gwg_run_grid with pinned host buffers ------------------
+    e2e = None
+    if not args.no_e2e:
+        b_host_t = torch.empty((m, t, p), dtype=torch.float64).pin_memory()
+        b_host = b_host_t.numpy()
+        y_host_t = torch.empty((t, n), dtype=torch.float64).pin_memory()
+        y_host_t.copy_(shared["y"].t())
+        y_host = y_host_t.numpy().T
+        h2_host = shared["h2"].cpu().numpy()
+        s2_host = np.ones(t)
+
+        def e2e_step():
+            eng.set_traits(y_host, h2_host, s2_host)
+            eng.run_grid(x_host, out=b_host)
+
+        for _ in range(max(1, args.warmup - 1)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+
+            tm = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            e2e_s = float(tm.item())
+        # the e2e results must equal the device-resident ones bitwise
+        same = bool(np.array_equal(b_host, b_dev.cpu().numpy()))
+        e2e = {"value": cells * args.steps / e2e_s, "unit": "GLS/s",
+               "h2d_bytes_per_step": n * m * 8 + n * t * 8 + 2 * t * 8,
+               "d2h_bytes_per_step": m * t * p * 8, "ms_per_step": 1e3 * e2e_s / args.steps,
+               "bitwise_equal_to_device_path": same}
+
+    # ---- CPU baseline: the oracle (reference restatement) on the host --------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, shared, x_host)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GLS/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE.json generators, seed %d)" % SEED,
+            "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": m, "t": t,
+                       "cells_per_step": cells, "parallelism": f"snp-shard x{world}",
+                       "l2": "inputs larger than L2 (X_R %.1f GB per GPU per step)" % (n * m * 8 / 1e9),
+                       "step": "rotate Y and X_R (own DMMA rotation kernel) + trait contexts + fused grid kernel"},
+            "tflops": grid_flops_step * world / (ms_step * 1e-3) / 1e12,
+            "tflops_convention": "2n(p+1) per cell (grid contraction); reference n(2p+3) = %.3f TF"
+                                 % (m * t * n * (2 * p + 3) * world / (ms_step * 1e-3) / 1e12),
+            "gpu_launches": int(cnt["kernel_launches"]),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
+                         "traffic": load_traffic(), "kernel": "gls_grid_kernel<P=4>",
+                         "kernel_ms": kernel_ms, "rotate_ms": rotate_ms,
+                         "peak_source": PEAK_SOURCE,
+                         "algorithmic_flops_per_launch": grid_flops_step},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "nan_cells": bad,
+            "preloop_eig_s": shared.get("eig_s"),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "r01_grid_kernel_ncu.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample_run(args, basis, values, xl, y, h2, x_sample, workers):
+    """The reference CPU step on a sample: OpenBLAS rotations + contexts +
+    compute_tile (CT, 160x160 blocks, `workers` threads)."""
+    from oracle import oracle as orc
+
+    orc.set_blas_threads(workers)
+    xr = orc.rotate(basis, x_sample)
+    yr = orc.rotate(basis, y)
+    xlr = orc.rotate(basis, xl)
+    return orc.compute_grid(values, xlr, xr, yr, h2, np.ones(len(h2)), workers=workers)
+
+
+def cpu_baseline(args, shared, x_host, sample_m: int | None = None):
+    basis = shared["basis"].cpu().numpy()
+    values = shared["values"].cpu().numpy()
+    xl = shared["xl"].cpu().numpy()
+    y = shared["y"].cpu().numpy()
+    h2 = shared["h2"].cpu().numpy()
+    workers = os.cpu_count() or 1
+    ms = sample_m or int(os.environ.get("GWG_CPU_SAMPLE_M", "100000"))
+    xs = np.asfortranarray(x_host[:, :ms])
+    cpu_sample_run(args, basis, values, xl, y, h2, xs[:, :160], workers)  # warm
+    t0 = time.perf_counter()
+    cpu_sample_run(args, basis, values, xl, y, h2, xs, workers)
+    dt = time.perf_counter() - t0
+    return {"value": ms * args.t / dt, "unit": "GLS/s", "cores": workers, "kind": "port",
+            "sample": f"{ms} SNPs x {args.t} traits of c1 (rotation + contexts + compute_tile CT, "
+                      f"{workers} worker threads, OpenBLAS {workers} threads), {dt:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    from paper_1210_7683_b200 import datagen, eigendecompose
+
+    n, p, t = args.n, args.p, args.t
+    phi = datagen.kinship(SEED, n, 2 * n)
+    basis, values = eigendecompose(phi)
+    xl = datagen.covariates(SEED, n, p)
+    y = datagen.normals(SEED, datagen.M_TRAITS, n, 0, t)
+    h2 = datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95)
+    ms = int(os.environ.get("GWG_CPU_SAMPLE_M", "8000"))
+    xs = datagen.genotypes(SEED, datagen.M_SNPS, n, 0, ms)
+    workers = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample_run(args, basis, values, xl, y, h2, xs[:, :160], workers)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_sample_run(args, basis, values, xl, y, h2, xs, workers)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = ms * t / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GLS/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json generators, seed %d)" % SEED,
+        "config": {"workload": "c1", "n": n, "p": p, "m_sample": ms, "t": t},
+        "cpu_baseline": {"value": value, "unit": "GLS/s", "cores": workers, "kind": "port",
+                         "sample": f"{ms} SNPs x {t} traits of c1 per step (oracle/ restatement "
+                                   "of gwgrid compute_tile CT + OpenBLAS rotation)"},
+        "e2e": {"value": value, "unit": "GLS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference (gwgrid) cannot be built here: Eigen3/CLI11/doctest absent; "
+                "this is the oracle/ C++ restatement of its CPU path",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

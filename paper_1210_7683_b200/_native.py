@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgwgrid_cuda.so")
+LIB_PATH = os.environ.get("GWG_LIB") or os.path.join(_HERE, "libgwgrid_cuda.so")
 
 GWG_OK = 0
 GWG_DIMENSION = 1

@@ -8,7 +8,6 @@
 //   pipeline.hpp:78-137)                     -> gwg_run_grid
 // Rotations are cuBLAS DGEMMs (plain library GEMMs); the per-trait context
 // and the fused grid kernel are this library's own sm_100a kernels.
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -25,6 +24,7 @@
 
 #include "../../include/gwgrid_cuda.h"
 #include "kernel_table.cuh"
+#include "rotate_kernel.cuh"
 
 namespace {
 
@@ -59,14 +59,6 @@ void clear_status(gwg_status* st) {
     if (err_ != cudaSuccess)                                                               \
       return set_status(st, GWG_CUDA, -1, -1, "%s failed: %s (%s:%d)", #expr,              \
                         cudaGetErrorString(err_), __FILE__, __LINE__);                     \
-  } while (0)
-
-#define GWG_BLAS_TRY(expr)                                                                 \
-  do {                                                                                     \
-    cublasStatus_t err_ = (expr);                                                          \
-    if (err_ != CUBLAS_STATUS_SUCCESS)                                                     \
-      return set_status(st, GWG_BACKEND, -1, -1, "%s failed: cublas status %d", #expr,     \
-                        int(err_));                                                        \
   } while (0)
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -132,16 +124,15 @@ struct gwg_engine {
   int64_t n = 0, p = 0, np = 0;
   KernelOps ops;
   cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
-  cublasHandle_t blas = nullptr;
 
-  DevBuf basis, lambda, xl_raw, xl_rot;
+  DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
   bool have_spectrum = false, have_covariates = false;
 
   int64_t t = 0;
   bool have_traits = false;
   DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
 
-  DevBuf raw[2], rot, out[2];
+  DevBuf raw[2], rot, out[2], stage;  // raw: ld np (H2D pitch-copied)
   DevBuf err;  // [0] trait error key, [1] cell error key
   unsigned long long* err_host = nullptr;
 
@@ -174,13 +165,66 @@ int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int wher
   return GWG_OK;
 }
 
-// dst (ld ldc) = Z^T src (n x cols, ld lds)
-int rotate(gwg_engine* e, const double* src, int64_t lds, int64_t cols, double* dst,
-           int64_t ldc, gwg_status* st) {
+// Upload an n x cols column-major operand (leading dimension lds) into dst
+// with leading dimension np (the TMA-aligned layout every kernel reads).
+int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int64_t cols,
+                int where, cudaStream_t s, gwg_status* st, int64_t ldd = 0) {
+  if (ldd == 0) ldd = e->np;
+  GWG_CUDA_TRY(dst.ensure(size_t(ldd) * std::max<int64_t>(cols, 1) * sizeof(double)));
+  if (cols == 0) return GWG_OK;
+  const cudaMemcpyKind kind =
+      where == GWG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (lds == e->n && ldd == e->n) {
+    GWG_CUDA_TRY(cudaMemcpyAsync(dst.ptr, src, size_t(e->n) * cols * sizeof(double), kind, s));
+  } else {
+    GWG_CUDA_TRY(cudaMemcpy2DAsync(dst.ptr, ldd * sizeof(double), src, lds * sizeof(double),
+                                   e->n * sizeof(double), cols, kind, s));
+  }
+  if (where != GWG_DEVICE) e->counters.bytes_loaded += uint64_t(e->n) * cols * 8;
+  return GWG_OK;
+}
+
+int encode_kmajor(CUtensorMap* map, const double* base, int64_t n, int64_t rows, int64_t ld,
+                  int box_rows, gwg_status* st) {
+  auto encode = get_encode();
+  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[2] = {cuuint64_t(n), cuuint64_t(rows)};
+  const cuuint64_t gstride[1] = {cuuint64_t(ld) * sizeof(double)};
+  const cuuint32_t box[2] = {8, cuuint32_t(box_rows)};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim,
+                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return GWG_OK;
+}
+
+// Leading dimension for raw operands: n itself when TMA can address it
+// (row pitch a multiple of 16 bytes), so host slabs move with one flat copy.
+int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
+
+// dst (n x cols, ld np) = Z^T src (n x cols, ld lds) with the deterministic
+// DMMA rotation kernel (rotate_kernel.cuh).
+int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
+           int64_t lds = 0) {
   if (cols <= 0) return GWG_OK;
-  const double one = 1.0, zero = 0.0;
-  GWG_BLAS_TRY(cublasDgemm(e->blas, CUBLAS_OP_T, CUBLAS_OP_N, int(e->n), int(cols), int(e->n),
-                           &one, e->basis.d(), int(e->n), src, int(lds), &zero, dst, int(ldc)));
+  if (lds == 0) lds = e->np;
+  CUtensorMap tz, tx;
+  if (int rc = encode_kmajor(&tz, e->basis.d(), e->n, e->n, e->np, gwg::RotCfg::BM, st)) return rc;
+  if (int rc = encode_kmajor(&tx, src, e->n, cols, lds, gwg::RotCfg::BN, st)) return rc;
+  gwg::RotArgs a;
+  a.dst = dst;
+  a.ldd = e->np;
+  a.n = int32_t(e->n);
+  a.cols = int32_t(cols);
+  a.tiles_m = int32_t(ceil_div(e->n, gwg::RotCfg::BM));
+  a.tiles_n = int32_t(ceil_div(cols, gwg::RotCfg::BN));
+  a.kchunks = int32_t(e->np / gwg::RotCfg::BK);
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
+  GWG_CUDA_TRY(gwg::launch_rotate(tz, tx, a, int(std::min<int64_t>(tiles, e->sms)), e->comp));
+  e->counters.kernel_launches += 1;
   e->counters.preloop_flops += 2ull * uint64_t(e->n) * uint64_t(e->n) * uint64_t(cols);
   return GWG_OK;
 }
@@ -201,19 +245,8 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
 // Grid kernel over one rotated slab (rot: ld np, `rows` SNPs) into dev_out.
 int launch_slab(gwg_engine* e, const double* rot, int64_t rows, int64_t i0, int64_t m_total,
                 double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
-  auto encode = get_encode();
-  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
-  const cuuint64_t gdim[2] = {cuuint64_t(e->n), cuuint64_t(rows)};
-  const cuuint64_t gstride[1] = {cuuint64_t(e->np) * sizeof(double)};
-  const cuuint32_t box[2] = {8, cuuint32_t(e->ops.bm)};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(rot), gdim,
-                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  if (int rc = encode_kmajor(&map, rot, e->n, rows, e->np, e->ops.bm, st)) return rc;
   gwg::GridArgs a;
   a.bops = e->bops.d();
   a.ctx = e->ctx.d();
@@ -263,7 +296,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
                (long long)p);
     return nullptr;
   }
-  if (n > (int64_t(1) << 30)) {
+  if (n > (int64_t(1) << 28)) {
     set_status(st, GWG_DIMENSION, -1, -1, "n too large");
     return nullptr;
   }
@@ -317,13 +350,6 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   cudaEventCreate(&e->ev_k1);
   cudaEventCreate(&e->ev_r0);
   cudaEventCreate(&e->ev_r1);
-  if (cublasCreate(&e->blas) != CUBLAS_STATUS_SUCCESS) {
-    set_status(st, GWG_BACKEND, -1, -1, "cublasCreate failed");
-    gwg_engine_destroy(e);
-    return nullptr;
-  }
-  cublasSetStream(e->blas, e->comp);
-  cublasSetMathMode(e->blas, CUBLAS_PEDANTIC_MATH);  // true FP64, no emulation
   if ((err = e->err.ensure(2 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMalloc", err);
   if ((err = cudaMallocHost(&e->err_host, 2 * sizeof(unsigned long long))) != cudaSuccess)
@@ -339,10 +365,9 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->d2h) cudaStreamSynchronize(e->d2h);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->out[0],
-                    &e->out[1], &e->err})
+                    &e->out[1], &e->stage, &e->err})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
-  if (e->blas) cublasDestroy(e->blas);
   for (int b = 0; b < 2; ++b) {
     if (e->ev_h2d[b]) cudaEventDestroy(e->ev_h2d[b]);
     if (e->ev_rot_done[b]) cudaEventDestroy(e->ev_rot_done[b]);
@@ -363,7 +388,7 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!basis || !lambda) return set_status(st, GWG_DIMENSION, -1, -1, "null spectrum operand");
-  if (int rc = upload(e, e->basis, basis, size_t(e->n) * e->n, where, st)) return rc;
+  if (int rc = upload_cols(e, e->basis, basis, e->n, e->n, where, e->comp, st)) return rc;
   if (int rc = upload(e, e->lambda, lambda, size_t(e->n), where, st)) return rc;
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   e->have_spectrum = true;
@@ -378,11 +403,11 @@ int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_s
   if (!e->have_spectrum)
     return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_spectrum must come first");
   const int64_t pm1 = e->p - 1;
-  GWG_CUDA_TRY(e->xl_rot.ensure(std::max<int64_t>(pm1, 1) * e->n * sizeof(double)));
+  GWG_CUDA_TRY(e->xl_rot.ensure(size_t(e->np) * std::max<int64_t>(pm1, 1) * sizeof(double)));
   if (pm1 > 0) {
     if (!xl) return set_status(st, GWG_DIMENSION, -1, -1, "null covariate block");
-    if (int rc = upload(e, e->xl_raw, xl, size_t(e->n) * pm1, where, st)) return rc;
-    if (int rc = rotate(e, e->xl_raw.d(), e->n, pm1, e->xl_rot.d(), e->n, st)) return rc;
+    if (int rc = upload_cols(e, e->xl_raw, xl, e->n, pm1, where, e->comp, st)) return rc;
+    if (int rc = rotate(e, e->xl_raw.d(), pm1, e->xl_rot.d(), st)) return rc;
   }
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   e->have_covariates = true;
@@ -396,29 +421,18 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   if (int rc = check_engine(e, st)) return rc;
   if (!e->have_covariates)
     return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_covariates must come first");
-  if (t < 1 || t > (int64_t(1) << 31) - 1)
+  if (t < 1 || t > (int64_t(1) << 30))
     return set_status(st, GWG_DIMENSION, -1, -1, "trait count out of range (got %lld)",
                       (long long)t);
   if (!y || !h2 || !sigma2) return set_status(st, GWG_DIMENSION, -1, -1, "null trait operand");
   e->have_traits = false;
   const int64_t n = e->n;
-  const double* y_rot = nullptr;
   if (is_rotated) {
-    if (where == GWG_DEVICE) {
-      y_rot = y;
-    } else {
-      if (int rc = upload(e, e->y_rot, y, size_t(n) * t, where, st)) return rc;
-      y_rot = e->y_rot.d();
-    }
+    if (int rc = upload_cols(e, e->y_rot, y, n, t, where, e->comp, st)) return rc;
   } else {
-    const double* src = y;
-    if (where != GWG_DEVICE) {
-      if (int rc = upload(e, e->y_raw, y, size_t(n) * t, where, st)) return rc;
-      src = e->y_raw.d();
-    }
-    GWG_CUDA_TRY(e->y_rot.ensure(size_t(n) * t * sizeof(double)));
-    if (int rc = rotate(e, src, n, t, e->y_rot.d(), n, st)) return rc;
-    y_rot = e->y_rot.d();
+    if (int rc = upload_cols(e, e->y_raw, y, n, t, where, e->comp, st)) return rc;
+    GWG_CUDA_TRY(e->y_rot.ensure(size_t(e->np) * t * sizeof(double)));
+    if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
   }
   if (int rc = upload(e, e->h2, h2, size_t(t), where, st)) return rc;
   if (int rc = upload(e, e->sigma2, sigma2, size_t(t), where, st)) return rc;
@@ -426,17 +440,21 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
   GWG_CUDA_TRY(e->bops.ensure(bops_doubles * sizeof(double)));
   GWG_CUDA_TRY(e->ctx.ensure(size_t(t) * e->ops.ctx_stride * sizeof(double)));
-  GWG_CUDA_TRY(cudaMemsetAsync(e->bops.ptr, 0, bops_doubles * sizeof(double), e->comp));
+  if (t % e->ops.bt)  // padded traits of the last tile contribute zeros
+    GWG_CUDA_TRY(cudaMemsetAsync(e->bops.d() + size_t(tiles_t - 1) * e->np * (e->p + 1) *
+                                                   e->ops.bt,
+                                 0, size_t(e->np) * (e->p + 1) * e->ops.bt * sizeof(double),
+                                 e->comp));
   if (int rc = reset_errors(e, st)) return rc;
   gwg::PrepArgs a;
   a.n = n;
   a.np = e->np;
   a.t = int32_t(t);
   a.lambda = e->lambda.d();
-  a.y = y_rot;
-  a.ldy = n;
+  a.y = e->y_rot.d();
+  a.ldy = e->np;
   a.xl = e->xl_rot.d();
-  a.ldxl = n;
+  a.ldxl = e->np;
   a.h2 = e->h2.d();
   a.sigma2 = e->sigma2.d();
   a.bops = e->bops.d();
@@ -470,6 +488,8 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   if (mb < 1 || i0 < 0 || !x_r || !b_out)
     return set_status(st, GWG_DIMENSION, -1, -1, "bad slab arguments (i0=%lld mb=%lld)",
                       (long long)i0, (long long)mb);
+  if (mb > (int64_t(1) << 30))
+    return set_status(st, GWG_DIMENSION, -1, -1, "slab too wide (mb=%lld)", (long long)mb);
   if (layout != GWG_LAYOUT_NUMPY && layout != GWG_LAYOUT_STREAM)
     return set_status(st, GWG_DIMENSION, -1, -1, "unknown layout %d", layout);
   if (layout == GWG_LAYOUT_STREAM && ldo < mb)
@@ -477,39 +497,33 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
                       (long long)mb);
   const int64_t n = e->n, t = e->t, p = e->p;
   if (layout == GWG_LAYOUT_NUMPY) ldo = mb;
-  // Rotated slab in the kernel's layout (ld = np).
   GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
   if (is_rotated) {
-    GWG_CUDA_TRY(cudaMemcpy2DAsync(e->rot.ptr, e->np * sizeof(double), x_r, n * sizeof(double),
-                                   n * sizeof(double), mb,
-                                   where == GWG_DEVICE ? cudaMemcpyDeviceToDevice
-                                                       : cudaMemcpyHostToDevice,
-                                   e->comp));
-    if (where != GWG_DEVICE) e->counters.bytes_loaded += uint64_t(n) * mb * 8;
+    if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;
   } else {
     const double* src = x_r;
-    if (where != GWG_DEVICE) {
-      if (int rc = upload(e, e->raw[0], x_r, size_t(n) * mb, where, st)) return rc;
+    const bool direct = where == GWG_DEVICE && raw_ld(e) == n &&
+                        (reinterpret_cast<uintptr_t>(x_r) & 15) == 0;
+    if (!direct) {
+      if (int rc = upload_cols(e, e->raw[0], x_r, n, mb, where, e->comp, st, raw_ld(e)))
+        return rc;
       src = e->raw[0].d();
     }
-    if (int rc = rotate(e, src, n, mb, e->rot.d(), e->np, st)) return rc;
+    if (int rc = rotate(e, src, mb, e->rot.d(), st, raw_ld(e))) return rc;
   }
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r1, e->comp));
   double* dev_out = b_out;
-  const size_t out_cells = layout == GWG_LAYOUT_NUMPY ? size_t(mb) * t : size_t(ldo) * t;
   if (out_where != GWG_DEVICE) {
     GWG_CUDA_TRY(e->out[0].ensure(size_t(mb) * t * p * sizeof(double)));
     dev_out = e->out[0].d();
   }
-  (void)out_cells;
   const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
   const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : (out_where == GWG_DEVICE ? ldo : mb);
+  const int64_t m_total = i0 + mb;
   if (int rc = reset_errors(e, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
-  if (int rc = launch_slab(e, e->rot.d(), mb, i0, std::max<int64_t>(i0 + mb, 1), dev_out, si,
-                           sj, st))
-    return rc;
+  if (int rc = launch_slab(e, e->rot.d(), mb, i0, m_total, dev_out, si, sj, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k1, e->comp));
   if (out_where != GWG_DEVICE) {
     if (layout == GWG_LAYOUT_NUMPY) {
@@ -527,7 +541,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
   if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
   // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
-  return raise_cell_error(e, std::max<int64_t>(i0 + mb, 1), st);
+  return raise_cell_error(e, m_total, st);
 }
 
 int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
@@ -551,7 +565,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
   if (mb == 0) {
     const int64_t tiles_t = ceil_div(t, e->ops.bt);
     const int64_t unit_tiles = e->sms / std::gcd<int64_t>(tiles_t, e->sms);
-    int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
+    const int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
     const int64_t target = std::max<int64_t>(1, (96ll << 20) / (t * p * 8));
     mb = std::max<int64_t>(1, target / unit) * unit;
   }
@@ -580,7 +594,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
   } unreg{x_reg ? x_r_host : nullptr, b_reg ? b_host : nullptr};
 
   for (int b = 0; b < nbuf; ++b) {
-    GWG_CUDA_TRY(e->raw[b].ensure(size_t(n) * mb * sizeof(double)));
+    GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));
     GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
   }
   GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
@@ -600,18 +614,19 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
     const int b = int(s % nbuf);
     const int64_t i0 = s * mb;
     const int64_t rows = std::min(mb, m - i0);
-    // H2D of the raw slab once the rotation of slab s - nbuf released raw[b].
     cudaStream_t up = dbuf ? e->h2d : e->comp;
     cudaStream_t down = dbuf ? e->d2h : e->comp;
+    // H2D of the raw slab (one flat copy for even n) once the rotation of
+    // slab s - nbuf released raw[b].
     GWG_CUDA_TRY(cudaStreamWaitEvent(up, e->ev_rot_done[b], 0));
-    GWG_CUDA_TRY(cudaMemcpyAsync(e->raw[b].ptr, x_r_host + size_t(i0) * n,
-                                 size_t(rows) * n * sizeof(double), cudaMemcpyHostToDevice, up));
+    if (int rc = upload_cols(e, e->raw[b], x_r_host + size_t(i0) * n, n, rows, GWG_HOST, up, st,
+                             raw_ld(e)))
+      return rc;
     GWG_CUDA_TRY(cudaEventRecord(e->ev_h2d[b], up));
-    e->counters.bytes_loaded += uint64_t(rows) * n * 8;
     // Compute: rotate + fused grid once the slab landed and out[b] drained.
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
-    if (int rc = rotate(e, e->raw[b].d(), n, rows, e->rot.d(), e->np, st)) return rc;
+    if (int rc = rotate(e, e->raw[b].d(), rows, e->rot.d(), st, raw_ld(e))) return rc;
     GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
     GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
     const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;

@@ -16,11 +16,13 @@
 // chol(S_TL) and the store of b_ij happen in registers: no m x t intermediate
 // ever reaches HBM.
 //
-// Data path (per CTA, persistent over tiles):
-//   producer warp : TMA 2-D loads of the rotated SNP tile (box 8 k x BM SNPs,
-//                   one per k-octet; zero-filled past n and past m) and one
-//                   1-D bulk copy of the pre-laid-out trait-operand stage,
-//                   STAGES-deep mbarrier ring.
+// Data path (per CTA, persistent over tiles, 8 warps = 2 per SM sub-partition
+// so each thread may hold up to 255 registers):
+//   producer      : thread 0, inside the k loop, issues TMA 2-D loads of the
+//                   rotated SNP tile (box 8 k x BM SNPs, one per k-octet;
+//                   zero-filled past n and past m) and one 1-D bulk copy of the
+//                   pre-laid-out trait-operand stage, STAGES-deep mbarrier ring
+//                   with STAGES-2 stages in flight.
 //   consumer warps: WARPS_M x WARPS_T warps, warp tile (8*WM_OCT SNPs) x
 //                   (8 traits) x (p+1) operand columns; LDS.128 fragment
 //                   loads (each lane's pair of k values is contiguous, so a
@@ -53,7 +55,8 @@ struct CtxLayout {
   __host__ __device__ static constexpr int off_idx(int a, int c) { return a * (a - 1) / 2 + c; }
 };
 
-template <int P_, int WM_OCT_, int WARPS_M_, int WARPS_T_, int BK_, int STAGES_>
+template <int P_, int WM_OCT_, int WARPS_M_, int WARPS_T_, int BK_, int STAGES_,
+          bool PRODUCER_WARP_ = true>
 struct GridCfg {
   static constexpr int P = P_;
   static constexpr int NC = P + 1;  // operand columns per trait
@@ -62,18 +65,25 @@ struct GridCfg {
   static constexpr int WARPS_T = WARPS_T_;
   static constexpr int BK = BK_;
   static constexpr int STAGES = STAGES_;
+  // PRODUCER_WARP: a 9th warp drives the TMA ring (STAGES in flight; 3 warps on
+  // one SM sub-partition caps registers at 168).  Otherwise thread 0 issues
+  // inside the k loop with LOOKAHEAD stages in flight (255 registers).
+  static constexpr bool PRODUCER_WARP = PRODUCER_WARP_;
+  static constexpr int LOOKAHEAD = STAGES - 2;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;
-  static constexpr int CONSUMER_WARPS = WARPS_M * WARPS_T;
-  static constexpr int THREADS = (CONSUMER_WARPS + 1) * 32;
+  static constexpr int WARPS = WARPS_M * WARPS_T;
+  static constexpr int THREADS = (WARPS + (PRODUCER_WARP ? 1 : 0)) * 32;
   static constexpr int A_STAGE = BK * BM;        // doubles
   static constexpr int B_STAGE = BK * NC * BT;   // doubles
   static constexpr uint32_t A_BYTES = A_STAGE * 8;
   static constexpr uint32_t B_BYTES = B_STAGE * 8;
   static constexpr size_t SMEM_BYTES =
-      size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t) + 1024;
+      size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
   static_assert(BK % 8 == 0, "BK must be a multiple of 8");
   static_assert(BM <= 256, "TMA box outer dimension is at most 256");
+  static_assert(PRODUCER_WARP || STAGES >= 3, "the in-loop producer needs one slack stage");
+  static_assert(WARPS == 8, "two consumer warps per SM sub-partition");
 };
 
 struct GridArgs {
@@ -95,8 +105,11 @@ struct GridArgs {
 
 // Bordered Cholesky solve of one cell.  The leading (p-1) block of chol(S) is
 // chol(S_TL) (computed once per trait), so only the last row is per cell:
-//   l = L^-1 s_bl,  pivot = s_br - |l|^2  (fails iff pivot <= 0, like Eigen's
-//   LLT: NaN passes), lambda = sqrt(pivot), then forward/back substitution.
+//   l = L^-1 s_bl            (Eigen LLT's last-row update, divisions by L_aa
+//                             folded into the stored reciprocals)
+//   pivot = s_br - |l|^2     fails iff pivot <= 0, like Eigen's LLT (NaN passes)
+//   beta_B = (b_B - l.z_T) / pivot     (= ((b_B - l.z_T)/lambda)/lambda)
+//   beta_T = L^-T (z_T - l beta_B)
 template <int P>
 __device__ __forceinline__ bool solve_cell(const double* acc, const double* __restrict__ cx,
                                            double* beta) {
@@ -118,8 +131,7 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   }
   const double pivot = acc[P] - sq;
   const bool ok = !(pivot <= 0.0) && __ldg(cx + L::FLAG) == 0.0;
-  const double lam = sqrt(pivot);
-  const double bb = ((acc[P1] - lz) / lam) / lam;
+  const double bb = (acc[P1] - lz) / pivot;
   beta[P1] = bb;
 #pragma unroll
   for (int a = P1 - 1; a >= 0; --a) {
@@ -131,109 +143,132 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   return ok;
 }
 
+// Issue the TMA/bulk loads of global k-iteration g (tile g / kchunks of this
+// CTA's static schedule, k-chunk g % kchunks) into its stage.
+template <class Cfg>
+__device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const GridArgs& args,
+                                            double* sA, double* sB, uint64_t* full,
+                                            uint64_t* empty, int g, int total_iters,
+                                            uint64_t pol_a, uint64_t pol_b) {
+  if (g >= total_iters) return;
+  constexpr int KO = Cfg::BK / 8;
+  const int s = g % Cfg::STAGES;
+  const int use = g / Cfg::STAGES;  // how many times this stage was filled before
+  if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+  const int local_tile = g / args.kchunks;
+  const int kc = g - local_tile * args.kchunks;
+  const int tile = blockIdx.x + local_tile * gridDim.x;
+  const int tm = tile / args.tiles_t;
+  const int tt = tile - tm * args.tiles_t;
+  mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+  double* a_dst = sA + s * Cfg::A_STAGE;
+#pragma unroll
+  for (int ko = 0; ko < KO; ++ko)
+    tma_load_2d(a_dst + ko * Cfg::BM * 8, tmap_a, (kc * KO + ko) * 8, tm * Cfg::BM, &full[s],
+                pol_a);
+  const double* bsrc = args.bops + size_t(tt) * size_t(args.np) * Cfg::NC * Cfg::BT +
+                       size_t(kc) * Cfg::B_STAGE;
+  bulk_load(sB + s * Cfg::B_STAGE, bsrc, Cfg::B_BYTES, &full[s], pol_b);
+}
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     gls_grid_kernel(const __grid_constant__ CUtensorMap tmap_a, const GridArgs args) {
   constexpr int P = Cfg::P;
   constexpr int NC = Cfg::NC;
-  constexpr int P1 = P - 1;
   constexpr int KO = Cfg::BK / 8;  // k-octets per stage
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  double* sA = reinterpret_cast<double*>(base);
+  constexpr int WO = Cfg::WM_OCT;
+  extern __shared__ __align__(1024) double smem[];
+  double* sA = smem;
   double* sB = sA + Cfg::STAGES * Cfg::A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_STAGE);
   uint64_t* empty = full + Cfg::STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int ntiles = args.tiles_m * args.tiles_t;
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total_iters = my_tiles * args.kchunks;
+  const bool producer = Cfg::PRODUCER_WARP ? (warp == Cfg::WARPS && lane == 0)
+                                            : threadIdx.x == 0;
+  uint64_t pol_a = 0, pol_b = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::CONSUMER_WARPS);
+      mbar_init(&empty[s], Cfg::WARPS);
     }
     fence_mbar_init();
   }
+  if (producer) {
+    pol_a = policy_evict_normal();  // SNP tile: re-read by the CTAs of its trait tiles
+    pol_b = policy_evict_last();    // trait operands: L2-resident for the whole launch
+  }
   __syncthreads();
-
-  const int ntiles = args.tiles_m * args.tiles_t;
-
-  if (warp == Cfg::CONSUMER_WARPS) {
-    // ---------------- producer: one elected lane drives the TMA ring ----------
-    if (lane == 0) {
-      const uint64_t keep = policy_evict_last();    // trait operands: L2-resident
-      const uint64_t stream = policy_evict_first();  // SNP tiles: read ~once
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tm = tile / args.tiles_t;
-        const int tt = tile - tm * args.tiles_t;
-        const double* bsrc = args.bops + size_t(tt) * size_t(args.np) * NC * Cfg::BT;
-        for (int kc = 0; kc < args.kchunks; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-          double* a_dst = sA + stage * Cfg::A_STAGE;
-#pragma unroll
-          for (int ko = 0; ko < KO; ++ko)
-            tma_load_2d(a_dst + ko * Cfg::BM * 8, &tmap_a, (kc * KO + ko) * 8, tm * Cfg::BM,
-                        &full[stage], stream);
-          bulk_load(sB + stage * Cfg::B_STAGE, bsrc + size_t(kc) * Cfg::B_STAGE, Cfg::B_BYTES,
-                    &full[stage], keep);
-          if (++stage == Cfg::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
+  if (Cfg::PRODUCER_WARP) {
+    if (warp == Cfg::WARPS) {
+      if (producer)
+        for (int g = 0; g < total_iters; ++g)
+          issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
+      return;
     }
-    return;
+  } else if (producer) {
+    for (int g = 0; g < Cfg::LOOKAHEAD; ++g)
+      issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
   }
 
-  // ---------------- consumers -------------------------------------------------
   const int wm = warp % Cfg::WARPS_M;
   const int wt = warp / Cfg::WARPS_M;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int g = 0;
+  for (int lt = 0; lt < my_tiles; ++lt) {
+    const int tile = blockIdx.x + lt * gridDim.x;
     const int tm = tile / args.tiles_t;
     const int tt = tile - tm * args.tiles_t;
 
-    double acc[Cfg::WM_OCT][NC][2];
+    double acc[WO][NC][2];
 #pragma unroll
-    for (int o = 0; o < Cfg::WM_OCT; ++o)
+    for (int o = 0; o < WO; ++o)
 #pragma unroll
       for (int c = 0; c < NC; ++c) acc[o][c][0] = acc[o][c][1] = 0.0;
 
-    for (int kc = 0; kc < args.kchunks; ++kc) {
-      mbar_wait(&full[stage], phase);
-      const double2* a2 = reinterpret_cast<const double2*>(sA + stage * Cfg::A_STAGE);
-      const double2* b2 = reinterpret_cast<const double2*>(sB + stage * Cfg::B_STAGE);
+    for (int kc = 0; kc < args.kchunks; ++kc, ++g) {
+      // thread 0 keeps LOOKAHEAD stages in flight ahead of this one; the stage it
+      // refills was consumed two iterations ago (one slack stage), so the wait
+      // on its empty barrier almost never blocks.
+      if (!Cfg::PRODUCER_WARP && producer)
+        issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g + Cfg::LOOKAHEAD,
+                         total_iters, pol_a, pol_b);
+      const int s = g % Cfg::STAGES;
+      mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
+      const double2* a2 = reinterpret_cast<const double2*>(sA + s * Cfg::A_STAGE);
+      const double2* b2 = reinterpret_cast<const double2*>(sB + s * Cfg::B_STAGE);
 #pragma unroll
       for (int ko = 0; ko < KO; ++ko) {
-        double2 bf[NC];
+        double2 bf[NC], af[WO], sq[WO];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
           bf[c] = b2[((ko * NC + c) * Cfg::WARPS_T + wt) * 32 + lane];
 #pragma unroll
-        for (int o = 0; o < Cfg::WM_OCT; ++o) {
-          const double2 af = a2[(ko * (Cfg::BM / 8) + wm * Cfg::WM_OCT + o) * 32 + lane];
-          const double sqx = af.x * af.x, sqy = af.y * af.y;
+        for (int o = 0; o < WO; ++o) {
+          af[o] = a2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
+          sq[o] = make_double2(af[o].x * af[o].x, af[o].y * af[o].y);
+        }
+        // even-k pass over every accumulator, then the odd-k pass: dependent
+        // DMMAs on one accumulator are WO*NC instructions apart.
 #pragma unroll
-          for (int c = 0; c < P; ++c) {
-            dmma(acc[o][c], af.x, bf[c].x);
-            dmma(acc[o][c], af.y, bf[c].y);
-          }
-          dmma(acc[o][P], sqx, bf[P].x);
-          dmma(acc[o][P], sqy, bf[P].y);
+        for (int o = 0; o < WO; ++o) {
+#pragma unroll
+          for (int c = 0; c < P; ++c) dmma(acc[o][c], af[o].x, bf[c].x);
+          dmma(acc[o][P], sq[o].x, bf[P].x);
+        }
+#pragma unroll
+        for (int o = 0; o < WO; ++o) {
+#pragma unroll
+          for (int c = 0; c < P; ++c) dmma(acc[o][c], af[o].y, bf[c].y);
+          dmma(acc[o][P], sq[o].y, bf[P].y);
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == Cfg::STAGES) {
-        stage = 0;
-        phase ^= 1;
-      }
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
 
     // ---------------- fused epilogue: bordered Cholesky + store -----------------
@@ -244,8 +279,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       if (j >= args.t) continue;
       const double* cx = args.ctx + size_t(j) * L::STRIDE;
 #pragma unroll
-      for (int o = 0; o < Cfg::WM_OCT; ++o) {
-        const int64_t il = int64_t(tm) * Cfg::BM + (wm * Cfg::WM_OCT + o) * 8 + (lane >> 2);
+      for (int o = 0; o < WO; ++o) {
+        const int64_t il = int64_t(tm) * Cfg::BM + (wm * WO + o) * 8 + (lane >> 2);
         if (il >= args.rows) continue;
         double cell[NC];
 #pragma unroll
@@ -263,7 +298,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int c = 0; c < P; ++c) __stcs(dst + c, beta[c]);
       }
     }
-    (void)P1;
   }
 }
 

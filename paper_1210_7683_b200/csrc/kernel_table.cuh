@@ -10,6 +10,10 @@
 
 namespace gwg {
 
+#ifndef GWG_PRODUCER_WARP
+#define GWG_PRODUCER_WARP true
+#endif
+
 constexpr int kBK = 32;  // k per pipeline stage; n is padded to a multiple of it
 
 // ---------------------------------------------------------------------------
@@ -30,14 +34,10 @@ struct KernelOps {
 template <class Cfg>
 cudaError_t launch_grid(const CUtensorMap& map, const GridArgs& a, int ctas,
                         cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gls_grid_kernel<Cfg>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg::SMEM_BYTES));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(gls_grid_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(Cfg::SMEM_BYTES));
+  if (e != cudaSuccess) return e;
   gls_grid_kernel<Cfg><<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(map, a);
   return cudaGetLastError();
 }
@@ -50,8 +50,8 @@ struct CfgFor {
   static constexpr int WARPS_M = 8 / WARPS_T;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;
-  static constexpr int STAGES = 3 * stage_bytes(BM, BT) + 2048 <= 227 * 1024 ? 3 : 2;
-  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, kBK, STAGES>;
+  static constexpr int STAGES = 4 * stage_bytes(BM, BT) + 64 <= 227 * 1024 ? 4 : 3;
+  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, kBK, STAGES, GWG_PRODUCER_WARP>;
 };
 
 template <int P>
