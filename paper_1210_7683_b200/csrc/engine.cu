@@ -132,7 +132,7 @@ struct gwg_engine {
   bool have_traits = false;
   DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
 
-  DevBuf raw[2], rot, out[2], stage;  // raw: ld np (H2D pitch-copied)
+  DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
   DevBuf err;  // [0] trait error key, [1] cell error key
   unsigned long long* err_host = nullptr;
 
@@ -208,7 +208,7 @@ int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
 // dst (n x cols, ld np) = Z^T src (n x cols, ld lds) with the deterministic
 // DMMA rotation kernel (rotate_kernel.cuh).
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds = 0) {
+           int64_t lds = 0, double* dst_sq = nullptr) {
   if (cols <= 0) return GWG_OK;
   if (lds == 0) lds = e->np;
   CUtensorMap tz, tx;
@@ -216,6 +216,7 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
   if (int rc = encode_kmajor(&tx, src, e->n, cols, lds, gwg::RotCfg::BN, st)) return rc;
   gwg::RotArgs a;
   a.dst = dst;
+  a.dst_sq = dst_sq;
   a.ldd = e->np;
   a.n = int32_t(e->n);
   a.cols = int32_t(cols);
@@ -242,11 +243,13 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
-// Grid kernel over one rotated slab (rot: ld np, `rows` SNPs) into dev_out.
-int launch_slab(gwg_engine* e, const double* rot, int64_t rows, int64_t i0, int64_t m_total,
-                double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
-  CUtensorMap map;
+// Grid kernel over one rotated slab (rot, rot_sq: ld np, `rows` SNPs) into dev_out.
+int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
+                int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
+                gwg_status* st) {
+  CUtensorMap map, map_sq;
   if (int rc = encode_kmajor(&map, rot, e->n, rows, e->np, e->ops.bm, st)) return rc;
+  if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->ops.bm, st)) return rc;
   gwg::GridArgs a;
   a.bops = e->bops.d();
   a.ctx = e->ctx.d();
@@ -259,12 +262,12 @@ int launch_slab(gwg_engine* e, const double* rot, int64_t rows, int64_t i0, int6
   a.t = int32_t(e->t);
   a.tiles_m = int32_t(ceil_div(rows, e->ops.bm));
   a.tiles_t = int32_t(ceil_div(e->t, e->ops.bt));
-  a.kchunks = int32_t(e->np / kBK);
+  a.kchunks = int32_t(e->np / e->ops.bk);
   a.np = e->np;
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_t;
   const int ctas = int(std::min<int64_t>(tiles, e->sms));
-  GWG_CUDA_TRY(e->ops.grid(map, a, ctas, e->comp));
+  GWG_CUDA_TRY(e->ops.grid(map, map_sq, a, ctas, e->comp));
   e->counters.kernel_launches += 1;
   const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
   e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
@@ -364,7 +367,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->h2d) cudaStreamSynchronize(e->h2d);
   if (e->d2h) cudaStreamSynchronize(e->d2h);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
-                    &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->out[0],
+                    &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
@@ -498,9 +501,12 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   const int64_t n = e->n, t = e->t, p = e->p;
   if (layout == GWG_LAYOUT_NUMPY) ldo = mb;
   GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
   if (is_rotated) {
     if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;
+    GWG_CUDA_TRY(gwg::launch_square(e->rot.d(), e->rot_sq.d(), size_t(e->np) * mb, e->comp));
+    e->counters.kernel_launches += 1;
   } else {
     const double* src = x_r;
     const bool direct = where == GWG_DEVICE && raw_ld(e) == n &&
@@ -510,7 +516,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
         return rc;
       src = e->raw[0].d();
     }
-    if (int rc = rotate(e, src, mb, e->rot.d(), st, raw_ld(e))) return rc;
+    if (int rc = rotate(e, src, mb, e->rot.d(), st, raw_ld(e), e->rot_sq.d())) return rc;
   }
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r1, e->comp));
   double* dev_out = b_out;
@@ -523,7 +529,8 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   const int64_t m_total = i0 + mb;
   if (int rc = reset_errors(e, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
-  if (int rc = launch_slab(e, e->rot.d(), mb, i0, m_total, dev_out, si, sj, st)) return rc;
+  if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), mb, i0, m_total, dev_out, si, sj, st))
+    return rc;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k1, e->comp));
   if (out_where != GWG_DEVICE) {
     if (layout == GWG_LAYOUT_NUMPY) {
@@ -598,6 +605,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
     GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
   }
   GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   const int64_t slabs = ceil_div(m, mb);
   while (int64_t(e->slab_events.size()) < 2 * slabs) {
     cudaEvent_t ev;
@@ -626,12 +634,14 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
     // Compute: rotate + fused grid once the slab landed and out[b] drained.
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
-    if (int rc = rotate(e, e->raw[b].d(), rows, e->rot.d(), st, raw_ld(e))) return rc;
+    if (int rc = rotate(e, e->raw[b].d(), rows, e->rot.d(), st, raw_ld(e), e->rot_sq.d()))
+      return rc;
     GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
     GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
     const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
     const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : rows;
-    if (int rc = launch_slab(e, e->rot.d(), rows, i0, m, e->out[b].d(), si, sj, st)) return rc;
+    if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), rows, i0, m, e->out[b].d(), si, sj, st))
+      return rc;
     GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s + 1], e->comp));
     GWG_CUDA_TRY(cudaEventRecord(e->ev_comp[b], e->comp));
     // D2H of the slab's results.

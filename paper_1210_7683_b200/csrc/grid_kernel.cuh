@@ -9,8 +9,10 @@
 //     S_BL[i,j,l] = X'^T (D.X_L'_l)     b_B[i,j] = X'^T (D.Y')
 //     S_BR[i,j]   = (X'.X')^T D
 // i.e. one GEMM with M = SNPs, N = traits x (p+1) operand columns, K = n, run
-// on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4).  X'.X' is formed
-// by squaring the A fragment in registers.  The p+1 accumulators of a cell
+// on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4).  X'.X' comes
+// precomputed from the rotation epilogue (squaring here would repeat the DMULs
+// once per trait tile and steal FP64-pipe cycles from the DMMAs).  The p+1
+// accumulators of a cell
 // land in the same thread (the N axis is ordered component-major inside each
 // 8-trait octet), so the bordered Cholesky solve against the per-trait
 // chol(S_TL) and the store of b_ij happen in registers: no m x t intermediate
@@ -29,7 +31,7 @@
 //                   warp load is 512 contiguous bytes: no bank conflicts).
 //
 // Shared-memory stage layouts (doubles):
-//   A[kc][i][kk]            kc < BK/8, i < BM, kk < 8         (TMA box order)
+//   A[kc][i][kk], then the same for X'.X'   kc < BK/8, i < BM, kk < 8 (TMA box)
 //   B[kc][c][g][jj][kk]     c < p+1, g < BT/8, jj < 8, kk < 8 (panel order)
 // The contraction order over k is fixed (k-octets ascending; within an octet
 // the even k then the odd k; DMMA-internal order within each) and independent
@@ -74,12 +76,13 @@ struct GridCfg {
   static constexpr int BT = 8 * WARPS_T;
   static constexpr int WARPS = WARPS_M * WARPS_T;
   static constexpr int THREADS = (WARPS + (PRODUCER_WARP ? 1 : 0)) * 32;
-  static constexpr int A_STAGE = BK * BM;        // doubles
+  static constexpr int A_STAGE = BK * BM;        // doubles (X' tile; X'.X' tile follows)
   static constexpr int B_STAGE = BK * NC * BT;   // doubles
-  static constexpr uint32_t A_BYTES = A_STAGE * 8;
+  static constexpr uint32_t A_BYTES = 2 * A_STAGE * 8;
   static constexpr uint32_t B_BYTES = B_STAGE * 8;
   static constexpr size_t SMEM_BYTES =
       size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
+  static constexpr int SA_STAGE = 2 * A_STAGE;   // smem doubles per stage for A and A.A
   static_assert(BK % 8 == 0, "BK must be a multiple of 8");
   static_assert(BM <= 256, "TMA box outer dimension is at most 256");
   static_assert(PRODUCER_WARP || STAGES >= 3, "the in-loop producer needs one slack stage");
@@ -146,7 +149,8 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
 // Issue the TMA/bulk loads of global k-iteration g (tile g / kchunks of this
 // CTA's static schedule, k-chunk g % kchunks) into its stage.
 template <class Cfg>
-__device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const GridArgs& args,
+__device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const CUtensorMap* tmap_q,
+                                            const GridArgs& args,
                                             double* sA, double* sB, uint64_t* full,
                                             uint64_t* empty, int g, int total_iters,
                                             uint64_t pol_a, uint64_t pol_b) {
@@ -161,11 +165,14 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const Gri
   const int tm = tile / args.tiles_t;
   const int tt = tile - tm * args.tiles_t;
   mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
-  double* a_dst = sA + s * Cfg::A_STAGE;
+  double* a_dst = sA + s * Cfg::SA_STAGE;
 #pragma unroll
-  for (int ko = 0; ko < KO; ++ko)
+  for (int ko = 0; ko < KO; ++ko) {
     tma_load_2d(a_dst + ko * Cfg::BM * 8, tmap_a, (kc * KO + ko) * 8, tm * Cfg::BM, &full[s],
                 pol_a);
+    tma_load_2d(a_dst + Cfg::A_STAGE + ko * Cfg::BM * 8, tmap_q, (kc * KO + ko) * 8,
+                tm * Cfg::BM, &full[s], pol_a);
+  }
   const double* bsrc = args.bops + size_t(tt) * size_t(args.np) * Cfg::NC * Cfg::BT +
                        size_t(kc) * Cfg::B_STAGE;
   bulk_load(sB + s * Cfg::B_STAGE, bsrc, Cfg::B_BYTES, &full[s], pol_b);
@@ -173,14 +180,15 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const Gri
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
-    gls_grid_kernel(const __grid_constant__ CUtensorMap tmap_a, const GridArgs args) {
+    gls_grid_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_q, const GridArgs args) {
   constexpr int P = Cfg::P;
   constexpr int NC = Cfg::NC;
   constexpr int KO = Cfg::BK / 8;  // k-octets per stage
   constexpr int WO = Cfg::WM_OCT;
   extern __shared__ __align__(1024) double smem[];
   double* sA = smem;
-  double* sB = sA + Cfg::STAGES * Cfg::A_STAGE;
+  double* sB = sA + Cfg::STAGES * Cfg::SA_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_STAGE);
   uint64_t* empty = full + Cfg::STAGES;
 
@@ -208,12 +216,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     if (warp == Cfg::WARPS) {
       if (producer)
         for (int g = 0; g < total_iters; ++g)
-          issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
+          issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
       return;
     }
   } else if (producer) {
     for (int g = 0; g < Cfg::LOOKAHEAD; ++g)
-      issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
+      issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
   }
 
   const int wm = warp % Cfg::WARPS_M;
@@ -235,11 +243,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // refills was consumed two iterations ago (one slack stage), so the wait
       // on its empty barrier almost never blocks.
       if (!Cfg::PRODUCER_WARP && producer)
-        issue_stage<Cfg>(&tmap_a, args, sA, sB, full, empty, g + Cfg::LOOKAHEAD,
+        issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g + Cfg::LOOKAHEAD,
                          total_iters, pol_a, pol_b);
       const int s = g % Cfg::STAGES;
       mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
-      const double2* a2 = reinterpret_cast<const double2*>(sA + s * Cfg::A_STAGE);
+      const double2* a2 = reinterpret_cast<const double2*>(sA + s * Cfg::SA_STAGE);
+      const double2* q2 = a2 + Cfg::A_STAGE / 2;
       const double2* b2 = reinterpret_cast<const double2*>(sB + s * Cfg::B_STAGE);
 #pragma unroll
       for (int ko = 0; ko < KO; ++ko) {
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
         for (int o = 0; o < WO; ++o) {
           af[o] = a2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
-          sq[o] = make_double2(af[o].x * af[o].x, af[o].y * af[o].y);
+          sq[o] = q2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
         }
         // even-k pass over every accumulator, then the odd-k pass: dependent
         // DMMAs on one accumulator are WO*NC instructions apart.

@@ -24,34 +24,39 @@ constexpr int kBK = 32;  // k per pipeline stage; n is padded to a multiple of i
 //   p <= 32: 64 x 8,  warp tile 8 x 8
 // ---------------------------------------------------------------------------
 struct KernelOps {
-  int bm = 0, bt = 0, threads = 0;
+  int bm = 0, bt = 0, bk = 0, threads = 0;
   size_t smem = 0;
   int ctx_stride = 0;
   cudaError_t (*prep)(const PrepArgs&, cudaStream_t) = nullptr;
-  cudaError_t (*grid)(const CUtensorMap&, const GridArgs&, int, cudaStream_t) = nullptr;
+  cudaError_t (*grid)(const CUtensorMap&, const CUtensorMap&, const GridArgs&, int,
+                      cudaStream_t) = nullptr;
 };
 
 template <class Cfg>
-cudaError_t launch_grid(const CUtensorMap& map, const GridArgs& a, int ctas,
-                        cudaStream_t s) {
+cudaError_t launch_grid(const CUtensorMap& map, const CUtensorMap& map_sq, const GridArgs& a,
+                        int ctas, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(gls_grid_kernel<Cfg>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(Cfg::SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  gls_grid_kernel<Cfg><<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(map, a);
+  gls_grid_kernel<Cfg><<<ctas, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(map, map_sq, a);
   return cudaGetLastError();
 }
 
 template <int P>
 struct CfgFor {
-  static constexpr int stage_bytes(int bm, int bt) { return kBK * (bm + (P + 1) * bt) * 8; }
+  static constexpr int LIM = 227 * 1024 - 64;
   static constexpr int WM_OCT = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
   static constexpr int WARPS_T = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
   static constexpr int WARPS_M = 8 / WARPS_T;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;
-  static constexpr int STAGES = 4 * stage_bytes(BM, BT) + 64 <= 227 * 1024 ? 4 : 3;
-  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, kBK, STAGES, GWG_PRODUCER_WARP>;
+  static constexpr int stage_bytes(int bk) { return bk * (2 * BM + (P + 1) * BT) * 8; }
+  // BK = 32 when three stages fit, else 16 with as many stages as fit (<= 6)
+  static constexpr int BK = 3 * stage_bytes(32) <= LIM ? 32 : 16;
+  static constexpr int FIT = LIM / stage_bytes(BK);
+  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, BK, STAGES, GWG_PRODUCER_WARP>;
 };
 
 template <int P>
@@ -61,6 +66,7 @@ KernelOps make_ops() {
   KernelOps k;
   k.bm = Cfg::BM;
   k.bt = Cfg::BT;
+  k.bk = Cfg::BK;
   k.threads = Cfg::THREADS;
   k.smem = Cfg::SMEM_BYTES;
   k.ctx_stride = CtxLayout<P>::STRIDE;

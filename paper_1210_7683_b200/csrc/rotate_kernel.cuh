@@ -16,9 +16,12 @@
 // loaded by TMA 2-D boxes of (8 k x rows) into [k-octet][row][k%8] shared
 // layout and read with conflict-free LDS.128 (each lane's two k values are
 // adjacent).  CTA tile 128 r x 128 i, 8 warps of 32 r x 64 i, persistent
-// static schedule with the same in-loop single-thread producer as the grid
-// kernel.
+// static schedule with an in-loop single-thread producer.  For SNP slabs the
+// epilogue also writes X'.X' (the A operand of S_BR = (X'.X')^T D), so the
+// grid kernel never squares on the FP64 pipe that its DMMAs need.
 #pragma once
+
+#include <algorithm>
 
 #include "gwg_device.cuh"
 
@@ -45,6 +48,7 @@ struct RotCfg {
 
 struct RotArgs {
   double* dst;        // n x cols, leading dimension ldd
+  double* dst_sq;     // optional: elementwise squares of dst (same layout), or null
   int64_t ldd;
   int32_t n;          // rows of dst (= samples)
   int32_t cols;
@@ -156,7 +160,10 @@ __global__ void __launch_bounds__(RotCfg::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = tn * C::BN + (wn * C::WN_OCT + j) * 8 + 2 * (lane & 3) + e;
-          if (col < a.cols) a.dst[int64_t(col) * a.ldd + r] = acc[i][j][e];
+          if (col < a.cols) {
+            a.dst[int64_t(col) * a.ldd + r] = acc[i][j][e];
+            if (a.dst_sq) a.dst_sq[int64_t(col) * a.ldd + r] = acc[i][j][e] * acc[i][j][e];
+          }
         }
       }
     }
@@ -173,6 +180,19 @@ inline cudaError_t launch_rotate(const CUtensorMap& tz, const CUtensorMap& tx, c
                                        int(RotCfg::SMEM_BYTES));
   if (e != cudaSuccess) return e;
   rotate_kernel<<<ctas, RotCfg::THREADS, RotCfg::SMEM_BYTES, s>>>(tz, tx, a);
+  return cudaGetLastError();
+}
+
+// Elementwise squares for slabs that arrive already rotated.
+__global__ void square_kernel(const double* __restrict__ x, double* __restrict__ y, size_t count) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count;
+       i += size_t(gridDim.x) * blockDim.x)
+    y[i] = x[i] * x[i];
+}
+
+inline cudaError_t launch_square(const double* x, double* y, size_t count, cudaStream_t s) {
+  const int blocks = int(std::min<size_t>((count + 255) / 256, 148 * 16));
+  square_kernel<<<blocks, 256, 0, s>>>(x, y, count);
   return cudaGetLastError();
 }
 
