@@ -58,34 +58,41 @@ struct CtxLayout {
 };
 
 template <int P_, int WM_OCT_, int WARPS_M_, int WARPS_T_, int BK_, int STAGES_,
-          bool PRODUCER_WARP_ = true>
+          bool PRODUCER_WARP_ = true, int GROUPS_ = 1>
 struct GridCfg {
   static constexpr int P = P_;
   static constexpr int NC = P + 1;  // operand columns per trait
   static constexpr int WM_OCT = WM_OCT_;
-  static constexpr int WARPS_M = WARPS_M_;
-  static constexpr int WARPS_T = WARPS_T_;
+  static constexpr int WARPS_M = WARPS_M_;  // per consumer group
+  static constexpr int WARPS_T = WARPS_T_;  // per consumer group
   static constexpr int BK = BK_;
-  static constexpr int STAGES = STAGES_;
-  // PRODUCER_WARP: a 9th warp drives the TMA ring (STAGES in flight; 3 warps on
-  // one SM sub-partition caps registers at 168).  Otherwise thread 0 issues
-  // inside the k loop with LOOKAHEAD stages in flight (255 registers).
+  static constexpr int STAGES = STAGES_;    // per consumer group
+  // PRODUCER_WARP: one extra warp per consumer group drives that group's TMA
+  // ring (STAGES in flight).  Otherwise thread 0 issues inside the k loop with
+  // LOOKAHEAD stages in flight.  GROUPS = 2 is the ping-pong schedule: two
+  // consumer groups (one warp of each per SM sub-partition) work on adjacent
+  // trait tiles half a tile out of phase, so one group's epilogue overlaps the
+  // other's DMMA main loop.
   static constexpr bool PRODUCER_WARP = PRODUCER_WARP_;
+  static constexpr int GROUPS = GROUPS_;
   static constexpr int LOOKAHEAD = STAGES - 2;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
-  static constexpr int BT = 8 * WARPS_T;
-  static constexpr int WARPS = WARPS_M * WARPS_T;
-  static constexpr int THREADS = (WARPS + (PRODUCER_WARP ? 1 : 0)) * 32;
+  static constexpr int BT = 8 * WARPS_T;     // traits per group tile
+  static constexpr int GWARPS = WARPS_M * WARPS_T;
+  static constexpr int WARPS = GWARPS * GROUPS;
+  static constexpr int THREADS = (WARPS + (PRODUCER_WARP ? GROUPS : 0)) * 32;
   static constexpr int A_STAGE = BK * BM;        // doubles (X' tile; X'.X' tile follows)
   static constexpr int B_STAGE = BK * NC * BT;   // doubles
   static constexpr uint32_t A_BYTES = 2 * A_STAGE * 8;
   static constexpr uint32_t B_BYTES = B_STAGE * 8;
-  static constexpr size_t SMEM_BYTES =
-      size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
   static constexpr int SA_STAGE = 2 * A_STAGE;   // smem doubles per stage for A and A.A
+  static constexpr size_t SMEM_BYTES =
+      size_t(GROUPS) * (size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t)) +
+      sizeof(uint64_t);
   static_assert(BK % 8 == 0, "BK must be a multiple of 8");
   static_assert(BM <= 256, "TMA box outer dimension is at most 256");
   static_assert(PRODUCER_WARP || STAGES >= 3, "the in-loop producer needs one slack stage");
+  static_assert(PRODUCER_WARP || GROUPS == 1, "ping-pong needs producer warps");
   static_assert(WARPS == 8, "two consumer warps per SM sub-partition");
 };
 
@@ -153,7 +160,7 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const CUt
                                             const GridArgs& args,
                                             double* sA, double* sB, uint64_t* full,
                                             uint64_t* empty, int g, int total_iters,
-                                            uint64_t pol_a, uint64_t pol_b) {
+                                            uint64_t pol_a, uint64_t pol_b, int group = 0) {
   if (g >= total_iters) return;
   constexpr int KO = Cfg::BK / 8;
   const int s = g % Cfg::STAGES;
@@ -161,7 +168,7 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const CUt
   if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
   const int local_tile = g / args.kchunks;
   const int kc = g - local_tile * args.kchunks;
-  const int tile = blockIdx.x + local_tile * gridDim.x;
+  const int tile = (blockIdx.x + local_tile * gridDim.x) * Cfg::GROUPS + group;
   const int tm = tile / args.tiles_t;
   const int tt = tile - tm * args.tiles_t;
   mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
@@ -186,25 +193,43 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   constexpr int NC = Cfg::NC;
   constexpr int KO = Cfg::BK / 8;  // k-octets per stage
   constexpr int WO = Cfg::WM_OCT;
+  constexpr int G = Cfg::GROUPS;
   extern __shared__ __align__(1024) double smem[];
-  double* sA = smem;
-  double* sB = sA + Cfg::STAGES * Cfg::SA_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_STAGE);
-  uint64_t* empty = full + Cfg::STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // consumer warps 0..WARPS-1: group = warp / GWARPS would put a group on two
+  // sub-partitions only; interleave instead so each SM sub-partition (warp % 4)
+  // hosts one warp of every group.
+  const bool is_producer_warp = Cfg::PRODUCER_WARP && warp >= Cfg::WARPS;
+  const int group = is_producer_warp ? warp - Cfg::WARPS : (G == 1 ? 0 : (warp / 4) % G);
+  const int lw = G == 1 ? warp : (warp % 4) + 4 * (warp / (4 * G));  // warp within group
+
+  double* sA = smem + size_t(group) * Cfg::STAGES * (Cfg::SA_STAGE + Cfg::B_STAGE);
+  double* sB = sA + Cfg::STAGES * Cfg::SA_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      smem + size_t(G) * Cfg::STAGES * (Cfg::SA_STAGE + Cfg::B_STAGE));
+  uint64_t* full = bars + group * 2 * Cfg::STAGES;
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* go = bars + G * 2 * Cfg::STAGES;  // ping-pong phase gate
+
   const int ntiles = args.tiles_m * args.tiles_t;
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nsuper = (ntiles + G - 1) / G;
+  const int my_super = blockIdx.x < nsuper ? (nsuper - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // this group's tiles: super tiles whose group-th member exists
+  int my_tiles = my_super;
+  if (my_super > 0 && (blockIdx.x + (my_super - 1) * gridDim.x) * G + group >= ntiles)
+    --my_tiles;
   const int total_iters = my_tiles * args.kchunks;
-  const bool producer = Cfg::PRODUCER_WARP ? (warp == Cfg::WARPS && lane == 0)
-                                            : threadIdx.x == 0;
+  const bool producer = Cfg::PRODUCER_WARP ? (is_producer_warp && lane == 0) : threadIdx.x == 0;
   uint64_t pol_a = 0, pol_b = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::WARPS);
-    }
+    for (int q = 0; q < G * 2 * Cfg::STAGES; q += 2 * Cfg::STAGES)
+      for (int s = 0; s < Cfg::STAGES; ++s) {
+        mbar_init(&bars[q + s], 1);
+        mbar_init(&bars[q + Cfg::STAGES + s], Cfg::GWARPS);
+      }
+    mbar_init(go, 1);
     fence_mbar_init();
   }
   if (producer) {
@@ -213,10 +238,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
   __syncthreads();
   if (Cfg::PRODUCER_WARP) {
-    if (warp == Cfg::WARPS) {
+    if (is_producer_warp) {
       if (producer)
         for (int g = 0; g < total_iters; ++g)
-          issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
+          issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a,
+                           pol_b, group);
       return;
     }
   } else if (producer) {
@@ -224,11 +250,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a, pol_b);
   }
 
-  const int wm = warp % Cfg::WARPS_M;
-  const int wt = warp / Cfg::WARPS_M;
+  const int wm = lw % Cfg::WARPS_M;
+  const int wt = lw / Cfg::WARPS_M;
+  const int half = args.kchunks / 2;
+  if (G > 1 && group > 0 && my_tiles > 0) mbar_wait(go, 0);  // start half a tile late
+  if (G > 1 && group == 0 && lw == 0 && lane == 0 && my_tiles == 0) mbar_arrive(go);
   int g = 0;
   for (int lt = 0; lt < my_tiles; ++lt) {
-    const int tile = blockIdx.x + lt * gridDim.x;
+    const int tile = (blockIdx.x + lt * gridDim.x) * G + group;
     const int tm = tile / args.tiles_t;
     const int tt = tile - tm * args.tiles_t;
 
@@ -239,9 +268,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int c = 0; c < NC; ++c) acc[o][c][0] = acc[o][c][1] = 0.0;
 
     for (int kc = 0; kc < args.kchunks; ++kc, ++g) {
-      // thread 0 keeps LOOKAHEAD stages in flight ahead of this one; the stage it
-      // refills was consumed two iterations ago (one slack stage), so the wait
-      // on its empty barrier almost never blocks.
+      if (G > 1 && group == 0 && lt == 0 && kc == half && lw == 0 && lane == 0) mbar_arrive(go);
+      // (in-loop producer only) thread 0 keeps LOOKAHEAD stages in flight; the
+      // stage it refills was consumed two iterations ago (one slack stage).
       if (!Cfg::PRODUCER_WARP && producer)
         issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g + Cfg::LOOKAHEAD,
                          total_iters, pol_a, pol_b);

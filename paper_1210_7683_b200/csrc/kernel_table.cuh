@@ -43,20 +43,29 @@ cudaError_t launch_grid(const CUtensorMap& map, const CUtensorMap& map_sq, const
   return cudaGetLastError();
 }
 
+#ifndef GWG_PINGPONG
+#define GWG_PINGPONG 1
+#endif
+
 template <int P>
 struct CfgFor {
-  static constexpr int LIM = 227 * 1024 - 64;
+  static constexpr int LIM = 227 * 1024 - 128;
+  // p <= 6 with ping-pong: two 4-warp groups, group tile 64 SNPs x 16 traits
+  static constexpr bool PP = GWG_PINGPONG && GWG_PRODUCER_WARP && P <= 6;
+  static constexpr int GROUPS = PP ? 2 : 1;
   static constexpr int WM_OCT = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
-  static constexpr int WARPS_T = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
-  static constexpr int WARPS_M = 8 / WARPS_T;
+  static constexpr int WARPS_T = PP ? 2 : (P <= 6 ? 4 : (P <= 12 ? 2 : 1));
+  static constexpr int WARPS_M = 8 / GROUPS / WARPS_T;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;
-  static constexpr int stage_bytes(int bk) { return bk * (2 * BM + (P + 1) * BT) * 8; }
-  // BK = 32 when three stages fit, else 16 with as many stages as fit (<= 6)
-  static constexpr int BK = 3 * stage_bytes(32) <= LIM ? 32 : 16;
+  static constexpr int stage_bytes(int bk) { return GROUPS * bk * (2 * BM + (P + 1) * BT) * 8; }
+  static constexpr int MIN_ST = PP ? 2 : 3;
+  // BK = 32 when MIN_ST stages fit, else 16 with as many stages as fit (<= 6)
+  static constexpr int BK = MIN_ST * stage_bytes(32) <= LIM ? 32 : 16;
   static constexpr int FIT = LIM / stage_bytes(BK);
   static constexpr int STAGES = FIT > 6 ? 6 : FIT;
-  using type = GridCfg<P, WM_OCT, WARPS_M, WARPS_T, BK, STAGES, GWG_PRODUCER_WARP>;
+  using type =
+      GridCfg<P, WM_OCT, WARPS_M, WARPS_T, BK, STAGES, GWG_PRODUCER_WARP, GROUPS>;
 };
 
 template <int P>
