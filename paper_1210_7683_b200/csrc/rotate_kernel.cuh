@@ -15,8 +15,8 @@
 // operands are K-contiguous in HBM (Z column r, src column i), so both are
 // loaded by TMA 2-D boxes of (8 k x rows) into [k-octet][row][k%8] shared
 // layout and read with conflict-free LDS.128 (each lane's two k values are
-// adjacent).  CTA tile 128 r x 128 i, 8 warps of 32 r x 64 i, persistent
-// static schedule with an in-loop single-thread producer.  For SNP slabs the
+// adjacent).  CTA tile 128 r x 64 i, 8 warps of 32 r x 32 i plus a TMA
+// producer warp, persistent static schedule.  For SNP slabs the
 // epilogue also writes X'.X' (the A operand of S_BR = (X'.X')^T D), so the
 // grid kernel never squares on the FP64 pipe that its DMMAs need.
 #pragma once
@@ -29,16 +29,15 @@ namespace gwg {
 
 struct RotCfg {
   static constexpr int BM = 128;        // r per CTA
-  static constexpr int BN = 128;        // columns per CTA
+  static constexpr int BN = 64;         // columns per CTA
   static constexpr int WARPS_M = 4;     // warps along r (32 r each)
-  static constexpr int WARPS_N = 2;     // warps along columns (64 each)
+  static constexpr int WARPS_N = 2;     // warps along columns (32 each)
   static constexpr int WM_OCT = 4;      // r octets per warp
-  static constexpr int WN_OCT = 8;      // column octets per warp
+  static constexpr int WN_OCT = 4;      // column octets per warp
   static constexpr int BK = 32;
-  static constexpr int STAGES = 3;
-  static constexpr int LOOKAHEAD = STAGES - 2;
+  static constexpr int STAGES = 4;
   static constexpr int WARPS = WARPS_M * WARPS_N;
-  static constexpr int THREADS = WARPS * 32;
+  static constexpr int THREADS = (WARPS + 1) * 32;  // + one TMA producer warp
   static constexpr int A_STAGE = BK * BM;
   static constexpr int B_STAGE = BK * BN;
   static constexpr uint32_t STAGE_BYTES = (A_STAGE + B_STAGE) * 8;
@@ -96,20 +95,23 @@ __global__ void __launch_bounds__(RotCfg::THREADS, 1)
   const int ntiles = a.tiles_m * a.tiles_n;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int total = my_tiles * a.kchunks;
-  const bool producer = threadIdx.x == 0;
-  uint64_t pol_z = 0, pol_x = 0;
-  if (producer) {
+  if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::WARPS);
     }
     fence_mbar_init();
-    pol_z = policy_evict_last();   // Z: shared by every CTA
-    pol_x = policy_evict_first();  // source columns: read by tiles_m CTAs back to back
-    for (int g = 0; g < C::LOOKAHEAD; ++g)
-      rot_issue(&tmap_z, &tmap_x, a, sA, sB, full, empty, g, total, pol_z, pol_x);
   }
   __syncthreads();
+  if (warp == C::WARPS) {  // producer warp: one lane drives the TMA ring
+    if (lane == 0) {
+      const uint64_t pol_z = policy_evict_last();   // Z: shared by every CTA
+      const uint64_t pol_x = policy_evict_first();  // source columns: read by tiles_m CTAs
+      for (int g = 0; g < total; ++g)
+        rot_issue(&tmap_z, &tmap_x, a, sA, sB, full, empty, g, total, pol_z, pol_x);
+    }
+    return;
+  }
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   int g = 0;
   for (int lt = 0; lt < my_tiles; ++lt) {
@@ -122,9 +124,6 @@ __global__ void __launch_bounds__(RotCfg::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < C::WN_OCT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int kc = 0; kc < a.kchunks; ++kc, ++g) {
-      if (producer)
-        rot_issue(&tmap_z, &tmap_x, a, sA, sB, full, empty, g + C::LOOKAHEAD, total, pol_z,
-                  pol_x);
       const int s = g % C::STAGES;
       mbar_wait(&full[s], (g / C::STAGES) & 1);
       const double2* a2 = reinterpret_cast<const double2*>(sA + s * C::A_STAGE);
