@@ -92,6 +92,20 @@ void gwg_engine_destroy(gwg_engine* e);
 int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambda,
                          int32_t where, gwg_status* st);
 
+/* Device eigendecomposition of the kinship matrix with the reference's
+ * contract (eigendecompose_kinship, gls.cpp:16-46): symmetry gate
+ * max|Phi-Phi^T| <= 1e-12 max|Phi| (else GWG_NON_SYMMETRIC), ascending
+ * eigenvalues, each eigenvector's largest-magnitude entry made positive.
+ * Standalone (no engine): phi n x n col-major on `where`; basis (n x n) and
+ * values (n) written to `out_where`. */
+int32_t gwg_eigendecompose(int32_t device, int64_t n, const double* phi, int32_t where,
+                           double* basis, double* values, int32_t out_where, gwg_status* st);
+
+/* precompute_grid's eigendecomposition on the device (grid.cpp:83-101): the
+ * engine eigendecomposes phi (n x n) in place and installs the spectrum, so
+ * the basis never travels to the host.  Alternative to gwg_set_spectrum. */
+int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_status* st);
+
 /* Install X_L (n x (p-1), col-major, raw) and rotate it on the device:
  * X_L' = Z^T X_L.  Replaces rotate_columns(Z, X_L) inside precompute_grid
  * (grid.cpp:83-101). */

@@ -31,6 +31,8 @@ EXPORTED_SYMBOLS = (
     "gwg_version",
     "gwg_engine_create",
     "gwg_engine_destroy",
+    "gwg_eigendecompose",
+    "gwg_set_kinship",
     "gwg_set_spectrum",
     "gwg_set_covariates",
     "gwg_set_traits",
@@ -102,6 +104,8 @@ def load() -> ctypes.CDLL:
         "gwg_engine_create": (P, [I32, I64, I64, S]),
         "gwg_engine_destroy": (None, [P]),
         "gwg_set_spectrum": (I32, [P, P, P, I32, S]),
+        "gwg_eigendecompose": (I32, [I32, I64, P, I32, P, P, I32, S]),
+        "gwg_set_kinship": (I32, [P, P, I32, S]),
         "gwg_set_covariates": (I32, [P, P, I32, S]),
         "gwg_set_traits": (I32, [P, I64, P, P, P, I32, I32, S]),
         "gwg_solve_snp_slab": (I32, [P, I64, I64, P, I32, I32, P, I32, I32, I64, S]),

@@ -400,6 +400,22 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
   return GWG_OK;
 }
 
+extern "C" int32_t gwg_internal_device_eig(double* a, int64_t n, int64_t lda, double* w,
+                                           cudaStream_t stream, gwg_status* st);
+
+int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!phi) return set_status(st, GWG_DIMENSION, -1, -1, "null kinship matrix");
+  e->have_spectrum = e->have_covariates = e->have_traits = false;
+  if (int rc = upload_cols(e, e->basis, phi, e->n, e->n, where, e->comp, st)) return rc;
+  GWG_CUDA_TRY(e->lambda.ensure(size_t(e->n) * sizeof(double)));
+  if (int rc = gwg_internal_device_eig(e->basis.d(), e->n, e->np, e->lambda.d(), e->comp, st))
+    return rc;
+  e->have_spectrum = true;
+  return GWG_OK;
+}
+
 int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_status* st) {
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;

@@ -60,13 +60,30 @@ class _Operand:
             self.where = nat.GWG_HOST
 
 
-def eigendecompose(phi: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+def eigendecompose(phi: np.ndarray, device: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     """Kinship eigensystem with the reference's contract (gls.cpp:16-46).
 
     Symmetry gate max|Phi - Phi^T| <= 1e-12 max|Phi|; ascending eigenvalues;
     each eigenvector's largest-magnitude entry (first on ties) made positive.
-    Runs on the CPU (LAPACK dsyevd via numpy), as the north star keeps it.
+    By default on the CPU (LAPACK dsyevd via numpy), as the north star keeps
+    it; ``device=k`` runs it on GPU k (cuSOLVER syevd + this library's gate
+    and sign-rule kernels, gwg_eigendecompose).
     """
+    if device is not None:
+        lib = nat.load()
+        a = np.asfortranarray(np.asarray(phi, dtype=np.float64))
+        if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < 1:
+            raise DimensionError("relatedness matrix must be square and non-empty")
+        n = a.shape[0]
+        basis = np.empty((n, n), dtype=np.float64, order="F")
+        values = np.empty(n, dtype=np.float64)
+        st = nat.Status()
+        rc = lib.gwg_eigendecompose(int(device), n, a.ctypes.data, nat.GWG_HOST,
+                                    basis.ctypes.data, values.ctypes.data, nat.GWG_HOST,
+                                    ctypes.byref(st))
+        if rc != nat.GWG_OK:
+            raise_for(st)
+        return basis, values
     phi = np.asarray(phi, dtype=np.float64)
     if phi.ndim != 2 or phi.shape[0] != phi.shape[1] or phi.shape[0] < 1:
         raise DimensionError("relatedness matrix must be square and non-empty")
@@ -131,6 +148,12 @@ class Engine:
         if b.where != v.where:
             raise DimensionError("basis and values must live on the same side")
         self._call(self._lib.gwg_set_spectrum, b.ptr, v.ptr, b.where)
+
+    def set_kinship(self, phi) -> None:
+        """Eigendecompose phi on the device and install the spectrum
+        (gwg_set_kinship; the basis never visits the host)."""
+        k = _Operand(phi, (self.n, self.n), "kinship")
+        self._call(self._lib.gwg_set_kinship, k.ptr, k.where)
 
     def set_covariates(self, xl) -> None:
         if self.p == 1:
@@ -260,7 +283,7 @@ def device_working_set_bytes(n: int, p: int, t: int, mb: int) -> int:
 def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,
                nb: int = 0, mb: int = 0, tb: int = 0, mbb: int = 0, tbb: int = 0,
                double_buffer: bool = True, memory_budget: int | None = None,
-               device: int = 0) -> dict:
+               device: int = 0, device_eig: bool = False) -> dict:
     """Solve the whole m x t grid; returns {'b': (m, t, p), 'counters': dict}.
 
     Same signature and semantics as gwgrid.solve_grid (bindings.cpp:115-190,
@@ -268,7 +291,9 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     reference's CPU tiling knobs: they are validated with the reference's
     rules (grid.cpp:64-77) and have no effect on the result, which is bitwise
     independent of tiling here as well.  ``mb`` is the streamed SNP slab
-    width.  ``memory_budget`` bounds the device working set.
+    width.  ``memory_budget`` bounds the device working set.  ``device_eig``
+    moves the one-off eigendecomposition to the GPU (cuSOLVER); by default it
+    runs on the CPU like the reference.
     """
     kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
         kinship, xl, snps, traits, h2, sigma2)
@@ -294,9 +319,11 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
             raise InfeasibleBudgetError(
                 f"working set of {device_working_set_bytes(n, p, t, mb)} bytes exceeds the "
                 f"memory budget of {memory_budget} bytes")
-    basis, values = eigendecompose(kinship)
     with Engine(n, p, device) as eng:
-        eng.set_spectrum(basis, values)
+        if device_eig:
+            eng.set_kinship(kinship)
+        else:
+            eng.set_spectrum(*eigendecompose(kinship))
         eng.set_covariates(xl)
         eng.set_traits(traits, h2, sigma2)
         b = np.empty((m, t, p), dtype=np.float64)

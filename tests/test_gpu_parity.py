@@ -262,3 +262,36 @@ def test_config1_full_size_properties():
                               ds["sigma2"], ii[:8], jj[:8])
     rel = np.linalg.norm(got[:8] - chol, axis=1) / np.linalg.norm(chol, axis=1)
     assert rel.max() < 1e-10
+
+
+def test_device_eigendecomposition_contract():
+    """gwg_eigendecompose keeps eigendecompose_kinship's contract
+    (gls.cpp:16-46; test_gls.cpp:70-109)."""
+    ds = datagen.generate(300, 3, 2, 2, seed=21)
+    phi = ds["kinship"]
+    z, lam = gw.eigendecompose(phi, device=0)
+    assert np.all(np.diff(lam) >= 0)
+    assert np.abs(z @ np.diag(lam) @ z.T - phi).max() < 1e-12 * np.abs(phi).max() * 10
+    assert np.abs(z.T @ z - np.eye(300)).max() < 1e-12
+    at = np.argmax(np.abs(z), axis=0)
+    assert np.all(z[at, np.arange(300)] > 0)
+    zc, lc = gw.eigendecompose(phi)
+    assert np.abs(lam - lc).max() < 1e-12 * np.abs(lc).max()
+    bad = np.eye(5)
+    bad[1, 3] = 0.5
+    with pytest.raises(gw.NonSymmetricError):
+        gw.eigendecompose(bad, device=0)
+    _, flat = gw.eigendecompose(np.eye(8), device=0)
+    assert np.abs(flat - 1.0).max() < 1e-14
+
+
+def test_device_eig_full_chain_matches_oracle():
+    """solve_grid with the eigendecomposition on the device: b is invariant to
+    the choice of eigenbasis, so it still matches the oracle's CPU chain."""
+    ds = datagen.generate(400, 4, 200, 30, seed=17)
+    res = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                        ds["sigma2"], device_eig=True)
+    ref = orc.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                         ds["sigma2"], workers=8)
+    normwise, floored, _, _ = metrics(res["b"], ref)
+    assert normwise < 1e-10 and floored < 1e-8
