@@ -146,6 +146,33 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
                      const gwg_run_options* opts, gwg_counters* counters,
                      gwg_status* st);
 
+/* ---- GWG1 file legs (proj/include/gwgrid/stream.hpp:15-41) ----------------
+ * 64-byte little-endian header: "GWG1", u16 version 1, u8 kind (1 snp, 2 trait,
+ * 3 result, 4 operand), u8 element type 0 (f64), u64 dims[3], u8 layout 0,
+ * u8 completeness (0 = complete), zero padding; column-major f64 payload;
+ * result cell (i, j) at element (j*m + i)*p.  Readers validate magic,
+ * version, kind, element type, layout, completeness and exact file length
+ * like InputStream::open (stream.cpp:219-257); failures are GWG_IO. */
+
+/* Header of a GWG1 file: kind, dims[3], complete flag (no payload checks). */
+int32_t gwg_stream_info(const char* path, int32_t* kind, int64_t* dims, int32_t* complete,
+                        gwg_status* st);
+
+/* load_pass from a trait stream (kind 2: n x t columns, then h2[t], sigma2[t]);
+ * equivalent to gwg_set_traits on the file's payload. */
+int32_t gwg_set_traits_file(gwg_engine* e, const char* traits_path, gwg_status* st);
+
+/* run_grid over GWG1 files (grid.cpp:454-641): the SNP stream (kind 1, raw, or
+ * rotated when snps_rotated) is read slab by slab by a reader thread into
+ * pinned buffers, solved on the device, and a writer thread stores each slab's
+ * cells into the result stream out_path (kind 3, dims (m, t, p)).  The output
+ * is created incomplete and finalized only when every cell landed and none
+ * failed; a failing cell returns GWG_NOT_POSITIVE_DEFINITE and leaves the file
+ * unreadable, like the reference. */
+int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_rotated,
+                           const char* out_path, const gwg_run_options* opts,
+                           gwg_counters* counters, gwg_status* st);
+
 /* Counters accumulated since the last reset. */
 int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out);
 void gwg_reset_counters(gwg_engine* e);

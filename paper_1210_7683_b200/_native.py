@@ -42,6 +42,9 @@ EXPORTED_SYMBOLS = (
     "gwg_reset_counters",
     "gwg_synchronize",
     "gwg_compute_stream",
+    "gwg_stream_info",
+    "gwg_set_traits_file",
+    "gwg_run_grid_files",
     "gwg_gen_genotypes",
     "gwg_gen_normals",
     "gwg_gen_uniform",
@@ -111,6 +114,11 @@ def load() -> ctypes.CDLL:
         "gwg_solve_snp_slab": (I32, [P, I64, I64, P, I32, I32, P, I32, I32, I64, S]),
         "gwg_run_grid": (I32, [P, I64, P, P, ctypes.POINTER(RunOptions),
                                ctypes.POINTER(Counters), S]),
+        "gwg_stream_info": (I32, [ctypes.c_char_p, ctypes.POINTER(I32), ctypes.POINTER(I64),
+                                  ctypes.POINTER(I32), S]),
+        "gwg_set_traits_file": (I32, [P, ctypes.c_char_p, S]),
+        "gwg_run_grid_files": (I32, [P, ctypes.c_char_p, I32, ctypes.c_char_p,
+                                     ctypes.POINTER(RunOptions), ctypes.POINTER(Counters), S]),
         "gwg_get_counters": (I32, [P, ctypes.POINTER(Counters)]),
         "gwg_reset_counters": (None, [P]),
         "gwg_synchronize": (I32, [P, S]),

@@ -23,10 +23,10 @@
 #include <vector>
 
 #include "../../include/gwgrid_cuda.h"
-#include "kernel_table.cuh"
+#include "engine_internal.cuh"
 #include "rotate_kernel.cuh"
 
-namespace {
+namespace gwg_host {
 
 using gwg::kBK;
 using gwg::KernelOps;
@@ -53,14 +53,6 @@ void clear_status(gwg_status* st) {
   }
 }
 
-#define GWG_CUDA_TRY(expr)                                                                 \
-  do {                                                                                     \
-    cudaError_t err_ = (expr);                                                             \
-    if (err_ != cudaSuccess)                                                               \
-      return set_status(st, GWG_CUDA, -1, -1, "%s failed: %s (%s:%d)", #expr,              \
-                        cudaGetErrorString(err_), __FILE__, __LINE__);                     \
-  } while (0)
-
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -78,35 +70,6 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-struct DevBuf {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t need) {
-    if (need <= bytes) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&ptr, need);
-    if (e == cudaSuccess) bytes = need;
-    return e;
-  }
-  void release() {
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    bytes = 0;
-  }
-  double* d() const { return static_cast<double*>(ptr); }
-};
-
-bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
 bool is_pinned_host(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -115,35 +78,6 @@ bool is_pinned_host(const void* p) {
   }
   return a.type == cudaMemoryTypeHost;
 }
-
-}  // namespace
-
-struct gwg_engine {
-  int device = 0;
-  int sms = 148;
-  int64_t n = 0, p = 0, np = 0;
-  KernelOps ops;
-  cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
-
-  DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
-  bool have_spectrum = false, have_covariates = false;
-
-  int64_t t = 0;
-  bool have_traits = false;
-  DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
-
-  DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
-  DevBuf err;  // [0] trait error key, [1] cell error key
-  unsigned long long* err_host = nullptr;
-
-  cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
-  cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
-  std::vector<cudaEvent_t> slab_events;
-
-  gwg_counters counters{};
-};
-
-namespace {
 
 int check_engine(gwg_engine* e, gwg_status* st) {
   if (!e) return set_status(st, GWG_DIMENSION, -1, -1, "null engine");
@@ -168,7 +102,7 @@ int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int wher
 // Upload an n x cols column-major operand (leading dimension lds) into dst
 // with leading dimension np (the TMA-aligned layout every kernel reads).
 int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int64_t cols,
-                int where, cudaStream_t s, gwg_status* st, int64_t ldd = 0) {
+                int where, cudaStream_t s, gwg_status* st, int64_t ldd) {
   if (ldd == 0) ldd = e->np;
   GWG_CUDA_TRY(dst.ensure(size_t(ldd) * std::max<int64_t>(cols, 1) * sizeof(double)));
   if (cols == 0) return GWG_OK;
@@ -208,7 +142,7 @@ int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
 // dst (n x cols, ld np) = Z^T src (n x cols, ld lds) with the deterministic
 // DMMA rotation kernel (rotate_kernel.cuh).
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds = 0, double* dst_sq = nullptr) {
+           int64_t lds, double* dst_sq) {
   if (cols <= 0) return GWG_OK;
   if (lds == 0) lds = e->np;
   CUtensorMap tz, tx;
@@ -275,6 +209,22 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
   return GWG_OK;
 }
 
+int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st) {
+  GWG_CUDA_TRY(gwg::launch_square(e->rot.d(), e->rot_sq.d(), size_t(e->np) * cols, e->comp));
+  e->counters.kernel_launches += 1;
+  return GWG_OK;
+}
+
+// Default streamed slab: whole waves of the persistent grid kernel
+// (tiles_m * tiles_t a multiple of the SM count) and ~64-128 MB of results.
+int64_t default_slab(const gwg_engine* e, int64_t m) {
+  const int64_t tiles_t = ceil_div(e->t, int64_t(e->ops.bt) * e->ops.groups);
+  const int64_t unit_tiles = e->sms / std::gcd<int64_t>(tiles_t, e->sms);
+  const int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
+  const int64_t target = std::max<int64_t>(1, (96ll << 20) / (e->t * e->p * 8));
+  return std::min(m, std::max<int64_t>(1, target / unit) * unit);
+}
+
 int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
   const unsigned long long key = e->err_host[1];
   if (key == ~0ull) return GWG_OK;
@@ -286,7 +236,9 @@ int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
                     (long long)i, (long long)j);
 }
 
-}  // namespace
+}  // namespace gwg_host
+
+using namespace gwg_host;
 
 extern "C" {
 
@@ -521,8 +473,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
   if (is_rotated) {
     if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;
-    GWG_CUDA_TRY(gwg::launch_square(e->rot.d(), e->rot_sq.d(), size_t(e->np) * mb, e->comp));
-    e->counters.kernel_launches += 1;
+    if (int rc = square_rotated(e, mb, st)) return rc;
   } else {
     const double* src = x_r;
     const bool direct = where == GWG_DEVICE && raw_ld(e) == n &&
@@ -584,15 +535,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
   const bool dbuf = opts ? opts->double_buffer != 0 : true;
   // Default slab: whole waves of the persistent grid (tiles_m * tiles_t a
   // multiple of the SM count) and ~64-128 MB of results per slab.
-  int64_t mb = opts && opts->mb > 0 ? opts->mb : 0;
-  if (mb == 0) {
-    const int64_t tiles_t = ceil_div(t, e->ops.bt);
-    const int64_t unit_tiles = e->sms / std::gcd<int64_t>(tiles_t, e->sms);
-    const int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
-    const int64_t target = std::max<int64_t>(1, (96ll << 20) / (t * p * 8));
-    mb = std::max<int64_t>(1, target / unit) * unit;
-  }
-  mb = std::min(mb, m);
+  const int64_t mb = opts && opts->mb > 0 ? std::min(opts->mb, m) : default_slab(e, m);
   const int nbuf = dbuf ? 2 : 1;
 
   const bool x_pinned = is_pinned_host(x_r_host);

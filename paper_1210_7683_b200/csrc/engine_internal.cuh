@@ -1,0 +1,100 @@
+// engine_internal.cuh — engine state and host helpers shared by engine.cu
+// (in-memory C ABI) and stream_io.cu (GWG1 file legs).  Not installed.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/gwgrid_cuda.h"
+#include "kernel_table.cuh"
+
+#define GWG_CUDA_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cudaError_t err_ = (expr);                                                             \
+    if (err_ != cudaSuccess)                                                               \
+      return gwg_host::set_status(st, GWG_CUDA, -1, -1, "%s failed: %s (%s:%d)", #expr,    \
+                                  cudaGetErrorString(err_), __FILE__, __LINE__);           \
+  } while (0)
+
+namespace gwg_host {
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(ptr); }
+};
+
+
+int set_status(gwg_status* st, int code, int64_t snp, int64_t trait, const char* fmt, ...);
+void clear_status(gwg_status* st);
+int64_t round_up(int64_t a, int64_t b);
+int64_t ceil_div(int64_t a, int64_t b);
+bool is_pinned_host(const void* p);
+
+}  // namespace gwg_host
+
+struct gwg_engine {
+  int device = 0;
+  int sms = 148;
+  int64_t n = 0, p = 0, np = 0;
+  gwg::KernelOps ops;
+  cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
+
+  gwg_host::DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
+  bool have_spectrum = false, have_covariates = false;
+
+  int64_t t = 0;
+  bool have_traits = false;
+  gwg_host::DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
+
+  gwg_host::DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
+  gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key
+  unsigned long long* err_host = nullptr;
+
+  cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
+  cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
+  std::vector<cudaEvent_t> slab_events;
+
+  gwg_counters counters{};
+};
+
+
+namespace gwg_host {
+
+int check_engine(gwg_engine* e, gwg_status* st);
+int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int where,
+           gwg_status* st);
+int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int64_t cols,
+                int where, cudaStream_t s, gwg_status* st, int64_t ldd = 0);
+int64_t raw_ld(const gwg_engine* e);
+int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
+           int64_t lds = 0, double* dst_sq = nullptr);
+int read_errors(gwg_engine* e, gwg_status* st, bool trait_only);
+int reset_errors(gwg_engine* e, gwg_status* st);
+int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
+                int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
+                gwg_status* st);
+int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st);
+// rot_sq <- rot .* rot for `cols` already-rotated columns
+int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st);
+int64_t default_slab(const gwg_engine* e, int64_t m);
+
+}  // namespace gwg_host

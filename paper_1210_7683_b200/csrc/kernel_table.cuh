@@ -24,7 +24,7 @@ constexpr int kBK = 32;  // k per pipeline stage; n is padded to a multiple of i
 //   p <= 32: 64 x 8,  warp tile 8 x 8
 // ---------------------------------------------------------------------------
 struct KernelOps {
-  int bm = 0, bt = 0, bk = 0, threads = 0;
+  int bm = 0, bt = 0, bk = 0, groups = 1, threads = 0;
   size_t smem = 0;
   int ctx_stride = 0;
   cudaError_t (*prep)(const PrepArgs&, cudaStream_t) = nullptr;
@@ -76,6 +76,7 @@ KernelOps make_ops() {
   k.bm = Cfg::BM;
   k.bt = Cfg::BT;
   k.bk = Cfg::BK;
+  k.groups = Cfg::GROUPS;
   k.threads = Cfg::THREADS;
   k.smem = Cfg::SMEM_BYTES;
   k.ctx_stride = CtxLayout<P>::STRIDE;

@@ -18,6 +18,7 @@ native library; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Any
 
 import numpy as np
@@ -221,6 +222,29 @@ class Engine:
         if rc != nat.GWG_OK:
             raise_for(st)
         return out
+
+    def set_traits_file(self, path: str) -> None:
+        """load_pass from a GWG1 trait stream (kind 2)."""
+        self._call(self._lib.gwg_set_traits_file, os.fsencode(path))
+        st = nat.Status()
+        kind, dims, complete = ctypes.c_int32(), (ctypes.c_int64 * 3)(), ctypes.c_int32()
+        self._lib.gwg_stream_info(os.fsencode(path), ctypes.byref(kind), dims,
+                                  ctypes.byref(complete), ctypes.byref(st))
+        self.t = int(dims[1])
+
+    def run_grid_files(self, snps_path: str, out_path: str, rotated: bool = False,
+                       mb: int = 0) -> dict:
+        """run_grid over GWG1 files: SNP stream in, result stream out
+        (gwg_run_grid_files; the output is finalized only on success)."""
+        opts = nat.RunOptions(int(mb), nat.GWG_LAYOUT_STREAM, 1)
+        cnt = nat.Counters()
+        st = nat.Status()
+        rc = self._lib.gwg_run_grid_files(self._h, os.fsencode(snps_path), int(rotated),
+                                          os.fsencode(out_path), ctypes.byref(opts),
+                                          ctypes.byref(cnt), ctypes.byref(st))
+        if rc != nat.GWG_OK:
+            raise_for(st)
+        return cnt.as_dict()
 
     def counters(self) -> dict:
         c = nat.Counters()
