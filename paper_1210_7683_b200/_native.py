@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "gwg_reset_counters",
     "gwg_synchronize",
     "gwg_compute_stream",
+    "gwg_verify_grid",
     "gwg_stream_info",
     "gwg_set_traits_file",
     "gwg_run_grid_files",
@@ -114,6 +115,8 @@ def load() -> ctypes.CDLL:
         "gwg_solve_snp_slab": (I32, [P, I64, I64, P, I32, I32, P, I32, I32, I64, S]),
         "gwg_run_grid": (I32, [P, I64, P, P, ctypes.POINTER(RunOptions),
                                ctypes.POINTER(Counters), S]),
+        "gwg_verify_grid": (I32, [I32, I64, I64, I64, I64, P, P, P, P, P, P, P,
+                                  ctypes.POINTER(D), S]),
         "gwg_stream_info": (I32, [ctypes.c_char_p, ctypes.POINTER(I32), ctypes.POINTER(I64),
                                   ctypes.POINTER(I32), S]),
         "gwg_set_traits_file": (I32, [P, ctypes.c_char_p, S]),

@@ -371,6 +371,29 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     return {"b": b, "counters": counters}
 
 
+def verify_grid(kinship, xl, snps, traits, h2, sigma2, b, device: int = 0) -> float:
+    """Max norm-wise relative error of b against the independent Cholesky
+    route over every cell (gwgrid.verify_grid, bindings.cpp:192-222), computed
+    on the device (gwg_verify_grid)."""
+    kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
+        kinship, xl, snps, traits, h2, sigma2)
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if b.shape != (m, t, p):
+        raise DimensionError("b must have shape (m, t, p)")
+    f = lambda a: np.asfortranarray(a)  # noqa: E731
+    kinship, xl, snps, traits = f(kinship), f(xl), f(snps), f(traits)
+    h2, sigma2 = np.ascontiguousarray(h2), np.ascontiguousarray(sigma2)
+    out = ctypes.c_double(0.0)
+    st = nat.Status()
+    rc = nat.load().gwg_verify_grid(int(device), n, p, m, t, kinship.ctypes.data,
+                                    xl.ctypes.data if p > 1 else None, snps.ctypes.data,
+                                    traits.ctypes.data, h2.ctypes.data, sigma2.ctypes.data,
+                                    b.ctypes.data, ctypes.byref(out), ctypes.byref(st))
+    if rc != nat.GWG_OK:
+        raise_for(st)
+    return float(out.value)
+
+
 def solve_cell(phi, xl, xr, y, h2: float, sigma2: float, device: int = 0) -> np.ndarray:
     """One fit via the eigendecomposition route (gwgrid.solve_cell,
     bindings.cpp:293-305), computed by the device engine."""

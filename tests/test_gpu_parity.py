@@ -295,3 +295,26 @@ def test_device_eig_full_chain_matches_oracle():
                          ds["sigma2"], workers=8)
     normwise, floored, _, _ = metrics(res["b"], ref)
     assert normwise < 1e-10 and floored < 1e-8
+
+
+def test_device_verify_grid_matches_reference_contract():
+    """gwgrid.verify_grid (bindings.cpp:192-222) on the device: the Cholesky
+    route accepts the engine's grid and flags a corrupted cell
+    (test_cli.cpp:199-226)."""
+    ds = datagen.generate(200, 4, 150, 20, seed=31)
+    args = (ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"], ds["sigma2"])
+    b = gw.solve_grid(*args)["b"]
+    err = gw.verify_grid(*args, b)
+    assert err < 1e-11
+    # agrees with the oracle's Cholesky route on a few cells
+    ref = orc.cholesky_cells(*args, [0, 77, 149], [0, 5, 19])
+    got = np.stack([b[0, 0], b[77, 5], b[149, 19]])
+    assert (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max() < 1e-11
+    bad = b.copy()
+    bad[77, 5, 2] += 1e-3 * np.abs(bad[77, 5]).max()
+    assert gw.verify_grid(*args, bad) > 1e-5
+    # p = 1
+    b1 = gw.solve_grid(ds["kinship"], np.zeros((200, 0)), ds["snps"], ds["traits"], ds["h2"],
+                       ds["sigma2"])["b"]
+    assert gw.verify_grid(ds["kinship"], np.zeros((200, 0)), ds["snps"], ds["traits"], ds["h2"],
+                          ds["sigma2"], b1) < 1e-11
