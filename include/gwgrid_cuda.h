@@ -151,12 +151,14 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
  * M_j = sigma2_j (h2_j Phi + (1 - h2_j) I) on the device, solve the GLS of
  * every cell through L^-1 [X_L | y_j | x_i] and the p x p normal equations,
  * and return the max norm-wise relative error |b - ref| / |ref| of b
- * ((m, t, p) numpy order, host) in *max_rel_err.  All operands raw, host,
+ * ((m, t, p) numpy order, host) in *max_rel_err, and every cell's error in
+ * cell_err ((m, t) numpy order) when non-null.  All operands raw, host,
  * column-major (kinship n x n, xl n x (p-1), snps n x m, traits n x t). */
 int32_t gwg_verify_grid(int32_t device, int64_t n, int64_t p, int64_t m, int64_t t,
                         const double* kinship, const double* xl, const double* snps,
                         const double* traits, const double* h2, const double* sigma2,
-                        const double* b, double* max_rel_err, gwg_status* st);
+                        const double* b, double* cell_err, double* max_rel_err,
+                        gwg_status* st);
 
 /* ---- GWG1 file legs (proj/include/gwgrid/stream.hpp:15-41) ----------------
  * 64-byte little-endian header: "GWG1", u16 version 1, u8 kind (1 snp, 2 trait,

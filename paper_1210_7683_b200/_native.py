@@ -115,7 +115,7 @@ def load() -> ctypes.CDLL:
         "gwg_solve_snp_slab": (I32, [P, I64, I64, P, I32, I32, P, I32, I32, I64, S]),
         "gwg_run_grid": (I32, [P, I64, P, P, ctypes.POINTER(RunOptions),
                                ctypes.POINTER(Counters), S]),
-        "gwg_verify_grid": (I32, [I32, I64, I64, I64, I64, P, P, P, P, P, P, P,
+        "gwg_verify_grid": (I32, [I32, I64, I64, I64, I64, P, P, P, P, P, P, P, P,
                                   ctypes.POINTER(D), S]),
         "gwg_stream_info": (I32, [ctypes.c_char_p, ctypes.POINTER(I32), ctypes.POINTER(I64),
                                   ctypes.POINTER(I32), S]),

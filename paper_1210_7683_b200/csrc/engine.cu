@@ -20,6 +20,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gwgrid_cuda.h"
@@ -223,6 +224,27 @@ int64_t default_slab(const gwg_engine* e, int64_t m) {
   const int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
   const int64_t target = std::max<int64_t>(1, (96ll << 20) / (e->t * e->p * 8));
   return std::min(m, std::max<int64_t>(1, target / unit) * unit);
+}
+
+// memcpy split over a few threads for large slabs (pageable user memory <->
+// pinned staging).
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+  const size_t kChunk = size_t(8) << 20;
+  const int threads = int(std::min<size_t>(8, (bytes + kChunk - 1) / kChunk));
+  if (threads <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t part = (bytes + threads - 1) / threads;
+  for (int w = 0; w < threads; ++w) {
+    const size_t lo = size_t(w) * part, hi = std::min(bytes, lo + part);
+    if (lo >= hi) break;
+    pool.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    });
+  }
+  for (auto& th : pool) th.join();
 }
 
 int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
@@ -538,26 +560,42 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
   const int64_t mb = opts && opts->mb > 0 ? std::min(opts->mb, m) : default_slab(e, m);
   const int nbuf = dbuf ? 2 : 1;
 
-  const bool x_pinned = is_pinned_host(x_r_host);
-  const bool b_pinned = is_pinned_host(b_host);
   const size_t x_bytes = size_t(n) * m * sizeof(double);
   const size_t b_bytes = size_t(m) * t * p * sizeof(double);
-  bool x_reg = false, b_reg = false;
-  if (!x_pinned && cudaHostRegister(const_cast<double*>(x_r_host), x_bytes,
-                                    cudaHostRegisterReadOnly) == cudaSuccess)
-    x_reg = true;
-  cudaGetLastError();
-  if (!b_pinned && cudaHostRegister(b_host, b_bytes, cudaHostRegisterDefault) == cudaSuccess)
-    b_reg = true;
-  cudaGetLastError();
-  struct Unreg {
-    const void* x;
-    void* b;
-    ~Unreg() {
-      if (x) cudaHostUnregister(const_cast<void*>(x));
-      if (b) cudaHostUnregister(b);
-    }
-  } unreg{x_reg ? x_r_host : nullptr, b_reg ? b_host : nullptr};
+  // Fully pinned buffers (both ends inside page-locked memory) take the direct
+  // async path.  Anything else goes through the staged pipeline's own pinned
+  // bounce buffers: registering arbitrary user memory in place is unsafe when
+  // a neighbouring allocation already registered part of its pages.
+  const bool direct =
+      is_pinned_host(x_r_host) &&
+      is_pinned_host(reinterpret_cast<const char*>(x_r_host) + x_bytes - 1) &&
+      is_pinned_host(b_host) && is_pinned_host(reinterpret_cast<const char*>(b_host) + b_bytes - 1);
+  if (!direct) {
+    SlabRead rd = [&](int64_t i0, int64_t rows, double* dst) {
+      parallel_copy(dst, x_r_host + size_t(i0) * n, size_t(n) * rows * 8);
+      return true;
+    };
+    SlabWrite wr = [&](int64_t i0, int64_t rows, const double* src) {
+      if (layout == GWG_LAYOUT_NUMPY) {
+        parallel_copy(b_host + size_t(i0) * t * p, src, size_t(rows) * t * p * 8);
+      } else {
+        for (int64_t j = 0; j < t; ++j)
+          std::memcpy(b_host + (size_t(j) * m + i0) * p, src + size_t(j) * rows * p,
+                      size_t(rows) * p * 8);
+      }
+      return true;
+    };
+    uint64_t loaded = 0, stored = 0;
+    const int rc = staged_pipeline(e, m, mb, false, layout, rd, wr, &loaded, &stored, nullptr, st);
+    if (rc != GWG_OK) return rc;
+    e->counters.bytes_loaded += loaded;
+    e->counters.bytes_stored += stored;
+    e->counters.wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0)
+            .count();
+    if (counters) *counters = e->counters;
+    return raise_cell_error(e, m, st);
+  }
 
   for (int b = 0; b < nbuf; ++b) {
     GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "../../include/gwgrid_cuda.h"
@@ -96,5 +97,14 @@ int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st);
 // rot_sq <- rot .* rot for `cols` already-rotated columns
 int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st);
 int64_t default_slab(const gwg_engine* e, int64_t m);
+
+// Staged slab pipeline (stream_io.cu): read_fn fills a pinned n x rows slab
+// (ld n); write_fn drains a pinned result slab in out_layout order
+// (NUMPY: (il*t + j)*p; STREAM: (j*rows + il)*p).
+using SlabRead = std::function<bool(int64_t i0, int64_t rows, double* dst)>;
+using SlabWrite = std::function<bool(int64_t i0, int64_t rows, const double* src)>;
+int staged_pipeline(gwg_engine* e, int64_t m, int64_t mb, bool rotated, int out_layout,
+                    const SlabRead& read_fn, const SlabWrite& write_fn, uint64_t* loaded,
+                    uint64_t* stored, int* io_error, gwg_status* st);
 
 }  // namespace gwg_host

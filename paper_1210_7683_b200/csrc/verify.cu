@@ -56,7 +56,7 @@ __global__ void cells_kernel(int64_t n, int p, int64_t m, const double* __restri
                              int64_t ldw, const double* __restrict__ g, int64_t ldg,
                              const double* __restrict__ sll, const double* __restrict__ rl,
                              const double* __restrict__ b, int64_t b_si, double* err_out,
-                             int* npd_out) {
+                             double* cell_err, int64_t cell_si, int* npd_out) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= m) return;
   const int pm1 = p - 1;
@@ -105,6 +105,7 @@ __global__ void cells_kernel(int64_t n, int p, int64_t m, const double* __restri
     r2 += r[c] * r[c];
   }
   const double rel = r2 > 0.0 ? sqrt(d2 / r2) : sqrt(d2);
+  if (cell_err) cell_err[i * cell_si] = rel;
   atomicMax(reinterpret_cast<unsigned long long*>(err_out),
             static_cast<unsigned long long>(__double_as_longlong(rel)));
 }
@@ -114,7 +115,8 @@ __global__ void cells_kernel(int64_t n, int p, int64_t m, const double* __restri
 extern "C" int32_t gwg_verify_grid(int32_t device, int64_t n, int64_t p, int64_t m, int64_t t,
                                    const double* kinship, const double* xl, const double* snps,
                                    const double* traits, const double* h2, const double* sigma2,
-                                   const double* b, double* max_rel_err, gwg_status* st) {
+                                   const double* b, double* cell_err, double* max_rel_err,
+                                   gwg_status* st) {
   if (st) {
     st->code = GWG_OK;
     st->snp_index = st->trait_index = -1;
@@ -144,6 +146,7 @@ extern "C" int32_t gwg_verify_grid(int32_t device, int64_t n, int64_t p, int64_t
   double* d_b = dalloc(size_t(m) * t * p * 8);
   double* d_y = dalloc(size_t(n) * t * 8);
   double* d_err = dalloc(8);
+  double* d_cell = cell_err ? dalloc(size_t(m) * t * 8) : nullptr;
   int* d_npd = reinterpret_cast<int*>(dalloc(8));
   cusolverDnHandle_t sh = nullptr;
   cublasHandle_t bh = nullptr;
@@ -207,7 +210,7 @@ extern "C" int32_t gwg_verify_grid(int32_t device, int64_t n, int64_t p, int64_t
                   int(n), &zero, d_sl, int(pm1));
     cells_kernel<<<int((m + 127) / 128), 128>>>(n, int(p), m, d_w, n, d_g, m, d_sl,
                                                 d_sl + pm1 * pm1, d_b + j * p, t * p, d_err,
-                                                d_npd);
+                                                d_cell ? d_cell + j : nullptr, t, d_npd);
   }
   if (rc == GWG_OK) {
     cudaError_t ce = cudaDeviceSynchronize();
@@ -216,6 +219,7 @@ extern "C" int32_t gwg_verify_grid(int32_t device, int64_t n, int64_t p, int64_t
   if (rc == GWG_OK) {
     int npd = 0;
     cudaMemcpy(max_rel_err, d_err, 8, cudaMemcpyDeviceToHost);
+    if (d_cell) cudaMemcpy(cell_err, d_cell, size_t(m) * t * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(&npd, d_npd, 4, cudaMemcpyDeviceToHost);
     if (npd)
       rc = fail(st, GWG_NOT_POSITIVE_DEFINITE, -1, -1,

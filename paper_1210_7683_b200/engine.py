@@ -371,10 +371,12 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     return {"b": b, "counters": counters}
 
 
-def verify_grid(kinship, xl, snps, traits, h2, sigma2, b, device: int = 0) -> float:
+def verify_grid(kinship, xl, snps, traits, h2, sigma2, b, device: int = 0,
+                cell_errors: bool = False):
     """Max norm-wise relative error of b against the independent Cholesky
     route over every cell (gwgrid.verify_grid, bindings.cpp:192-222), computed
-    on the device (gwg_verify_grid)."""
+    on the device (gwg_verify_grid).  With ``cell_errors`` also returns the
+    (m, t) array of per-cell errors."""
     kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
         kinship, xl, snps, traits, h2, sigma2)
     b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
@@ -384,14 +386,16 @@ def verify_grid(kinship, xl, snps, traits, h2, sigma2, b, device: int = 0) -> fl
     kinship, xl, snps, traits = f(kinship), f(xl), f(snps), f(traits)
     h2, sigma2 = np.ascontiguousarray(h2), np.ascontiguousarray(sigma2)
     out = ctypes.c_double(0.0)
+    cells = np.empty((m, t), dtype=np.float64) if cell_errors else None
     st = nat.Status()
     rc = nat.load().gwg_verify_grid(int(device), n, p, m, t, kinship.ctypes.data,
                                     xl.ctypes.data if p > 1 else None, snps.ctypes.data,
                                     traits.ctypes.data, h2.ctypes.data, sigma2.ctypes.data,
-                                    b.ctypes.data, ctypes.byref(out), ctypes.byref(st))
+                                    b.ctypes.data, cells.ctypes.data if cells is not None else None,
+                                    ctypes.byref(out), ctypes.byref(st))
     if rc != nat.GWG_OK:
         raise_for(st)
-    return float(out.value)
+    return (float(out.value), cells) if cell_errors else float(out.value)
 
 
 def solve_cell(phi, xl, xr, y, h2: float, sigma2: float, device: int = 0) -> np.ndarray:
