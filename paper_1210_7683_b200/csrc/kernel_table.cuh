@@ -47,14 +47,23 @@ cudaError_t launch_grid(const CUtensorMap& map, const CUtensorMap& map_sq, const
 #define GWG_PINGPONG 1
 #endif
 
+#ifndef GWG_PINGPONG_MAXP
+#define GWG_PINGPONG_MAXP 24
+#endif
+
 template <int P>
 struct CfgFor {
   static constexpr int LIM = 227 * 1024 - 128;
-  // p <= 6 with ping-pong: two 4-warp groups, group tile 64 SNPs x 16 traits
-  static constexpr bool PP = GWG_PINGPONG && GWG_PRODUCER_WARP && P <= 6;
+  // Ping-pong (two 4-warp consumer groups, one producer warp each):
+  //   p <= 6 : group tile 64 SNPs x 16 traits, warp tile 32 x 8
+  //   p <= 12: group tile 64 x 8, warp tile 16 x 8
+  //   p <= 24: group tile 32 x 8, warp tile 8 x 8
+  // Single group of 8 warps otherwise: 64x32 / 64x16 / 64x8.
+  static constexpr bool PP = GWG_PINGPONG && GWG_PRODUCER_WARP && P <= GWG_PINGPONG_MAXP;
   static constexpr int GROUPS = PP ? 2 : 1;
   static constexpr int WM_OCT = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
-  static constexpr int WARPS_T = PP ? 2 : (P <= 6 ? 4 : (P <= 12 ? 2 : 1));
+  static constexpr int WARPS_T =
+      PP ? (P <= 6 ? 2 : 1) : (P <= 6 ? 4 : (P <= 12 ? 2 : 1));
   static constexpr int WARPS_M = 8 / GROUPS / WARPS_T;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;

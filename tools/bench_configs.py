@@ -20,11 +20,14 @@ import paper_1210_7683_b200 as gw  # noqa: E402
 from paper_1210_7683_b200 import datagen  # noqa: E402
 
 PEAK = 37.15
-SLAB = {"c0": 10_000, "c1": 100_000, "c2": 100_000, "c3": 4_736, "c4": 50_000}
+SLAB = {"c0": 10_000, "c1": 100_000, "c2": 100_000, "c3": 4_736, "c4": 50_000,
+        "p8": 50_000, "p12": 50_000}
+EXTRA = {"p8": datagen.GridConfig("p8", 1000, 8, 50_000, 1000, 2000),
+         "p12": datagen.GridConfig("p12", 1000, 12, 50_000, 1000, 2000)}
 
 
 def run(name, steps):
-    cfg = datagen.CONFIGS[name]
+    cfg = datagen.CONFIGS.get(name) or EXTRA[name]
     n, p, t, m = cfg.n, cfg.p, cfg.t, SLAB[name]
     seed = 7
     dev = torch.device("cuda", 0)
