@@ -48,17 +48,18 @@ cudaError_t launch_grid(const CUtensorMap& map, const CUtensorMap& map_sq, const
 #endif
 
 #ifndef GWG_PINGPONG_MAXP
-#define GWG_PINGPONG_MAXP 24
+#define GWG_PINGPONG_MAXP 12
 #endif
 
 template <int P>
 struct CfgFor {
   static constexpr int LIM = 227 * 1024 - 128;
-  // Ping-pong (two 4-warp consumer groups, one producer warp each):
+  // Ping-pong (two 4-warp consumer groups, one producer warp each), p <= 12:
   //   p <= 6 : group tile 64 SNPs x 16 traits, warp tile 32 x 8
   //   p <= 12: group tile 64 x 8, warp tile 16 x 8
-  //   p <= 24: group tile 32 x 8, warp tile 8 x 8
-  // Single group of 8 warps otherwise: 64x32 / 64x16 / 64x8.
+  // p > 12: one group of 8 warps, tile 64 x 8, warp tile 8 x 8 (measured on
+  // the B200: ping-pong with 32 x 8 group tiles is slower there, 31.1 vs
+  // 32.2 TFLOP/s at p = 20; faster at p = 8 and 12, 31.6 vs 30.7 / 30.8 vs 29.8).
   static constexpr bool PP = GWG_PINGPONG && GWG_PRODUCER_WARP && P <= GWG_PINGPONG_MAXP;
   static constexpr int GROUPS = PP ? 2 : 1;
   static constexpr int WM_OCT = P <= 6 ? 4 : (P <= 12 ? 2 : 1);
