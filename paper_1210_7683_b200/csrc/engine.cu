@@ -145,6 +145,7 @@ int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
            int64_t lds, double* dst_sq) {
   if (cols <= 0) return GWG_OK;
+  NvtxRange nvtx_("rotate");
   if (lds == 0) lds = e->np;
   CUtensorMap tz, tx;
   if (int rc = encode_kmajor(&tz, e->basis.d(), e->n, e->n, e->np, gwg::RotCfg::BM, st)) return rc;
@@ -378,6 +379,7 @@ extern "C" int32_t gwg_internal_device_eig(double* a, int64_t n, int64_t lda, do
                                            cudaStream_t stream, gwg_status* st);
 
 int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_status* st) {
+  NvtxRange nvtx_("gwg_set_kinship");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!phi) return set_status(st, GWG_DIMENSION, -1, -1, "null kinship matrix");
@@ -410,6 +412,7 @@ int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_s
 
 int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* h2,
                        const double* sigma2, int32_t where, int32_t is_rotated, gwg_status* st) {
+  NvtxRange nvtx_("gwg_set_traits");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!e->have_covariates)
@@ -474,6 +477,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
 int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* x_r,
                            int32_t where, int32_t is_rotated, double* b_out, int32_t out_where,
                            int32_t layout, int64_t ldo, gwg_status* st) {
+  NvtxRange nvtx_("gwg_solve_snp_slab");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!e->have_traits)
@@ -542,6 +546,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
 
 int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
                      const gwg_run_options* opts, gwg_counters* counters, gwg_status* st) {
+  NvtxRange nvtx_("gwg_run_grid");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!e->have_traits)

@@ -10,6 +10,8 @@
 #include <functional>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gwgrid_cuda.h"
 #include "kernel_table.cuh"
 
@@ -22,6 +24,14 @@
   } while (0)
 
 namespace gwg_host {
+
+// NVTX range for profiler timelines (no-op unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DevBuf {
   void* ptr = nullptr;

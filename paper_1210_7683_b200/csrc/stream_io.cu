@@ -389,6 +389,7 @@ extern "C" {
 int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_rotated,
                            const char* out_path, const gwg_run_options* opts,
                            gwg_counters* counters, gwg_status* st) {
+  NvtxRange nvtx_("gwg_run_grid_files");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
   if (!e->have_traits)

@@ -1,0 +1,24 @@
+"""Small end-to-end case for compute-sanitizer runs (one tool per gpurun call)."""
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+import paper_1210_7683_b200 as gw  # noqa: E402
+from paper_1210_7683_b200 import datagen  # noqa: E402
+
+for (n, p, m, t) in ((130, 4, 150, 37), (96, 1, 40, 9), (200, 8, 70, 20), (64, 20, 30, 9)):
+    ds = datagen.generate(n, p, m, t, seed=3)
+    z, lam = gw.eigendecompose(ds["kinship"])
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(z, lam)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        b = eng.run_grid(ds["snps"], mb=64)
+        b2 = eng.solve_snp_slab(ds["snps"])
+        assert np.array_equal(b, b2) and not np.isnan(b).any()
+    err = gw.verify_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                         ds["sigma2"], b)
+    print(n, p, m, t, "verify", err)
+z2, l2 = gw.eigendecompose(datagen.kinship(1, 300, 600), device=0)
+print("ok")
