@@ -281,7 +281,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   KernelOps ops;
   if (!gwg::ops_for(p, &ops)) {
     set_status(st, GWG_DIMENSION, -1, -1,
-               "p=%lld is outside the compiled predictor range 1..24", (long long)p);
+               "p=%lld is outside the compiled predictor range 1..32", (long long)p);
     return nullptr;
   }
   int count = 0;

@@ -95,13 +95,14 @@ KernelOps make_ops() {
   return k;
 }
 
-// One per translation unit (kernels_a.cu / kernels_b.cu / kernels_c.cu).
+// One per translation unit (kernels_a.cu .. kernels_d.cu), compiled in parallel.
 bool ops_for_a(int64_t p, KernelOps* out);
 bool ops_for_b(int64_t p, KernelOps* out);
 bool ops_for_c(int64_t p, KernelOps* out);
+bool ops_for_d(int64_t p, KernelOps* out);
 
 inline bool ops_for(int64_t p, KernelOps* out) {
-  return ops_for_a(p, out) || ops_for_b(p, out) || ops_for_c(p, out);
+  return ops_for_a(p, out) || ops_for_b(p, out) || ops_for_c(p, out) || ops_for_d(p, out);
 }
 
 }  // namespace gwg

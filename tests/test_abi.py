@@ -72,5 +72,5 @@ def test_bad_dimensions_rejected_before_device():
     st = nat.Status()
     assert not nat.load().gwg_engine_create(0, 4, 5, ctypes.byref(st))  # p > n
     assert st.code == nat.GWG_DIMENSION
-    assert not nat.load().gwg_engine_create(0, 100, 99, ctypes.byref(st))  # p out of range
-    assert st.code == nat.GWG_DIMENSION
+    assert not nat.load().gwg_engine_create(0, 100, 33, ctypes.byref(st))  # p out of range
+    assert st.code == nat.GWG_DIMENSION and b"1..32" in st.msg

@@ -74,7 +74,8 @@ def device_grid(ds, basis, values, **kw):
     (300, 7, 130, 21),
     (320, 12, 80, 19),
     (500, 20, 70, 13),       # config 4's p
-    (31, 24, 20, 5),         # largest compiled p, n < 32
+    (31, 24, 20, 5),         # n < 32
+    (40, 32, 20, 5),         # largest compiled p
 ])
 def test_grid_matches_oracle(n, p, m, t):
     ds = datagen.generate(n, p, m, t, seed=n + p)
