@@ -151,6 +151,8 @@ def make_inputs(args, rank: int, world: int, dev_index: int):
             buf = shared[key]
             base = buf.t() if buf.dim() == 2 else buf
             dist.broadcast(base, src=0)
+        # the engine reads these on its own stream: finish the broadcasts first
+        torch.cuda.synchronize(dev)
     shared["sigma2"] = torch.ones(t, dtype=torch.float64, device=dev)
     # this rank's SNP shard: global columns [rank*m, (rank+1)*m), pinned host
     x_host = torch.empty((m, n), dtype=torch.float64).pin_memory()

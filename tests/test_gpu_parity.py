@@ -321,3 +321,19 @@ def test_device_verify_grid_matches_reference_contract():
                        ds["sigma2"])["b"]
     assert gw.verify_grid(ds["kinship"], np.zeros((200, 0)), ds["snps"], ds["traits"], ds["h2"],
                           ds["sigma2"], b1) < 1e-11
+
+
+def test_engine_argument_errors():
+    """The C ABI rejects empty / mismatched operands with DimensionError."""
+    with gw.Engine(16, 3) as eng:
+        with pytest.raises(gw.DimensionError, match="set_traits"):
+            eng.solve_snp_slab(np.ones((16, 2)))
+        eng.set_spectrum(np.eye(16), np.ones(16))
+        eng.set_covariates(np.ones((16, 2)))
+        with pytest.raises(gw.DimensionError):
+            eng.set_traits(np.ones((16, 0)), [], [])
+        eng.set_traits(np.ones((16, 2)), [0.5, 0.5], [1.0, 1.0])
+        with pytest.raises(gw.DimensionError):
+            eng.solve_snp_slab(np.ones((15, 2)))
+        with pytest.raises(gw.DimensionError):
+            eng.run_grid(np.ones((16, 0)))

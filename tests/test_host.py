@@ -184,3 +184,14 @@ def test_snp_sharding_over_two_ranks_matches_single_rank():
     whole = orc.compute_grid(lam, z.T @ ds["xl"], z.T @ ds["snps"], z.T @ ds["traits"],
                              ds["h2"], np.ones(4))
     assert np.array_equal(sharded, whole)
+
+
+def test_empty_grids_are_dimension_errors():
+    """ProblemDims::validate (types.cpp:7-17): m, t >= 1 — checked before any
+    device work, like the reference."""
+    ds = small()
+    with pytest.raises(gw.DimensionError, match="m must be >= 1"):
+        gw.solve_grid(ds["kinship"], ds["xl"], np.zeros((16, 0)), ds["traits"], ds["h2"],
+                      ds["sigma2"])
+    with pytest.raises(gw.DimensionError, match="t must be >= 1"):
+        gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], np.zeros((16, 0)), [], [])
