@@ -48,6 +48,10 @@ class _Operand:
                 x = x.t().contiguous().t()
             elif x.dim() <= 1 or x.shape[0] <= 1 or x.shape[1] <= 1:
                 x = x.contiguous()
+            if x.is_cuda:
+                # the engine reads on its own stream: order it after torch's
+                # pending work on this tensor's device
+                torch.cuda.current_stream(x.device).synchronize()
             self.keep = x
             self.ptr = x.data_ptr()
             self.where = nat.GWG_DEVICE if x.is_cuda else nat.GWG_HOST
@@ -192,6 +196,10 @@ class Engine:
         if _is_torch(out):
             if tuple(out.shape) != shape or not out.is_contiguous():
                 raise DimensionError(f"out must be a contiguous tensor of shape {shape}")
+            if out.is_cuda:
+                import torch
+
+                torch.cuda.current_stream(out.device).synchronize()
             optr, owhere = out.data_ptr(), nat.GWG_DEVICE if out.is_cuda else nat.GWG_HOST
         else:
             if out.shape != shape or not out.flags.c_contiguous or out.dtype != np.float64:
