@@ -41,6 +41,15 @@
 
 #include "gwg_device.cuh"
 
+// Timing experiments only (never in a shipped build): 1 = skip the Cholesky
+// epilogue math, 2 = feed every k-chunk from the first STAGES loads.
+#ifndef GWG_EXPERIMENT
+#define GWG_EXPERIMENT 0
+#endif
+#ifndef GWG_RCP_MAXP
+#define GWG_RCP_MAXP 4
+#endif
+
 namespace gwg {
 
 // Per-trait epilogue context: 1/L_aa (p-1), strictly-lower L (packed by rows),
@@ -118,7 +127,8 @@ struct GridArgs {
 //   l = L^-1 s_bl            (Eigen LLT's last-row update, divisions by L_aa
 //                             folded into the stored reciprocals)
 //   pivot = s_br - |l|^2     fails iff pivot <= 0, like Eigen's LLT (NaN passes)
-//   beta_B = (b_B - l.z_T) / pivot     (= ((b_B - l.z_T)/lambda)/lambda)
+//   beta_B = (b_B - l.z_T) / pivot     (= ((b_B - l.z_T)/lambda)/lambda;
+//                                       reciprocal by rcp.approx + Newton)
 //   beta_T = L^-T (z_T - l beta_B)
 template <int P>
 __device__ __forceinline__ bool solve_cell(const double* acc, const double* __restrict__ cx,
@@ -141,7 +151,19 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   }
   const double pivot = acc[P] - sq;
   const bool ok = !(pivot <= 0.0) && __ldg(cx + L::FLAG) == 0.0;
-  const double bb = (acc[P1] - lz) / pivot;
+  // 1/pivot: MUFU approximation + two Newton steps (<= 1 ulp; far cheaper on
+  // the FP64 pipe than an IEEE division, which the other ping-pong group's
+  // DMMAs are competing for)
+  double bb;
+  if (P <= GWG_RCP_MAXP) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(pivot));
+    r = fma(r, fma(-pivot, r, 1.0), r);
+    r = fma(r, fma(-pivot, r, 1.0), r);
+    bb = (acc[P1] - lz) * r;
+  } else {  // large p: the O(p^2) substitutions dominate; keep register pressure low
+    bb = (acc[P1] - lz) / pivot;
+  }
   beta[P1] = bb;
 #pragma unroll
   for (int a = P1 - 1; a >= 0; --a) {
@@ -240,7 +262,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   if (Cfg::PRODUCER_WARP) {
     if (is_producer_warp) {
       if (producer)
-        for (int g = 0; g < total_iters; ++g)
+        for (int g = 0; g < (GWG_EXPERIMENT == 2 ? min(total_iters, Cfg::STAGES) : total_iters);
+             ++g)
           issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g, total_iters, pol_a,
                            pol_b, group);
       return;
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         issue_stage<Cfg>(&tmap_a, &tmap_q, args, sA, sB, full, empty, g + Cfg::LOOKAHEAD,
                          total_iters, pol_a, pol_b);
       const int s = g % Cfg::STAGES;
-      mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
+      if (GWG_EXPERIMENT != 2 || g < Cfg::STAGES) mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
       const double2* a2 = reinterpret_cast<const double2*>(sA + s * Cfg::SA_STAGE);
       const double2* q2 = a2 + Cfg::A_STAGE / 2;
       const double2* b2 = reinterpret_cast<const double2*>(sB + s * Cfg::B_STAGE);
@@ -324,7 +347,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < NC; ++c) cell[c] = acc[o][c][e];
         double beta[P];
+#if GWG_EXPERIMENT == 1
+        bool ok = true;
+#pragma unroll
+        for (int c = 0; c < P; ++c) beta[c] = cell[c] + cell[P];
+#else
         const bool ok = solve_cell<P>(cell, cx, beta);
+#endif
         double* dst = args.out + (il * args.out_si + int64_t(j) * args.out_sj) * P;
         if (!ok) {
           atomicMin(args.err_key,
