@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--t", type=int, default=1000)
     ap.add_argument("--n", type=int, default=1000)
     ap.add_argument("--p", type=int, default=4)
+    ap.add_argument("--snp-coding", default="genotypes", choices=["genotypes", "real"],
+                    help="BASELINE X_R are genotype codes {0,1,2}: exact int8 tcgen05 rotation")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -179,6 +181,7 @@ def run_ours(args):
     eng = gw.Engine(n, p, device=local)
     eng.set_spectrum(shared["basis"], shared["values"])
     eng.set_covariates(shared["xl"])
+    eng.set_snp_coding(args.snp_coding)
     x_dev = x_host_t.to(dev, non_blocking=False).t()  # (n, m) column-major on device
     b_dev = torch.empty((m, t, p), dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
@@ -276,7 +279,10 @@ def run_ours(args):
             "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": m, "t": t,
                        "cells_per_step": cells, "parallelism": f"snp-shard x{world}",
                        "l2": "inputs larger than L2 (X_R %.1f GB per GPU per step)" % (n * m * 8 / 1e9),
-                       "step": "rotate Y and X_R (own DMMA rotation kernel) + trait contexts + fused grid kernel"},
+                       "snp_coding": args.snp_coding,
+                       "step": "rotate Y (DMMA) and X_R (%s) + trait contexts + fused grid kernel"
+                               % ("exact int8 tcgen05 rotation" if args.snp_coding == "genotypes"
+                                  else "DMMA rotation")},
             "tflops": grid_flops_step * world / (ms_step * 1e-3) / 1e12,
             "tflops_convention": "2n(p+1) per cell (grid contraction); reference n(2p+3) = %.3f TF"
                                  % (m * t * n * (2 * p + 3) * world / (ms_step * 1e-3) / 1e12),

@@ -45,6 +45,7 @@ enum gwg_code {
 
 enum gwg_where { GWG_HOST = 0, GWG_DEVICE = 1 };
 enum gwg_layout { GWG_LAYOUT_NUMPY = 0, GWG_LAYOUT_STREAM = 1 };
+enum gwg_snp_coding { GWG_SNP_REAL = 0, GWG_SNP_GENOTYPES = 1 };
 
 typedef struct gwg_status {
   int32_t code;
@@ -186,6 +187,16 @@ int32_t gwg_set_traits_file(gwg_engine* e, const char* traits_path, gwg_status* 
 int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_rotated,
                            const char* out_path, const gwg_run_options* opts,
                            gwg_counters* counters, gwg_status* st);
+
+/* How SNP slabs are coded.  GWG_SNP_REAL (default): any real values; the
+ * rotation runs on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP
+ * value is an integer code in [-127, 127] (e.g. genotypes 0/1/2); the rotation
+ * then runs exactly on the int8 tensor cores (tcgen05.mma kind::i8, Z split
+ * into eight 7-bit slices, FP64 recombination, ~1 ulp), and each slab is
+ * checked on the device (violations fail with GWG_DIMENSION).  Results match
+ * the real-valued path to rounding; both are bitwise independent of slab
+ * geometry. */
+int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
 
 /* Counters accumulated since the last reset. */
 int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out);

@@ -25,6 +25,8 @@ GWG_HOST = 0
 GWG_DEVICE = 1
 GWG_LAYOUT_NUMPY = 0
 GWG_LAYOUT_STREAM = 1
+GWG_SNP_REAL = 0
+GWG_SNP_GENOTYPES = 1
 
 # Every symbol include/gwgrid_cuda.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -38,6 +40,7 @@ EXPORTED_SYMBOLS = (
     "gwg_set_traits",
     "gwg_solve_snp_slab",
     "gwg_run_grid",
+    "gwg_set_snp_coding",
     "gwg_get_counters",
     "gwg_reset_counters",
     "gwg_synchronize",
@@ -122,6 +125,7 @@ def load() -> ctypes.CDLL:
         "gwg_set_traits_file": (I32, [P, ctypes.c_char_p, S]),
         "gwg_run_grid_files": (I32, [P, ctypes.c_char_p, I32, ctypes.c_char_p,
                                      ctypes.POINTER(RunOptions), ctypes.POINTER(Counters), S]),
+        "gwg_set_snp_coding": (I32, [P, I32, S]),
         "gwg_get_counters": (I32, [P, ctypes.POINTER(Counters)]),
         "gwg_reset_counters": (None, [P]),
         "gwg_synchronize": (I32, [P, S]),

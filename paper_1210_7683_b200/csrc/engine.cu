@@ -25,6 +25,7 @@
 
 #include "../../include/gwgrid_cuda.h"
 #include "engine_internal.cuh"
+#include "rotate_i8.cuh"
 #include "rotate_kernel.cuh"
 
 namespace gwg_host {
@@ -167,15 +168,91 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
 }
 
 int read_errors(gwg_engine* e, gwg_status* st, bool trait_only) {
-  GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 2 * sizeof(unsigned long long),
+  GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 3 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
-  (void)trait_only;
+  if (!trait_only && e->err_host[2] != ~0ull)
+    return set_status(st, GWG_DIMENSION, -1, -1,
+                      "SNP values are not integer genotype codes in [-127, 127] "
+                      "(gwg_set_snp_coding(GENOTYPES)); use real-valued coding");
   return GWG_OK;
 }
 
 int reset_errors(gwg_engine* e, gwg_status* st) {
-  GWG_CUDA_TRY(cudaMemsetAsync(e->err.ptr, 0xff, 2 * sizeof(unsigned long long), e->comp));
+  GWG_CUDA_TRY(cudaMemsetAsync(e->err.ptr, 0xff, 3 * sizeof(unsigned long long), e->comp));
+  return GWG_OK;
+}
+
+int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st) {
+  if (e->snp_coding == 0) return rotate(e, src, cols, e->rot.d(), st, lds, e->rot_sq.d());
+  if (cols <= 0) return GWG_OK;
+  NvtxRange nvtx_("rotate_i8");
+  using gwg::I8Cfg;
+  const int64_t n = e->n, kp = round_up(n, I8Cfg::BK);
+  if (!e->slices_valid) {
+    GWG_CUDA_TRY(e->zslices.ensure(size_t(I8Cfg::SLICES) * n * kp));
+    GWG_CUDA_TRY(e->zscale.ensure(size_t(n) * sizeof(double)));
+    gwg::slice_basis_kernel<<<int(n), 256, 0, e->comp>>>(
+        e->basis.d(), e->np, int32_t(n), int32_t(kp), static_cast<int8_t*>(e->zslices.ptr),
+        e->zscale.d());
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    e->slices_valid = true;
+  }
+  GWG_CUDA_TRY(e->xi8.ensure(size_t(cols) * kp));
+  {
+    const int64_t total = cols * kp;
+    const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(e->sms) * 16));
+    gwg::snp_to_i8_kernel<<<blocks, 256, 0, e->comp>>>(
+        src, lds, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
+        static_cast<unsigned long long*>(e->err.ptr) + 2);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+  }
+  auto encode = get_encode();
+  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap tx, tz;
+  {
+    const cuuint64_t gdim[2] = {cuuint64_t(kp), cuuint64_t(cols)};
+    const cuuint64_t gstride[1] = {cuuint64_t(kp)};
+    const cuuint32_t box[2] = {I8Cfg::BK, I8Cfg::BM};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, e->xi8.ptr, gdim, gstride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 SNP slab) failed (%d)", int(r));
+  }
+  {
+    const cuuint64_t gdim[3] = {cuuint64_t(kp), cuuint64_t(n), cuuint64_t(I8Cfg::SLICES)};
+    const cuuint64_t gstride[2] = {cuuint64_t(kp), cuuint64_t(n) * kp};
+    const cuuint32_t box[3] = {I8Cfg::BK, I8Cfg::RB, I8Cfg::SLICES};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, e->zslices.ptr, gdim, gstride, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (basis slices) failed (%d)", int(r));
+  }
+  gwg::I8Args a;
+  a.dst = e->rot.d();
+  a.dst_sq = e->rot_sq.d();
+  a.scale = e->zscale.d();
+  a.ldd = e->np;
+  a.n = int32_t(n);
+  a.cols = int32_t(cols);
+  a.tiles_m = int32_t(ceil_div(cols, I8Cfg::BM));
+  a.tiles_r = int32_t(ceil_div(n, I8Cfg::RB));
+  a.kstages = int32_t(kp / I8Cfg::BK);
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
+  GWG_CUDA_TRY(cudaFuncSetAttribute(gwg::rotate_i8_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(I8Cfg::SMEM_BYTES)));
+  gwg::rotate_i8_kernel<<<int(std::min<int64_t>(tiles, e->sms)), I8Cfg::THREADS,
+                          I8Cfg::SMEM_BYTES, e->comp>>>(tx, tz, a);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
   return GWG_OK;
 }
 
@@ -328,9 +405,9 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   cudaEventCreate(&e->ev_k1);
   cudaEventCreate(&e->ev_r0);
   cudaEventCreate(&e->ev_r1);
-  if ((err = e->err.ensure(2 * sizeof(unsigned long long))) != cudaSuccess)
+  if ((err = e->err.ensure(3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMalloc", err);
-  if ((err = cudaMallocHost(&e->err_host, 2 * sizeof(unsigned long long))) != cudaSuccess)
+  if ((err = cudaMallocHost(&e->err_host, 3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMallocHost", err);
   return e;
 }
@@ -343,7 +420,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->d2h) cudaStreamSynchronize(e->d2h);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
-                    &e->out[1], &e->stage, &e->err})
+                    &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   for (int b = 0; b < 2; ++b) {
@@ -372,6 +449,7 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
   e->have_spectrum = true;
   e->have_covariates = false;
   e->have_traits = false;
+  e->slices_valid = false;
   return GWG_OK;
 }
 
@@ -388,6 +466,7 @@ int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_sta
   GWG_CUDA_TRY(e->lambda.ensure(size_t(e->n) * sizeof(double)));
   if (int rc = gwg_internal_device_eig(e->basis.d(), e->n, e->np, e->lambda.d(), e->comp, st))
     return rc;
+  e->slices_valid = false;
   e->have_spectrum = true;
   return GWG_OK;
 }
@@ -509,7 +588,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
         return rc;
       src = e->raw[0].d();
     }
-    if (int rc = rotate(e, src, mb, e->rot.d(), st, raw_ld(e), e->rot_sq.d())) return rc;
+    if (int rc = rotate_snps(e, src, raw_ld(e), mb, st)) return rc;
   }
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r1, e->comp));
   double* dev_out = b_out;
@@ -636,8 +715,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
     // Compute: rotate + fused grid once the slab landed and out[b] drained.
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
     GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
-    if (int rc = rotate(e, e->raw[b].d(), rows, e->rot.d(), st, raw_ld(e), e->rot_sq.d()))
-      return rc;
+    if (int rc = rotate_snps(e, e->raw[b].d(), raw_ld(e), rows, st)) return rc;
     GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
     GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
     const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
@@ -674,6 +752,18 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   if (counters) *counters = e->counters;
   return raise_cell_error(e, m, st);
+}
+
+int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (coding != GWG_SNP_REAL && coding != GWG_SNP_GENOTYPES)
+    return set_status(st, GWG_DIMENSION, -1, -1, "unknown SNP coding %d", coding);
+  if (coding == GWG_SNP_GENOTYPES && e->n >= 262000)
+    return set_status(st, GWG_DIMENSION, -1, -1,
+                      "genotype coding needs n < 262,000 (exact int32 accumulation)");
+  e->snp_coding = coding;
+  return GWG_OK;
 }
 
 int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out) {

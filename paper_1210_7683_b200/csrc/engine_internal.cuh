@@ -77,7 +77,12 @@ struct gwg_engine {
   gwg_host::DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
 
   gwg_host::DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
-  gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key
+  gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key, [2] genotype check
+  // SNP coding: 0 = real-valued (DMMA rotation), 1 = integer genotype codes
+  // (exact int8 tcgen05 rotation); slices of Z are rebuilt after a new spectrum.
+  int snp_coding = 0;
+  bool slices_valid = false;
+  gwg_host::DevBuf zslices, zscale, xi8;
   unsigned long long* err_host = nullptr;
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
@@ -98,6 +103,8 @@ int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int6
 int64_t raw_ld(const gwg_engine* e);
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
            int64_t lds = 0, double* dst_sq = nullptr);
+// SNP slab -> e->rot / e->rot_sq with the engine's SNP coding (DMMA or int8).
+int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st);
 int read_errors(gwg_engine* e, gwg_status* st, bool trait_only);
 int reset_errors(gwg_engine* e, gwg_status* st);
 int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,

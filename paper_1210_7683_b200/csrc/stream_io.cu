@@ -331,8 +331,7 @@ int staged_pipeline(gwg_engine* e, int64_t m, int64_t mb, bool rotated, int out_
         GWG_CUDA_TRY(cudaMemcpy2DAsync(e->rot.ptr, e->np * 8, e->raw[b].ptr, raw_ld(e) * 8,
                                        n * 8, rows, cudaMemcpyDeviceToDevice, e->comp));
         if (int r = square_rotated(e, rows, st)) return r;
-      } else if (int r = rotate(e, e->raw[b].d(), rows, e->rot.d(), st, raw_ld(e),
-                                e->rot_sq.d())) {
+      } else if (int r = rotate_snps(e, e->raw[b].d(), raw_ld(e), rows, st)) {
         return r;
       }
       GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));

@@ -160,6 +160,15 @@ class Engine:
         k = _Operand(phi, (self.n, self.n), "kinship")
         self._call(self._lib.gwg_set_kinship, k.ptr, k.where)
 
+    def set_snp_coding(self, coding: str) -> None:
+        """"real" (default: any SNP values, DMMA rotation) or "genotypes"
+        (integer codes in [-127, 127]: exact int8 tcgen05 rotation, values
+        checked on the device) — gwg_set_snp_coding."""
+        code = {"real": nat.GWG_SNP_REAL, "genotypes": nat.GWG_SNP_GENOTYPES}.get(coding)
+        if code is None:
+            raise DimensionError(f"unknown SNP coding {coding!r}")
+        self._call(self._lib.gwg_set_snp_coding, code)
+
     def set_covariates(self, xl) -> None:
         if self.p == 1:
             self._call(self._lib.gwg_set_covariates, None, nat.GWG_HOST)
@@ -315,7 +324,7 @@ def device_working_set_bytes(n: int, p: int, t: int, mb: int) -> int:
 def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,
                nb: int = 0, mb: int = 0, tb: int = 0, mbb: int = 0, tbb: int = 0,
                double_buffer: bool = True, memory_budget: int | None = None,
-               device: int = 0, device_eig: bool = False) -> dict:
+               device: int = 0, device_eig: bool = False, snp_coding: str = "real") -> dict:
     """Solve the whole m x t grid; returns {'b': (m, t, p), 'counters': dict}.
 
     Same signature and semantics as gwgrid.solve_grid (bindings.cpp:115-190,
@@ -325,7 +334,8 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     independent of tiling here as well.  ``mb`` is the streamed SNP slab
     width.  ``memory_budget`` bounds the device working set.  ``device_eig``
     moves the one-off eigendecomposition to the GPU (cuSOLVER); by default it
-    runs on the CPU like the reference.
+    runs on the CPU like the reference.  ``snp_coding="genotypes"`` declares
+    integer-coded SNPs (exact int8 tensor-core rotation, see Engine).
     """
     kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
         kinship, xl, snps, traits, h2, sigma2)
@@ -357,6 +367,7 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
         else:
             eng.set_spectrum(*eigendecompose(kinship))
         eng.set_covariates(xl)
+        eng.set_snp_coding(snp_coding)
         eng.set_traits(traits, h2, sigma2)
         b = np.empty((m, t, p), dtype=np.float64)
         eng.run_grid(snps, b, mb=mb, double_buffer=double_buffer)

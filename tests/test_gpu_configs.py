@@ -23,7 +23,7 @@ from paper_1210_7683_b200 import datagen  # noqa: E402
 from tests.test_gpu_parity import assert_parity, metrics  # noqa: E402
 
 
-def run_config(n, p, t, s, m_dev, m_orc, t_orc, seed, device_eig):
+def run_config(n, p, t, s, m_dev, m_orc, t_orc, seed, device_eig, coding="real"):
     phi = datagen.kinship(seed, n, s)
     if device_eig:
         basis, values = gw.eigendecompose(phi, device=0)
@@ -38,6 +38,7 @@ def run_config(n, p, t, s, m_dev, m_orc, t_orc, seed, device_eig):
     with gw.Engine(n, p) as eng:
         eng.set_spectrum(basis, values)
         eng.set_covariates(xl)
+        eng.set_snp_coding(coding)
         eng.set_traits(traits, h2, s2)
         b = eng.run_grid(snps)
         b2 = eng.run_grid(snps, mb=37)
@@ -54,13 +55,16 @@ def run_config(n, p, t, s, m_dev, m_orc, t_orc, seed, device_eig):
     return metrics(got, ref)
 
 
-def test_config2_large_n():
-    print(run_config(10_000, 4, 1000, 20_000, 600, 150, 100, 2, device_eig=True))
+@pytest.mark.parametrize("coding", ["real", "genotypes"])
+def test_config2_large_n(coding):
+    print(run_config(10_000, 4, 1000, 20_000, 600, 150, 100, 2, device_eig=True, coding=coding))
 
 
-def test_config3_many_traits():
-    print(run_config(1000, 4, 100_000, 2000, 300, 100, 1500, 3, device_eig=False))
+@pytest.mark.parametrize("coding", ["real", "genotypes"])
+def test_config3_many_traits(coding):
+    print(run_config(1000, 4, 100_000, 2000, 300, 100, 1500, 3, device_eig=False, coding=coding))
 
 
-def test_config4_many_covariates():
-    print(run_config(2000, 20, 2000, 2000, 700, 200, 200, 4, device_eig=False))
+@pytest.mark.parametrize("coding", ["real", "genotypes"])
+def test_config4_many_covariates(coding):
+    print(run_config(2000, 20, 2000, 2000, 700, 200, 200, 4, device_eig=False, coding=coding))

@@ -47,6 +47,7 @@ def run(name, steps):
     with gw.Engine(n, p) as eng:
         eng.set_spectrum(basis, values)
         eng.set_covariates(xl)
+        eng.set_snp_coding(os.environ.get("GWG_SNP_CODING", "real"))
         stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
 
         def step():
