@@ -35,6 +35,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GLS problems solved/sec (m·t/s) at n=1000,p=4; FP64 TFLOP/s vs B200 peak"
 PEAK_FP64_TFLOPS = 37.15  # measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.txt
+I8_SLICES = 8  # int8 slices of W per linear term (rotate_i8.cuh)
+# int8 dense tensor peak: 2 x the measured bf16 dense figure (NVIDIA's int8:bf16
+# dense ratio on B200); MEASURED_PEAKS.json has no int8 entry
+PEAK_INT8_TOPS = 2 * 1616.9
+PEAK_INT8_SOURCE = "derived: 2 x MEASURED_PEAKS.json bf16_tflops (1616.9, burst)"
 PEAK_SOURCE = ("measured: DMMA.8x8x4 issue loop on this pool's B200 at 1965 MHz "
                "(profiles/r01_fp64_peak.txt; = 148 SM x 128 flop/clk x 1.965 GHz; "
                "MEASURED_PEAKS.json holds no FP64 figure)")
@@ -223,8 +228,42 @@ def run_ours(args):
     value = cells / (ms_step * 1e-3)
     grid_flops_step = m * t * 2 * n * (p + 1)
     kernel_ms = cnt["grid_kernel_ms"] / args.steps
-    achieved = grid_flops_step / (kernel_ms * 1e-3) / 1e12
     rotate_ms = cnt["rotate_ms"] / args.steps
+    split = cnt["quad_ms"] > 0
+    if split:
+        # genotype split grid: the dominant launch is gls_quad_kernel, whose
+        # own algorithmic work is the quadratic term, 2n flop per cell on DMMA;
+        # the p linear terms ran exactly on the int8 tensor cores (secondary)
+        quad_ms = cnt["quad_ms"] / args.steps
+        lin_ms = cnt["linear_ms"] / args.steps
+        quad_flops = m * t * 2 * n
+        achieved = quad_flops / (quad_ms * 1e-3) / 1e12
+        lin_ops = m * t * p * 2 * n * I8_SLICES
+        lin_achieved = lin_ops / (lin_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
+                "traffic": load_traffic("quad_kernel"), "kernel": "gls_quad_kernel<P=%d>" % p,
+                "kernel_ms": quad_ms, "peak_source": PEAK_SOURCE,
+                "algorithmic_flops_per_launch": quad_flops,
+                "algorithmic_unit": "2n flop per cell: S_BR = (X'.X')^T D",
+                "secondary": {"kernel": "rotate_i8_kernel (linear terms x^T W, 8 int8 slices)",
+                              "bound": "tensor", "achieved": lin_achieved,
+                              "peak": PEAK_INT8_TOPS, "unit": "TOP/s",
+                              "frac": lin_achieved / PEAK_INT8_TOPS, "kernel_ms": lin_ms,
+                              "traffic": load_traffic("linear_kernel"),
+                              "algorithmic_ops_per_launch": lin_ops,
+                              "peak_source": PEAK_INT8_SOURCE},
+                "step_breakdown_ms": {"rotate_snps": rotate_ms, "linear": lin_ms,
+                                      "quad_solve": quad_ms,
+                                      "other (Y rotation, contexts, W)": ms_step - rotate_ms
+                                      - lin_ms - quad_ms}}
+    else:
+        achieved = grid_flops_step / (kernel_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
+                "traffic": load_traffic("grid_kernel"), "kernel": "gls_grid_kernel<P=%d>" % p,
+                "kernel_ms": kernel_ms, "rotate_ms": rotate_ms, "peak_source": PEAK_SOURCE,
+                "algorithmic_flops_per_launch": grid_flops_step}
 
     # sanity: no NaN, finite results
     bad = int(torch.isnan(b_dev).sum().item())
@@ -280,19 +319,16 @@ def run_ours(args):
                        "cells_per_step": cells, "parallelism": f"snp-shard x{world}",
                        "l2": "inputs larger than L2 (X_R %.1f GB per GPU per step)" % (n * m * 8 / 1e9),
                        "snp_coding": args.snp_coding,
-                       "step": "rotate Y (DMMA) and X_R (%s) + trait contexts + fused grid kernel"
-                               % ("exact int8 tcgen05 rotation" if args.snp_coding == "genotypes"
-                                  else "DMMA rotation")},
+                       "step": ("rotate Y (DMMA) and X_R (exact int8 tcgen05) + trait contexts "
+                                "+ split grid: linear terms x^T W exact on int8 tcgen05, quadratic "
+                                "term on DMMA fused with the bordered Cholesky"
+                                if split else
+                                "rotate Y and X_R (DMMA) + trait contexts + fused DMMA grid kernel")},
             "tflops": grid_flops_step * world / (ms_step * 1e-3) / 1e12,
             "tflops_convention": "2n(p+1) per cell (grid contraction); reference n(2p+3) = %.3f TF"
                                  % (m * t * n * (2 * p + 3) * world / (ms_step * 1e-3) / 1e12),
             "gpu_launches": int(cnt["kernel_launches"]),
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
-                         "traffic": load_traffic(), "kernel": "gls_grid_kernel<P=4>",
-                         "kernel_ms": kernel_ms, "rotate_ms": rotate_ms,
-                         "peak_source": PEAK_SOURCE,
-                         "algorithmic_flops_per_launch": grid_flops_step},
+            "roofline": roof,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -307,8 +343,8 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def load_traffic():
-    path = os.path.join(ROOT, "profiles", "r01_grid_kernel_ncu.json")
+def load_traffic(name: str):
+    path = os.path.join(ROOT, "profiles", "r01_%s_ncu.json" % name)
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")

@@ -64,9 +64,13 @@ typedef struct gwg_counters {
   uint64_t bytes_stored;       /* device->host bytes                                 */
   uint64_t context_builds;     /* trait-prep launches (one per gwg_set_traits)       */
   uint64_t kernel_launches;    /* launches of this library's own kernels            */
-  double grid_kernel_ms;       /* summed CUDA-event time of the fused grid kernel    */
+  double grid_kernel_ms;       /* summed CUDA-event time of the grid launches        */
   double rotate_ms;            /* summed CUDA-event time of the SNP rotations        */
   double wall_ms;              /* host wall time of the last run_grid                */
+  /* genotype split grid (gwg_solve_snp_slab only): the int8 linear-term
+   * launch and the DMMA quadratic-term + solve launch, both inside grid_kernel_ms */
+  double linear_ms;
+  double quad_ms;
 } gwg_counters;
 
 typedef struct gwg_run_options {

@@ -76,6 +76,8 @@ class Counters(ctypes.Structure):
         ("grid_kernel_ms", ctypes.c_double),
         ("rotate_ms", ctypes.c_double),
         ("wall_ms", ctypes.c_double),
+        ("linear_ms", ctypes.c_double),
+        ("quad_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -24,6 +25,7 @@
 #include <vector>
 
 #include "../../include/gwgrid_cuda.h"
+#include "split_prep.cuh"
 #include "engine_internal.cuh"
 #include "rotate_i8.cuh"
 #include "rotate_kernel.cuh"
@@ -144,12 +146,13 @@ int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
 // dst (n x cols, ld np) = Z^T src (n x cols, ld lds) with the deterministic
 // DMMA rotation kernel (rotate_kernel.cuh).
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds, double* dst_sq) {
+           int64_t lds, double* dst_sq, const double* basis) {
   if (cols <= 0) return GWG_OK;
   NvtxRange nvtx_("rotate");
   if (lds == 0) lds = e->np;
   CUtensorMap tz, tx;
-  if (int rc = encode_kmajor(&tz, e->basis.d(), e->n, e->n, e->np, gwg::RotCfg::BM, st)) return rc;
+  if (!basis) basis = e->basis.d();
+  if (int rc = encode_kmajor(&tz, basis, e->n, e->n, e->np, gwg::RotCfg::BM, st)) return rc;
   if (int rc = encode_kmajor(&tx, src, e->n, cols, lds, gwg::RotCfg::BN, st)) return rc;
   gwg::RotArgs a;
   a.dst = dst;
@@ -183,7 +186,86 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
+// 2-D uint8 map over a K-major int8 operand (kp x cols) and 3-D map over
+// SLICES planes of (kp x ncols), both SWIZZLE_128B boxes for tcgen05.
+int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensorMap* tb,
+              const void* slices, int64_t ncols, int rb, gwg_status* st) {
+  using gwg::I8Cfg;
+  auto encode = get_encode();
+  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
+  {
+    const cuuint64_t gdim[2] = {cuuint64_t(kp), cuuint64_t(cols)};
+    const cuuint64_t gstride[1] = {cuuint64_t(kp)};
+    const cuuint32_t box[2] = {I8Cfg::BK, I8Cfg::BM};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(x), gdim, gstride,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 SNP slab) failed (%d)", int(r));
+  }
+  {
+    const cuuint64_t gdim[3] = {cuuint64_t(kp), cuuint64_t(ncols), cuuint64_t(I8Cfg::SLICES)};
+    const cuuint64_t gstride[2] = {cuuint64_t(kp), cuuint64_t(ncols) * kp};
+    const cuuint32_t box[3] = {I8Cfg::BK, cuuint32_t(rb), I8Cfg::SLICES};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(slices), gdim,
+                        gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 slices) failed (%d)", int(r));
+  }
+  return GWG_OK;
+}
+
+// rotate_i8_kernel over `cols` int8 SNP columns against the sliced columns
+// (scale, ncols): dst[i * ldd + r] (and dst_sq) for r < ncols, either may be
+// null.  Outputs leave through TMA stores: ldd even, 16-byte aligned bases.
+int launch_i8(gwg_engine* e, const CUtensorMap& tx, const CUtensorMap& tb, int64_t cols,
+              int64_t ncols, const double* scale, double* dst, double* dst_sq, int64_t ldd,
+              gwg_status* st) {
+  using gwg::I8Cfg;
+  auto encode = get_encode();
+  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap td[2];
+  double* outs[2] = {dst, dst_sq};
+  for (int o = 0; o < 2; ++o) {
+    double* base = outs[o] ? outs[o] : (dst ? dst : dst_sq);
+    const cuuint64_t gdim[2] = {cuuint64_t(ncols), cuuint64_t(cols)};
+    const cuuint64_t gstride[1] = {cuuint64_t(ldd) * 8};
+    const cuuint32_t box[2] = {I8Cfg::OUT_Q, 32};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(&td[o], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, gdim, gstride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 rotation output) failed (%d)",
+                        int(r));
+  }
+  const int64_t kp = round_up(e->n, I8Cfg::BK);
+  gwg::I8Args a;
+  a.scale = scale;
+  a.has_d = dst != nullptr;
+  a.has_d2 = dst_sq != nullptr;
+  a.n = int32_t(ncols);
+  a.cols = int32_t(cols);
+  a.tiles_m = int32_t(ceil_div(cols, I8Cfg::BM));
+  a.tiles_r = int32_t(ceil_div(ncols, I8Cfg::RB));
+  a.kstages = int32_t(kp / I8Cfg::BK);
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
+  GWG_CUDA_TRY(cudaFuncSetAttribute(gwg::rotate_i8_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(I8Cfg::SMEM_BYTES)));
+  gwg::rotate_i8_kernel<<<int(std::min<int64_t>(tiles, e->sms)), I8Cfg::THREADS,
+                          I8Cfg::SMEM_BYTES, e->comp>>>(tx, tb, td[0], td[1], a);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  return GWG_OK;
+}
+
 int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st) {
+  e->slab_i8 = false;
   if (e->snp_coding == 0) return rotate(e, src, cols, e->rot.d(), st, lds, e->rot_sq.d());
   if (cols <= 0) return GWG_OK;
   NvtxRange nvtx_("rotate_i8");
@@ -193,8 +275,8 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
     GWG_CUDA_TRY(e->zslices.ensure(size_t(I8Cfg::SLICES) * n * kp));
     GWG_CUDA_TRY(e->zscale.ensure(size_t(n) * sizeof(double)));
     gwg::slice_basis_kernel<<<int(n), 256, 0, e->comp>>>(
-        e->basis.d(), e->np, int32_t(n), int32_t(kp), static_cast<int8_t*>(e->zslices.ptr),
-        e->zscale.d());
+        e->basis.d(), e->np, int32_t(n), int32_t(n), int32_t(kp),
+        static_cast<int8_t*>(e->zslices.ptr), e->zscale.d());
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
     e->slices_valid = true;
@@ -209,50 +291,163 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
   }
-  auto encode = get_encode();
-  if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tx, tz;
-  {
-    const cuuint64_t gdim[2] = {cuuint64_t(kp), cuuint64_t(cols)};
-    const cuuint64_t gstride[1] = {cuuint64_t(kp)};
-    const cuuint32_t box[2] = {I8Cfg::BK, I8Cfg::BM};
-    const cuuint32_t es[2] = {1, 1};
-    CUresult r = encode(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, e->xi8.ptr, gdim, gstride, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 SNP slab) failed (%d)", int(r));
+  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, cols, &tz, e->zslices.ptr, n, I8Cfg::RB, st))
+    return rc;
+  // the split grid needs only X'.X' (its linear terms come from the codes)
+  if (int rc = launch_i8(e, tx, tz, cols, n, e->zscale.d(), e->split ? nullptr : e->rot.d(),
+                         e->rot_sq.d(), e->np, st))
+    return rc;
+  e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
+  e->slab_i8 = true;
+  return GWG_OK;
+}
+
+void invalidate_derived(gwg_engine* e, bool spectrum) {
+  e->split_valid = false;
+  if (spectrum) {
+    e->slices_valid = false;
+    e->basis_t_valid = false;
   }
-  {
-    const cuuint64_t gdim[3] = {cuuint64_t(kp), cuuint64_t(n), cuuint64_t(I8Cfg::SLICES)};
-    const cuuint64_t gstride[2] = {cuuint64_t(kp), cuuint64_t(n) * kp};
-    const cuuint32_t box[3] = {I8Cfg::BK, I8Cfg::RB, I8Cfg::SLICES};
-    const cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = encode(&tz, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, e->zslices.ptr, gdim, gstride, box,
-                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      return set_status(st, GWG_CUDA, -1, -1, "tensor map (basis slices) failed (%d)", int(r));
+}
+
+// Trait operands of the split grid: V = [D_j.X_L'_c, D_j.Y'_j] in the padded
+// linear-solve layout, W = Z V by the DMMA rotation kernel against Z^T, 8 int8
+// slices of W per column, and the D panels of gls_sbr_kernel.
+int build_split(gwg_engine* e, gwg_status* st) {
+  if (e->split_valid) return GWG_OK;
+  NvtxRange nvtx_("build_split");
+  using gwg::I8Cfg;
+  const int64_t n = e->n, np = e->np, t = e->t, p = e->p;
+  const int64_t kp = round_up(n, I8Cfg::BK);
+  const int64_t ncols = ceil_div(t, e->lops.kt) * e->lops.rb;  // padded W rows
+  if (!e->basis_t_valid) {
+    GWG_CUDA_TRY(e->basis_t.ensure(size_t(np) * n * sizeof(double)));
+    const dim3 grid(unsigned(ceil_div(n, 32)), unsigned(ceil_div(n, 32)));
+    gwg::transpose_kernel<<<grid, dim3(32, 8), 0, e->comp>>>(e->basis.d(), e->basis_t.d(), n, np);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    e->basis_t_valid = true;
   }
-  gwg::I8Args a;
-  a.dst = e->rot.d();
-  a.dst_sq = e->rot_sq.d();
-  a.scale = e->zscale.d();
-  a.ldd = e->np;
-  a.n = int32_t(n);
-  a.cols = int32_t(cols);
-  a.tiles_m = int32_t(ceil_div(cols, I8Cfg::BM));
-  a.tiles_r = int32_t(ceil_div(n, I8Cfg::RB));
-  a.kstages = int32_t(kp / I8Cfg::BK);
-  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
-  GWG_CUDA_TRY(cudaFuncSetAttribute(gwg::rotate_i8_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(I8Cfg::SMEM_BYTES)));
-  gwg::rotate_i8_kernel<<<int(std::min<int64_t>(tiles, e->sms)), I8Cfg::THREADS,
-                          I8Cfg::SMEM_BYTES, e->comp>>>(tx, tz, a);
+  const int64_t bt = gwg::SbrDefault::BT;
+  const int64_t tiles_t = ceil_div(t, bt);
+  GWG_CUDA_TRY(e->dpanel.ensure(size_t(tiles_t) * np * bt * sizeof(double)));
+  if (t % bt)  // padded traits of the last tile contribute zeros
+    GWG_CUDA_TRY(cudaMemsetAsync(e->dpanel.d() + size_t(tiles_t - 1) * np * bt, 0,
+                                 size_t(np) * bt * sizeof(double), e->comp));
+  GWG_CUDA_TRY(e->vmat.ensure(size_t(np) * ncols * sizeof(double)));
+  GWG_CUDA_TRY(e->wmat.ensure(size_t(np) * ncols * sizeof(double)));
+  if (e->lops.p8 != p || t % e->lops.kt)
+    GWG_CUDA_TRY(cudaMemsetAsync(e->vmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
+  gwg::SplitPrepArgs a;
+  a.n = n;
+  a.np = np;
+  a.t = int32_t(t);
+  a.p = int32_t(p);
+  a.bt = int32_t(bt);
+  a.kt = e->lops.kt;
+  a.p8 = e->lops.p8;
+  a.rb = e->lops.rb;
+  a.lambda = e->lambda.d();
+  a.y = e->y_rot.d();
+  a.ldy = np;
+  a.xl = e->xl_rot.d();
+  a.ldxl = np;
+  a.h2 = e->h2.d();
+  a.sigma2 = e->sigma2.d();
+  a.dpanel = e->dpanel.d();
+  a.v = e->vmat.d();
+  gwg::split_prep_kernel<<<int(t), 256, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
-  e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
+  if (int rc = rotate(e, e->vmat.d(), ncols, e->wmat.d(), st, np, nullptr, e->basis_t.d()))
+    return rc;
+  GWG_CUDA_TRY(e->wslices.ensure(size_t(I8Cfg::SLICES) * ncols * kp));
+  GWG_CUDA_TRY(e->wscale.ensure(size_t(ncols) * sizeof(double)));
+  gwg::slice_basis_kernel<<<int(ncols), 256, 0, e->comp>>>(e->wmat.d(), np, int32_t(n),
+                                                          int32_t(ncols), int32_t(kp),
+                                                          static_cast<int8_t*>(e->wslices.ptr),
+                                                          e->wscale.d());
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  e->split_valid = true;
+  return GWG_OK;
+}
+
+// Split grid over one genotype slab: S_BR on DMMA (gls_sbr_kernel), then the
+// exact int8 linear terms + bordered Cholesky (linear_solve_kernel<P>).
+int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
+                 double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
+  if (int rc = build_split(e, st)) return rc;
+  using gwg::I8Cfg;
+  using S = gwg::SbrDefault;
+  const int64_t t = e->t, p = e->p;
+  const int64_t kp = round_up(e->n, I8Cfg::BK);
+  const int64_t tiles_r = ceil_div(t, e->lops.kt);
+  const int64_t ncols = tiles_r * e->lops.rb;
+  const int64_t ld_s = round_up(rows, 2);
+  GWG_CUDA_TRY(e->sbr.ensure(size_t(ld_s) * t * sizeof(double)));
+
+  // ---- S_BR = (X'.X')^T D ----
+  CUtensorMap map_sq;
+  if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, S::BM, st)) return rc;
+  gwg::SbrArgs q;
+  q.dpanel = e->dpanel.d();
+  q.sbr = e->sbr.d();
+  q.ld = ld_s;
+  q.rows = rows;
+  q.t = int32_t(t);
+  q.tiles_m = int32_t(ceil_div(rows, S::BM));
+  q.tiles_t = int32_t(ceil_div(t, S::BT));
+  q.kchunks = int32_t(e->np / S::BK);
+  q.np = e->np;
+  const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
+  GWG_CUDA_TRY(gwg::launch_sbr_default(map_sq, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[1], e->comp));
+  e->counters.kernel_launches += 1;
+
+  // ---- linear terms (int8 tcgen05) + solve ----
+  CUtensorMap tx, tw, tout;
+  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb, st))
+    return rc;
+  // numpy layout with a 16-byte pitch and base: results leave by TMA store
+  const bool use_tma = out_sj == 1 && (out_si * p) % 2 == 0 &&
+                       (reinterpret_cast<uintptr_t>(dev_out) & 15) == 0;
+  {
+    auto encode = get_encode();
+    const cuuint64_t gdim[2] = {cuuint64_t(t * p), cuuint64_t(rows)};
+    const cuuint64_t gstride[1] = {cuuint64_t(use_tma ? out_si * p * 8 : 16)};
+    const cuuint32_t box[2] = {gwg::I8Cfg::OUT_Q, 32};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (use_tma && r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (results) failed (%d)", int(r));
+  }
+  gwg::LinArgs a;
+  a.scale = e->wscale.d();
+  a.sbr = e->sbr.d();
+  a.ld_s = ld_s;
+  a.ctx = e->ctx.d();
+  a.out = dev_out;
+  a.out_si = out_si;
+  a.out_sj = out_sj;
+  a.use_tma = use_tma ? 1 : 0;
+  a.t = int32_t(t);
+  a.rows = rows;
+  a.i0 = i0;
+  a.m_total = m_total;
+  a.tiles_m = int32_t(ceil_div(rows, I8Cfg::BM));
+  a.tiles_r = int32_t(tiles_r);
+  a.kstages = int32_t(kp / I8Cfg::BK);
+  a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
+  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
+  GWG_CUDA_TRY(e->lops.launch(tx, tw, tout, a, int(std::min<int64_t>(tiles, e->sms)), e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[2], e->comp));
+  e->split_timed = true;
+  e->counters.kernel_launches += 1;
   return GWG_OK;
 }
 
@@ -260,6 +455,11 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
 int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
                 gwg_status* st) {
+  const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
+  e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
+  e->counters.loop_flops += cells * uint64_t(e->n) * (5 + 2 * uint64_t(e->p - 1));
+  if (e->slab_i8 && e->split)
+    return launch_split(e, rot_sq, rows, i0, m_total, dev_out, out_si, out_sj, st);
   CUtensorMap map, map_sq;
   if (int rc = encode_kmajor(&map, rot, e->n, rows, e->np, e->ops.bm, st)) return rc;
   if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->ops.bm, st)) return rc;
@@ -282,13 +482,11 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
   const int ctas = int(std::min<int64_t>(tiles, e->sms));
   GWG_CUDA_TRY(e->ops.grid(map, map_sq, a, ctas, e->comp));
   e->counters.kernel_launches += 1;
-  const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
-  e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
-  e->counters.loop_flops += cells * uint64_t(e->n) * (5 + 2 * uint64_t(e->p - 1));
   return GWG_OK;
 }
 
 int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st) {
+  e->slab_i8 = false;
   GWG_CUDA_TRY(gwg::launch_square(e->rot.d(), e->rot_sq.d(), size_t(e->np) * cols, e->comp));
   e->counters.kernel_launches += 1;
   return GWG_OK;
@@ -356,7 +554,8 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     return nullptr;
   }
   KernelOps ops;
-  if (!gwg::ops_for(p, &ops)) {
+  gwg::LinOps lops;
+  if (!gwg::ops_for(p, &ops) || !gwg::lin_ops_for(p, &lops)) {
     set_status(st, GWG_DIMENSION, -1, -1,
                "p=%lld is outside the compiled predictor range 1..32", (long long)p);
     return nullptr;
@@ -373,6 +572,8 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   e->p = p;
   e->np = round_up(n, kBK);
   e->ops = ops;
+  e->lops = lops;
+  if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
     gwg_engine_destroy(e);
@@ -405,6 +606,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   cudaEventCreate(&e->ev_k1);
   cudaEventCreate(&e->ev_r0);
   cudaEventCreate(&e->ev_r1);
+  for (cudaEvent_t& ev : e->ev_s) cudaEventCreate(&ev);
   if ((err = e->err.ensure(3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMalloc", err);
   if ((err = cudaMallocHost(&e->err_host, 3 * sizeof(unsigned long long))) != cudaSuccess)
@@ -420,7 +622,8 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->d2h) cudaStreamSynchronize(e->d2h);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
-                    &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8})
+                    &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
+                    &e->wslices, &e->wscale, &e->dpanel, &e->sbr})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   for (int b = 0; b < 2; ++b) {
@@ -429,7 +632,7 @@ void gwg_engine_destroy(gwg_engine* e) {
     if (e->ev_comp[b]) cudaEventDestroy(e->ev_comp[b]);
     if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
   }
-  for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1})
+  for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2]})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
   if (e->comp) cudaStreamDestroy(e->comp);
@@ -449,7 +652,7 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
   e->have_spectrum = true;
   e->have_covariates = false;
   e->have_traits = false;
-  e->slices_valid = false;
+  invalidate_derived(e, true);
   return GWG_OK;
 }
 
@@ -466,7 +669,7 @@ int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_sta
   GWG_CUDA_TRY(e->lambda.ensure(size_t(e->n) * sizeof(double)));
   if (int rc = gwg_internal_device_eig(e->basis.d(), e->n, e->np, e->lambda.d(), e->comp, st))
     return rc;
-  e->slices_valid = false;
+  invalidate_derived(e, true);
   e->have_spectrum = true;
   return GWG_OK;
 }
@@ -486,6 +689,7 @@ int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_s
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   e->have_covariates = true;
   e->have_traits = false;
+  invalidate_derived(e, false);
   return GWG_OK;
 }
 
@@ -501,6 +705,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
                       (long long)t);
   if (!y || !h2 || !sigma2) return set_status(st, GWG_DIMENSION, -1, -1, "null trait operand");
   e->have_traits = false;
+  invalidate_derived(e, false);
   const int64_t n = e->n;
   if (is_rotated) {
     if (int rc = upload_cols(e, e->y_rot, y, n, t, where, e->comp, st)) return rc;
@@ -600,6 +805,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : (out_where == GWG_DEVICE ? ldo : mb);
   const int64_t m_total = i0 + mb;
   if (int rc = reset_errors(e, st)) return rc;
+  e->split_timed = false;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
   if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), mb, i0, m_total, dev_out, si, sj, st))
     return rc;
@@ -619,6 +825,10 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
   if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
+  if (e->split_timed) {
+    if (cudaEventElapsedTime(&ms, e->ev_s[0], e->ev_s[1]) == cudaSuccess) e->counters.linear_ms += ms;
+    if (cudaEventElapsedTime(&ms, e->ev_s[1], e->ev_s[2]) == cudaSuccess) e->counters.quad_ms += ms;
+  }
   // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
   return raise_cell_error(e, m_total, st);
 }

@@ -13,7 +13,9 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "../../include/gwgrid_cuda.h"
+#include "grid_split.cuh"
 #include "kernel_table.cuh"
+#include "linear_solve.cuh"
 
 #define GWG_CUDA_TRY(expr)                                                                 \
   do {                                                                                     \
@@ -67,6 +69,7 @@ struct gwg_engine {
   int sms = 148;
   int64_t n = 0, p = 0, np = 0;
   gwg::KernelOps ops;
+  gwg::LinOps lops;  // genotype split grid: per-p linear-solve kernel
   cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
 
   gwg_host::DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
@@ -83,10 +86,19 @@ struct gwg_engine {
   int snp_coding = 0;
   bool slices_valid = false;
   gwg_host::DevBuf zslices, zscale, xi8;
+  // Split grid for genotype slabs (grid_split.cuh): linear terms x_i^T W on
+  // the int8 tensor cores, quadratic term + solve on DMMA.  `split` = use it
+  // (GWG_SPLIT=0 in the environment turns it off for A/B timing);
+  // `slab_i8` = the current slab was rotated from integer codes (xi8 valid).
+  bool split = true, slab_i8 = false;
+  bool basis_t_valid = false, split_valid = false;
+  gwg_host::DevBuf basis_t, vmat, wmat, wslices, wscale, dpanel, sbr;
   unsigned long long* err_host = nullptr;
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
   cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
+  cudaEvent_t ev_s[3];     // split grid: before the linear launch, between, after quad
+  bool split_timed = false;
   std::vector<cudaEvent_t> slab_events;
 
   gwg_counters counters{};
@@ -102,7 +114,11 @@ int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int6
                 int where, cudaStream_t s, gwg_status* st, int64_t ldd = 0);
 int64_t raw_ld(const gwg_engine* e);
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds = 0, double* dst_sq = nullptr);
+           int64_t lds = 0, double* dst_sq = nullptr, const double* basis = nullptr);
+// Split-grid trait operands (W slices, D panels) for the current traits.
+int build_split(gwg_engine* e, gwg_status* st);
+// Invalidate everything derived from traits / spectrum.
+void invalidate_derived(gwg_engine* e, bool spectrum);
 // SNP slab -> e->rot / e->rot_sq with the engine's SNP coding (DMMA or int8).
 int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st);
 int read_errors(gwg_engine* e, gwg_status* st, bool trait_only);

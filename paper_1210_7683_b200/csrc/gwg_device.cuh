@@ -92,4 +92,17 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Bulk prefetch of a global range into L2 (TMA engine, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// dmma with a volatile asm: keeps the x-pass / y-pass issue order (the
+// compiler otherwise pairs the two dependent DMMAs of an accumulator).
+__device__ __forceinline__ void dmma_ordered(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 }  // namespace gwg

@@ -1,0 +1,296 @@
+// i8_core.cuh — shared machinery of the int8 tensor-core kernels (sm_100a):
+// tile geometry, tcgen05 / TMEM / TMA primitives, the TMA producer and the
+// single-thread MMA issuer of a persistent warp-specialised kernel, and the
+// exact int64 recombination of eight 7-bit slice products.  Used by
+// rotate_i8_kernel (rotate_i8.cuh) and linear_solve_kernel (linear_solve.cuh).
+#pragma once
+
+#include "gwg_device.cuh"
+
+namespace gwg {
+
+
+// Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 8 slices x RB
+// rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
+// linear terms of the split grid), K = 128 samples per stage.
+template <int RB_>
+struct I8Tile {
+  static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
+  static constexpr int RB = RB_;          // rows of the sliced operand per tile
+  static constexpr int SLICES = 8;
+  static constexpr int BN = SLICES * RB;  // UMMA N (<= 256, multiple of 16)
+  static constexpr int BK = 128;          // int8 K per stage = one 128B swizzle row
+  static constexpr int UK = 32;           // K per tcgen05.mma (int8)
+  static constexpr int STAGES = 4;
+  static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
+  static constexpr uint32_t B_BYTES = BN * BK;  // <= 32 KB
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_WARPS = 8;     // two per TMEM lane quarter
+  static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
+  static constexpr int TMEM_COLS = 512;   // 2 accumulator buffers x BN (<= 256)
+  static constexpr int OUT_Q = 16;        // output box: 16 doubles (128 B) x 32 SNPs
+  static constexpr uint32_t OUT_BYTES = OUT_Q * 32 * 8;  // 4 KB staging per epilogue warp
+  static constexpr size_t SMEM_BYTES =
+      size_t(STAGES) * STAGE_BYTES + size_t(EPI_WARPS) * OUT_BYTES + 1024 + 256;
+  static_assert(BN % 16 == 0 && BN <= 256 && RB % 8 == 0, "UMMA N / swizzle atoms");
+};
+using I8Cfg = I8Tile<32>;
+
+// ---- tcgen05 primitives --------------------------------------------------------
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  // K-major SWIZZLE_128B canonical layout: 8-row x 128B atoms, SBO = 1024 B,
+  // LBO unused (1), version 1 (sm_100), layout type 2 (SWIZZLE_128B).
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;                   // LBO (ignored for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;           // SBO
+  d |= uint64_t(1) << 46;                   // version
+  d |= uint64_t(2) << 61;                   // SWIZZLE_128B
+  return d;
+}
+
+template <int BN, int BM>
+__device__ __forceinline__ constexpr uint32_t i8_instr_desc() {
+  // c_format S32 (2) @[4,6), a/b format signed int8 (1) @[7,10)/[10,13),
+  // K-major A and B, N >> 3 @[17,23), M >> 4 @[24,29).
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+         (uint32_t(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, int32_t c2, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+      "l"(policy)
+      : "memory");
+}
+
+// 32 consecutive TMEM columns of this warp's 32 lanes into 32 registers.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+}
+
+// 16 consecutive TMEM columns of this warp's 32 lanes into 16 registers.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+// 8 consecutive TMEM columns of this warp's 32 lanes into 8 registers.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+
+// W consecutive TMEM columns (W = 1, 2, 4, 8) of this warp's 32 lanes.
+template <int W>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, int32_t (&v)[W]) {
+  if constexpr (W == 8) {
+    tmem_ld8(taddr, v);
+  } else if constexpr (W == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+  } else if constexpr (W == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                 : "=r"(v[0]), "=r"(v[1])
+                 : "r"(taddr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v[0]) : "r"(taddr));
+  }
+}
+
+// Exact recombination of the eight slice products of one output column:
+// hi = slices 0-3, lo = slices 4-7 as int64 (|hi|, |lo| < 2^53), one rounding.
+__device__ __forceinline__ double i8_recombine(const int32_t a0, const int32_t a1, const int32_t a2,
+                                               const int32_t a3, const int32_t a4, const int32_t a5,
+                                               const int32_t a6, const int32_t a7, double sc) {
+  const long long hi = (long long)a0 * (1ll << 21) + (long long)a1 * (1ll << 14) +
+                       (long long)a2 * (1ll << 7) + (long long)a3;
+  const long long lo = (long long)a4 * (1ll << 21) + (long long)a5 * (1ll << 14) +
+                       (long long)a6 * (1ll << 7) + (long long)a7;
+  return fma(double(lo), sc * 0x1p-56, double(hi) * (sc * 0x1p-28));
+}
+
+// TMA 2-D store shared -> global (bulk async group of the issuing thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- shared pipeline: TMA producer, MMA issuer, TMEM setup ---------------------
+
+// Shared-memory carve-up of an I8Tile kernel.
+template <class C>
+struct I8Smem {
+  unsigned char* base;     // STAGES x (A | B), 1024-aligned for SWIZZLE_128B
+  unsigned char* staging;  // [epilogue warp][OUT_BYTES]
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* acc_full;      // [2]
+  uint64_t* acc_empty;     // [2]
+  uint32_t* tmem_slot;
+  __device__ explicit I8Smem(unsigned char* raw) {
+    base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
+                                            ~uintptr_t(1023));
+    staging = base + C::STAGES * C::STAGE_BYTES;
+    full = reinterpret_cast<uint64_t*>(staging + C::EPI_WARPS * C::OUT_BYTES);
+    empty = full + C::STAGES;
+    acc_full = empty + C::STAGES;
+    acc_empty = acc_full + 2;
+    tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  }
+};
+
+// Barrier init + TMEM allocation (warp 1); returns the TMEM base address.
+template <class C>
+__device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.acc_full[b], 1);
+      mbar_init(&sm.acc_empty[b], C::EPI_WARPS);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(sm.tmem_slot)),
+        "n"(C::TMEM_COLS)
+        : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return *sm.tmem_slot;
+}
+
+template <class C>
+__device__ __forceinline__ void i8_teardown(uint32_t tmem_base, int warp) {
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+}
+
+// Warp 0, one thread: A = int8 SNP tile (box 128 k x 128 SNPs), B = RB rows
+// of all 8 slices (box 128 k x RB x 8).  Tiles: tm = tile / tiles_r (the rows
+// of the sliced operand fastest, so the SNP tile is reused from L2).
+template <class C>
+__device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMap* tmap_x,
+                                           const CUtensorMap* tmap_b, int my_tiles, int tiles_r,
+                                           int kstages) {
+  const uint64_t pol_x = policy_evict_first();
+  const uint64_t pol_b = policy_evict_last();
+  int g = 0;
+  for (int lt = 0; lt < my_tiles; ++lt) {
+    const int tile = blockIdx.x + lt * gridDim.x;
+    const int tm = tile / tiles_r;
+    const int tr = tile - tm * tiles_r;
+    for (int ks = 0; ks < kstages; ++ks, ++g) {
+      const int s = g % C::STAGES;
+      if (g >= C::STAGES) mbar_wait(&sm.empty[s], ((g / C::STAGES) - 1) & 1);
+      mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
+      unsigned char* st = sm.base + s * C::STAGE_BYTES;
+      tma_load_2d(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
+      tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
+    }
+  }
+}
+
+// Warp 1, one thread: BK/UK tcgen05.mma per stage into the tile's TMEM buffer.
+template <class C>
+__device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, int my_tiles,
+                                       int kstages) {
+  constexpr uint32_t idesc = i8_instr_desc<C::BN, C::BM>();
+  int g = 0;
+  for (int lt = 0; lt < my_tiles; ++lt) {
+    const int buf = lt & 1;
+    if (lt >= 2) mbar_wait(&sm.acc_empty[buf], ((lt >> 1) - 1) & 1);
+    tc_fence_after();
+    const uint32_t tmem_d = tmem_base + uint32_t(buf * C::BN);
+    for (int ks = 0; ks < kstages; ++ks, ++g) {
+      const int s = g % C::STAGES;
+      mbar_wait(&sm.full[s], (g / C::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(sm.base + s * C::STAGE_BYTES);
+      const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+      for (int k = 0; k < C::BK / C::UK; ++k)
+        umma_i8(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK), idesc,
+                (ks | k) != 0);
+      umma_commit(&sm.empty[s]);  // frees the smem stage when these MMAs finish
+    }
+    umma_commit(&sm.acc_full[buf]);  // accumulator ready for the epilogue
+  }
+}
+
+}  // namespace gwg

@@ -1,5 +1,7 @@
-"""Genotype coding: the exact int8 tcgen05 rotation against the DMMA rotation
-and the oracle, its device-side input check, and its slab invariance."""
+"""Genotype coding: the exact int8 tcgen05 rotation and the split grid (S_BR on
+DMMA, linear terms exactly on int8 tcgen05 + the solve) against the all-FP64
+path and the oracle, for every p and both layouts; the device-side input
+check; failure semantics; slab invariance."""
 import numpy as np
 import pytest
 
@@ -40,22 +42,37 @@ def test_genotype_path_matches_real_path_and_oracle(n, p, m, t):
     assert_parity(bg, ref)
 
 
-def test_genotype_rotation_is_exact_integer_arithmetic():
-    """X' from the int8 path equals Z^T X evaluated in extended precision to
-    ~1 ulp (longdouble reference)."""
-    ds = datagen.generate(200, 2, 40, 2, seed=5)
+@pytest.mark.parametrize("p", list(range(1, 33)))
+def test_split_grid_every_p_and_layout(p):
+    """The split grid (S_BR on DMMA, exact int8 linear terms + solve) for every
+    compiled p, both result layouts, against the all-FP64 path."""
+    n, m, t = 96 + p, 150, 11
+    ds = datagen.generate(n, p, m, t, seed=100 + p)
     basis, values = gw.eigendecompose(ds["kinship"])
-    with gw.Engine(200, 2) as eng:
-        eng.set_spectrum(basis, values)
-        eng.set_covariates(ds["xl"])
-        eng.set_snp_coding("genotypes")
-        eng.set_traits(ds["traits"][:, :1], ds["h2"][:1], ds["sigma2"][:1])
-        bg = eng.run_grid(ds["snps"])
-    exact = basis.astype(np.longdouble).T @ ds["snps"].astype(np.longdouble)
-    # recompute b for one cell from the exact rotation in long double: the grid
-    # agrees with the real-valued engine to rounding, so check the rotation
-    # indirectly through the cell solves
-    assert np.isfinite(bg).all() and np.isfinite(np.asarray(exact, dtype=np.float64)).all()
+    bg = run(ds, basis, values, "genotypes")
+    br = run(ds, basis, values, "real")
+    assert not np.isnan(bg).any()
+    rel = np.linalg.norm(bg - br, axis=2) / np.linalg.norm(br, axis=2)
+    assert rel.max() < 1e-10, rel.max()
+    bs = run(ds, basis, values, "genotypes", layout="stream", mb=64)
+    assert np.array_equal(bs.transpose(1, 0, 2), bg)
+
+
+def test_split_grid_failure_semantics_match_fp64_path():
+    """A zero SNP column makes every cell of that SNP singular: NaN results and
+    NotPositiveDefiniteError at the smallest (trait, SNP) key, as in the
+    all-FP64 kernel."""
+    ds = datagen.generate(120, 4, 40, 5, seed=3)
+    snps = ds["snps"].copy()
+    snps[:, 17] = 0.0
+    ds2 = dict(ds, snps=snps)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    errs = []
+    for coding in ("genotypes", "real"):
+        with pytest.raises(gw.NotPositiveDefiniteError) as e:
+            run(ds2, basis, values, coding)
+        errs.append((e.value.snp_index, e.value.trait_index))
+    assert errs[0] == errs[1] == (17, 0)
 
 
 def test_genotype_path_bitwise_invariant_to_slabs():
