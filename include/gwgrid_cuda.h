@@ -67,8 +67,9 @@ typedef struct gwg_counters {
   double grid_kernel_ms;       /* summed CUDA-event time of the grid launches        */
   double rotate_ms;            /* summed CUDA-event time of the SNP rotations        */
   double wall_ms;              /* host wall time of the last run_grid                */
-  /* genotype split grid (gwg_solve_snp_slab only): the int8 linear-term
-   * launch and the DMMA quadratic-term + solve launch, both inside grid_kernel_ms */
+  /* genotype split grid (gwg_solve_snp_slab only), both inside grid_kernel_ms:
+   * linear_ms = int8 linear terms + Cholesky solve (linear_solve_kernel),
+   * quad_ms = S_BR = (X'.X')^T D on DMMA (gls_sbr_kernel) */
   double linear_ms;
   double quad_ms;
 } gwg_counters;

@@ -826,8 +826,9 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
   if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
   if (e->split_timed) {
-    if (cudaEventElapsedTime(&ms, e->ev_s[0], e->ev_s[1]) == cudaSuccess) e->counters.linear_ms += ms;
-    if (cudaEventElapsedTime(&ms, e->ev_s[1], e->ev_s[2]) == cudaSuccess) e->counters.quad_ms += ms;
+    // ev_s: [0] before gls_sbr_kernel, [1] before linear_solve_kernel, [2] after
+    if (cudaEventElapsedTime(&ms, e->ev_s[0], e->ev_s[1]) == cudaSuccess) e->counters.quad_ms += ms;
+    if (cudaEventElapsedTime(&ms, e->ev_s[1], e->ev_s[2]) == cudaSuccess) e->counters.linear_ms += ms;
   }
   // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
   return raise_cell_error(e, m_total, st);

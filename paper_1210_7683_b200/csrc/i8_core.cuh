@@ -205,8 +205,10 @@ struct I8Smem {
 };
 
 // Barrier init + TMEM allocation (warp 1); returns the TMEM base address.
+// acc_arrivals = epilogue warps that release each accumulator buffer.
 template <class C>
-__device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp) {
+__device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp,
+                                             int acc_arrivals = C::EPI_WARPS) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -214,7 +216,7 @@ __device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp) {
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.acc_full[b], 1);
-      mbar_init(&sm.acc_empty[b], C::EPI_WARPS);  // one arrive per epilogue warp
+      mbar_init(&sm.acc_empty[b], acc_arrivals);  // one arrive per epilogue warp using it
     }
     fence_mbar_init();
   }

@@ -9,7 +9,8 @@
 // columns padded to P8 (a power of two <= 8, else a multiple of 8) so that a
 // trait's columns are one aligned tcgen05.ld.
 //
-// Epilogue (8 warps, two per TMEM lane quarter; thread = SNP row): per cell
+// Epilogue (8 warps, two per TMEM lane quarter taking alternate tiles; thread
+// = SNP row): per cell
 // (i, j) the p linear terms x_i^T W_{j,c} are recombined exactly from the
 // eight slice products (i8_recombine, one rounding), S_BR[j][i] comes from
 // gls_sbr_kernel (prefetched before the accumulator wait), and solve_cell<P>
@@ -30,10 +31,14 @@ struct LinCfg {
   static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
   static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
   using Tile = I8Tile<RB>;
-  static constexpr int HALVES = KT >= 2 ? 2 : 1;          // epilogue warps per lane quarter in use
-  static constexpr int CELLS = KT >= 2 ? KT / 2 : 1;      // cells per epilogue thread per tile
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
-  static constexpr bool TMA_OUT = CELLS * P == Tile::OUT_Q;  // a 128-byte row per thread
+  static constexpr int ROW = KT * P;                      // results per SNP row per tile
+  static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
+  static constexpr bool TMA_OUT = ROW % CHUNK == 0;       // whole 128-byte chunks
+  // cells solved together (independent chains; KT is a power of two or 1)
+  static constexpr int GMAX = P <= 4 ? 4 : (P <= 16 ? 2 : 1);
+  static constexpr int GROUP = KT < GMAX ? KT : GMAX;
+  static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
 };
 
 struct LinArgs {
@@ -63,117 +68,137 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
   using L = LinCfg<P>;
   using C = typename L::Tile;
   using CX = CtxLayout<P>;
-  constexpr int CELLS = L::CELLS;
   extern __shared__ __align__(1024) unsigned char smem_ls[];
   const I8Smem<C> sm(smem_ls);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.tiles_m * a.tiles_r;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint32_t tmem_base = i8_setup<C>(sm, warp);
+  const uint32_t tmem_base = i8_setup<C>(sm, warp, 4);  // one warp per quarter per tile
 
   if (warp == 0) {
     if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, my_tiles, a.tiles_r, a.kstages);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
   } else if (warp >= 4) {
+    // warp w owns TMEM lane quarter w % 4; the two warps of a quarter take
+    // alternate tiles (= alternate accumulator buffers), each doing all KT
+    // cells of its tile, so two tiles' epilogues are in flight per quarter.
     const int ew = warp - 4;
     const int qd = warp & 3;
     const int h = ew >> 2;
-    const bool active = h < L::HALVES;
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
-    for (int lt = 0; lt < my_tiles; ++lt) {
+    for (int lt = h; lt < my_tiles; lt += 2) {
       const int buf = lt & 1;
       const int tile = blockIdx.x + lt * gridDim.x;
       const int tm = tile / a.tiles_r;
       const int tr = tile - tm * a.tiles_r;
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
       const bool iv = il < a.rows;
-      const int j0 = tr * L::KT + h * CELLS;  // first trait of this warp
-      double sbr[CELLS];
+      const int j0 = tr * L::KT;  // first trait of the tile
+      double sbr[L::KT];
 #pragma unroll
-      for (int cc = 0; cc < CELLS; ++cc) {
+      for (int cc = 0; cc < L::KT; ++cc) {
         const int j = j0 + cc;
-        sbr[cc] = (active && iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
+        sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
       }
+      // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
+      // to the recombination below: no per-column memory round trip
+      const double sc_lane = lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
       mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
       tc_fence_after();
-      double lin[CELLS][P];
-      if (active) {
-        const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
+      const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
+      const bool tma = L::TMA_OUT && a.use_tma;
+      // GROUP cells at a time: recombine their linear terms from TMEM (PAIR
+      // cells per TMEM round trip), release TMEM after the last group, then
+      // solve the group's independent cells together and store them
 #pragma unroll
-        for (int cc = 0; cc < CELLS; ++cc) {
-          const int col0 = (h * CELLS + cc) * L::P8;
+      for (int g0 = 0; g0 < L::KT; g0 += L::GROUP) {
+        double lin[L::GROUP][P];
+#pragma unroll
+        for (int u0 = 0; u0 < L::GROUP; u0 += L::PAIR) {
 #pragma unroll
           for (int c0 = 0; c0 < P; c0 += L::CW) {
-            int32_t v[C::SLICES][L::CW];
+            int32_t v[L::PAIR][C::SLICES][L::CW];
 #pragma unroll
-            for (int sl = 0; sl < C::SLICES; ++sl)
-              tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + col0 + c0), v[sl]);
+            for (int u = 0; u < L::PAIR; ++u)
+#pragma unroll
+              for (int sl = 0; sl < C::SLICES; ++sl)
+                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (g0 + u0 + u) * L::P8 + c0),
+                                v[u][sl]);
             tmem_ld_wait();
 #pragma unroll
-            for (int r = 0; r < L::CW; ++r) {
-              if (c0 + r < P) {
-                const double sc = __ldg(a.scale + tr * C::RB + col0 + c0 + r);
-                lin[cc][c0 + r] = i8_recombine(v[0][r], v[1][r], v[2][r], v[3][r], v[4][r],
-                                               v[5][r], v[6][r], v[7][r], sc);
+            for (int u = 0; u < L::PAIR; ++u)
+#pragma unroll
+              for (int r = 0; r < L::CW; ++r) {
+                if (c0 + r < P) {
+                  const double sc =
+                      __shfl_sync(0xffffffffu, sc_lane, (g0 + u0 + u) * L::P8 + c0 + r);
+                  lin[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
+                                                     v[u][3][r], v[u][4][r], v[u][5][r],
+                                                     v[u][6][r], v[u][7][r], sc);
+                }
               }
-            }
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for the next tile
-      if (!active) continue;
-
-      // ---- bordered Cholesky per cell (FP64 pipe; no DMMA in this kernel) ----
-      double beta[CELLS][P];
+        if (g0 + L::GROUP >= L::KT) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for tile lt + 2
+        }
+        double beta[L::GROUP][P];
+        bool ok[L::GROUP];
 #pragma unroll
-      for (int cc = 0; cc < CELLS; ++cc) {
-        const int j = j0 + cc;
-        if (j < a.t && iv) {
+        for (int u = 0; u < L::GROUP; ++u) {
+          const int j = j0 + g0 + u;
+          const bool cv = j < a.t && iv;
           double cell[P + 1];
 #pragma unroll
-          for (int c = 0; c < P; ++c) cell[c] = lin[cc][c];
-          cell[P] = sbr[cc];
-          const bool ok = solve_cell<P>(cell, a.ctx + size_t(j) * CX::STRIDE, beta[cc]);
-          if (!ok) {
+          for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
+          cell[P] = sbr[g0 + u];
+          ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
+        }
+#pragma unroll
+        for (int u = 0; u < L::GROUP; ++u) {
+          if (!ok[u]) {
+            const int j = j0 + g0 + u;
             atomicMin(a.err_key, (unsigned long long)(int64_t(j) * a.m_total + a.i0 + il));
 #pragma unroll
-            for (int c = 0; c < P; ++c) beta[cc][c] = __longlong_as_double(0x7ff8000000000000LL);
+            for (int c = 0; c < P; ++c) beta[u][c] = __longlong_as_double(0x7ff8000000000000LL);
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < P; ++c) beta[cc][c] = 0.0;
         }
-      }
-      bool stored = false;
-      if constexpr (L::TMA_OUT) {
-        if (a.use_tma) {
-          stored = true;
-          if (lane == 0) bulk_wait_read0();  // the previous store has left the staging tile
-          __syncwarp();
+        if (tma) {
+          // flat index f = (g0+u)*P + c of this row; 128-byte chunks of 16
+          // doubles, 16-byte units XOR-swizzled by row (SWIZZLE_128B), one
+          // TMA store per chunk
 #pragma unroll
-          for (int ch = 0; ch < C::OUT_Q / 2; ++ch) {
-            const int f = 2 * ch;
-            double2 w;
-            w.x = beta[f / P][f % P];
-            w.y = beta[(f + 1) / P][(f + 1) % P];
-            *reinterpret_cast<double2*>(stg + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) {
+              const int f = (g0 + u) * P + c;
+              if (f % L::CHUNK == 0) {  // starting a chunk: the staging tile must be free
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+              }
+              const int q = (f % L::CHUNK) >> 1;
+              *reinterpret_cast<double*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4) +
+                                         (f & 1) * 8) = beta[u][c];
+              if (f % L::CHUNK == L::CHUNK - 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0)
+                  tma_store_2d(&tmap_out, stg, j0 * P + (f / L::CHUNK) * L::CHUNK,
+                               tm * C::BM + qd * 32);
+              }
+            }
+        } else if (iv) {
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u) {
+            const int j = j0 + g0 + u;
+            if (j >= a.t) continue;
+            double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
+#pragma unroll
+            for (int c = 0; c < P; ++c) __stcs(dst + c, beta[u][c]);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) tma_store_2d(&tmap_out, stg, j0 * P, tm * C::BM + qd * 32);
-        }
-      }
-      if (!stored && iv) {
-#pragma unroll
-        for (int cc = 0; cc < CELLS; ++cc) {
-          const int j = j0 + cc;
-          if (j >= a.t) continue;
-          double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
-#pragma unroll
-          for (int c = 0; c < P; ++c) __stcs(dst + c, beta[cc][c]);
         }
       }
     }
