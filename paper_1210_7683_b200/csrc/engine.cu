@@ -283,8 +283,7 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   }
   GWG_CUDA_TRY(e->xi8.ensure(size_t(cols) * kp));
   {
-    const int64_t total = cols * kp;
-    const int blocks = int(std::min<int64_t>((total + 255) / 256, int64_t(e->sms) * 16));
+    const int blocks = int(std::min<int64_t>(cols, int64_t(e->sms) * 16));
     gwg::snp_to_i8_kernel<<<blocks, 256, 0, e->comp>>>(
         src, lds, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
         static_cast<unsigned long long*>(e->err.ptr) + 2);

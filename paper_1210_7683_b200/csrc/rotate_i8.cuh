@@ -122,26 +122,35 @@ __global__ void __launch_bounds__(I8Cfg::THREADS, 1)
 // ---- slab / basis preparation ------------------------------------------------------
 
 // X (n x cols, ld lds, f64 genotype codes) -> int8 [col][kp] with zero padding;
-// flags (*bad = 0) any value that is not an integer in [-127, 127].
-__global__ void snp_to_i8_kernel(const double* __restrict__ x, int64_t lds, int32_t n,
-                                 int32_t cols, int32_t kp, int8_t* __restrict__ out,
-                                 unsigned long long* __restrict__ bad) {
-  const int64_t total = int64_t(cols) * kp;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t c = idx / kp;
-    const int k = int(idx - c * kp);
-    int8_t q = 0;
-    if (k < n) {
-      const double v = x[c * lds + k];
-      if (!(v == rint(v)) || !(fabs(v) <= 127.0)) {
-        *bad = 0;  // error words are reset to all ones
-      } else {
-        q = int8_t(v);
+// flags (*bad = 0) any value that is not an integer in [-127, 127].  HBM-bound
+// (8 bytes in, 1 out per code): blocks stride over columns, each thread turns
+// one 16-byte pair of codes into 2 bytes, so loads and stores are contiguous
+// across the warp (lds is even: 16-byte aligned columns).
+__global__ void __launch_bounds__(256) snp_to_i8_kernel(const double* __restrict__ x, int64_t lds,
+                                                        int32_t n, int32_t cols, int32_t kp,
+                                                        int8_t* __restrict__ out,
+                                                        unsigned long long* __restrict__ bad) {
+  bool ok = true;
+  const int pairs = kp >> 1;
+  for (int c = blockIdx.x; c < cols; c += gridDim.x) {
+    const double2* col = reinterpret_cast<const double2*>(x + int64_t(c) * lds);
+    uint16_t* dst = reinterpret_cast<uint16_t*>(out + int64_t(c) * kp);
+    for (int k2 = threadIdx.x; k2 < pairs; k2 += blockDim.x) {
+      const int k = 2 * k2;
+      double2 v = make_double2(0.0, 0.0);
+      if (k + 1 < n) {
+        v = __ldcs(col + k2);
+      } else if (k < n) {
+        v.x = reinterpret_cast<const double*>(col)[k];
       }
+      const bool good = (v.x == rint(v.x)) & (fabs(v.x) <= 127.0) & (v.y == rint(v.y)) &
+                        (fabs(v.y) <= 127.0);
+      ok &= good;
+      dst[k2] = good ? uint16_t((uint32_t(int(v.x)) & 0xffu) | ((uint32_t(int(v.y)) & 0xffu) << 8))
+                     : uint16_t(0);
     }
-    out[idx] = q;
   }
+  if (!ok) *bad = 0;  // error words are reset to all ones
 }
 
 // Z (n x ncols, ld ldz) -> slices [s][r][kp] int8 and scale[r] = sigma_r: one
