@@ -13,7 +13,7 @@ namespace gwg {
 // Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 8 slices x RB
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
-template <int RB_>
+template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1>
 struct I8Tile {
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
@@ -21,7 +21,8 @@ struct I8Tile {
   static constexpr int BN = SLICES * RB;  // UMMA N (<= 256, multiple of 16)
   static constexpr int BK = 128;          // int8 K per stage = one 128B swizzle row
   static constexpr int UK = 32;           // K per tcgen05.mma (int8)
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int OUT_BUFS = OUT_BUFS_;     // staging tiles per epilogue warp
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
   static constexpr uint32_t B_BYTES = BN * BK;  // <= 32 KB
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -29,9 +30,11 @@ struct I8Tile {
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
   static constexpr int TMEM_COLS = 512;   // 2 accumulator buffers x BN (<= 256)
   static constexpr int OUT_Q = 16;        // output box: 16 doubles (128 B) x 32 SNPs
-  static constexpr uint32_t OUT_BYTES = OUT_Q * 32 * 8;  // 4 KB staging per epilogue warp
+  static constexpr uint32_t OUT_TILE = OUT_Q * 32 * 8;     // one 4 KB staging tile
+  static constexpr uint32_t OUT_BYTES = OUT_BUFS * OUT_TILE;  // staging per epilogue warp
   static constexpr size_t SMEM_BYTES =
       size_t(STAGES) * STAGE_BYTES + size_t(EPI_WARPS) * OUT_BYTES + 1024 + 256;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(BN % 16 == 0 && BN <= 256 && RB % 8 == 0, "UMMA N / swizzle atoms");
 };
 using I8Cfg = I8Tile<32>;
@@ -168,6 +171,10 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// at most one bulk store group of this thread still reading shared memory
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

@@ -23,6 +23,8 @@
 #include "grid_kernel.cuh"
 #include "i8_core.cuh"
 
+#include <cstdlib>
+
 namespace gwg {
 
 template <int P>
@@ -30,7 +32,9 @@ struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
   static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
   static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
-  using Tile = I8Tile<RB>;
+  // 4 operand stages + one 4 KB staging tile per epilogue warp (3 stages +
+  // double-buffered staging measured slower on the B200: 3.21 vs 3.05 ms)
+  using Tile = I8Tile<RB, 4, 1>;
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
   static constexpr int ROW = KT * P;                      // results per SNP row per tile
   static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
@@ -60,7 +64,7 @@ struct LinArgs {
   unsigned long long* err_key;
 };
 
-template <int P>
+template <int P, int EXP>
 __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const __grid_constant__ CUtensorMap tmap_w,
@@ -87,6 +91,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     const int qd = warp & 3;
     const int h = ew >> 2;
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
+    int nchunk = 0;  // result chunks this warp has stored (staging tile = nchunk & 1)
     for (int lt = h; lt < my_tiles; lt += 2) {
       const int buf = lt & 1;
       const int tile = blockIdx.x + lt * gridDim.x;
@@ -107,15 +112,15 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
       mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
-      const bool tma = L::TMA_OUT && a.use_tma;
+      const bool tma = L::TMA_OUT && a.use_tma && !(EXP & 2);
       // GROUP cells at a time: recombine their linear terms from TMEM (PAIR
       // cells per TMEM round trip), release TMEM after the last group, then
-      // solve the group's independent cells together and store them
+      // solve the group's independent cells together and store them.
+      // EXP (timing experiments only): bit 1 = no solve, bit 2 = no stores,
+      // 4 = release TMEM right after acc_full (no recombination)
+      auto recombine = [&](int cell0, int count, double(*dst)[P]) {
 #pragma unroll
-      for (int g0 = 0; g0 < L::KT; g0 += L::GROUP) {
-        double lin[L::GROUP][P];
-#pragma unroll
-        for (int u0 = 0; u0 < L::GROUP; u0 += L::PAIR) {
+        for (int u0 = 0; u0 < count; u0 += L::PAIR) {
 #pragma unroll
           for (int c0 = 0; c0 < P; c0 += L::CW) {
             int32_t v[L::PAIR][C::SLICES][L::CW];
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
             for (int u = 0; u < L::PAIR; ++u)
 #pragma unroll
               for (int sl = 0; sl < C::SLICES; ++sl)
-                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (g0 + u0 + u) * L::P8 + c0),
+                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (cell0 + u0 + u) * L::P8 + c0),
                                 v[u][sl]);
             tmem_ld_wait();
 #pragma unroll
@@ -132,19 +137,29 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
               for (int r = 0; r < L::CW; ++r) {
                 if (c0 + r < P) {
                   const double sc =
-                      __shfl_sync(0xffffffffu, sc_lane, (g0 + u0 + u) * L::P8 + c0 + r);
-                  lin[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
+                      __shfl_sync(0xffffffffu, sc_lane, (cell0 + u0 + u) * L::P8 + c0 + r);
+                  dst[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
                                                      v[u][3][r], v[u][4][r], v[u][5][r],
                                                      v[u][6][r], v[u][7][r], sc);
                 }
               }
           }
         }
-        if (g0 + L::GROUP >= L::KT) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for tile lt + 2
-        }
+      };
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for tile lt + 2
+      };
+      if (EXP & 4) {
+        release();
+        continue;
+      }
+#pragma unroll
+      for (int g0 = 0; g0 < L::KT; g0 += L::GROUP) {
+        double lin[L::GROUP][P];
+        recombine(g0, L::GROUP, lin);
+        if (g0 + L::GROUP >= L::KT) release();
         double beta[L::GROUP][P];
         bool ok[L::GROUP];
 #pragma unroll
@@ -155,7 +170,13 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
           cell[P] = sbr[g0 + u];
-          ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
+          if (EXP & 1) {
+            ok[u] = true;
+#pragma unroll
+            for (int c = 0; c < P; ++c) beta[u][c] = cell[c] + cell[P];
+          } else {
+            ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
+          }
         }
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {
@@ -175,22 +196,29 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < P; ++c) {
               const int f = (g0 + u) * P + c;
-              if (f % L::CHUNK == 0) {  // starting a chunk: the staging tile must be free
-                if (lane == 0) bulk_wait_read0();
+              unsigned char* tile_buf =
+                  stg + (C::OUT_BUFS == 2 ? ((nchunk + f / L::CHUNK) & 1) * C::OUT_TILE : 0);
+              if (f % L::CHUNK == 0) {  // starting a chunk: its staging tile must be free
+                if (lane == 0) {
+                  if (C::OUT_BUFS == 2)
+                    bulk_wait_read1();
+                  else
+                    bulk_wait_read0();
+                }
                 __syncwarp();
               }
               const int q = (f % L::CHUNK) >> 1;
-              *reinterpret_cast<double*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4) +
+              *reinterpret_cast<double*>(tile_buf + lane * 128 + ((q ^ (lane & 7)) << 4) +
                                          (f & 1) * 8) = beta[u][c];
               if (f % L::CHUNK == L::CHUNK - 1) {
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0)
-                  tma_store_2d(&tmap_out, stg, j0 * P + (f / L::CHUNK) * L::CHUNK,
+                  tma_store_2d(&tmap_out, tile_buf, j0 * P + (f / L::CHUNK) * L::CHUNK,
                                tm * C::BM + qd * 32);
               }
             }
-        } else if (iv) {
+        } else if (iv && !(EXP & 2)) {
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u) {
             const int j = j0 + g0 + u;
@@ -201,22 +229,23 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
           }
         }
       }
+      if (tma) nchunk += L::ROW / L::CHUNK;
     }
     if (lane == 0) bulk_wait0();
   }
   i8_teardown<C>(tmem_base, warp);
 }
 
-template <int P>
+template <int P, int EXP>
 cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int ctas,
                                 cudaStream_t s) {
   using C = typename LinCfg<P>::Tile;
-  cudaError_t e = cudaFuncSetAttribute(linear_solve_kernel<P>,
+  cudaError_t e = cudaFuncSetAttribute(linear_solve_kernel<P, EXP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(C::SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  linear_solve_kernel<P><<<ctas, C::THREADS, C::SMEM_BYTES, s>>>(tx, tw, tout, a);
+  linear_solve_kernel<P, EXP><<<ctas, C::THREADS, C::SMEM_BYTES, s>>>(tx, tw, tout, a);
   return cudaGetLastError();
 }
 
@@ -233,7 +262,18 @@ LinOps make_lin_ops() {
   o.kt = LinCfg<P>::KT;
   o.p8 = LinCfg<P>::P8;
   o.rb = LinCfg<P>::RB;
-  o.launch = &launch_linear_solve<P>;
+  o.launch = &launch_linear_solve<P, 0>;
+  if (P == 4) {  // timing experiments (GWG_LIN_EXP=bits), never in a shipped run
+    if (const char* v = std::getenv("GWG_LIN_EXP")) {
+      switch (std::atoi(v)) {
+        case 1: o.launch = &launch_linear_solve<P, 1>; break;
+        case 2: o.launch = &launch_linear_solve<P, 2>; break;
+        case 3: o.launch = &launch_linear_solve<P, 3>; break;
+        case 4: o.launch = &launch_linear_solve<P, 4>; break;
+        default: break;
+      }
+    }
+  }
   return o;
 }
 
