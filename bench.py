@@ -36,10 +36,12 @@ sys.path.insert(0, ROOT)
 METRIC = "GLS problems solved/sec (m·t/s) at n=1000,p=4; FP64 TFLOP/s vs B200 peak"
 PEAK_FP64_TFLOPS = 37.15  # measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.txt
 I8_SLICES = 8  # int8 slices of W per linear term (rotate_i8.cuh)
-# int8 dense tensor peak: 2 x the measured bf16 dense figure (NVIDIA's int8:bf16
-# dense ratio on B200); MEASURED_PEAKS.json has no int8 entry
-PEAK_INT8_TOPS = 2 * 1616.9
-PEAK_INT8_SOURCE = "derived: 2 x MEASURED_PEAKS.json bf16_tflops (1616.9, burst)"
+# int8 dense tensor peak measured on this pool's B200 (tools/i8_peak.cu:
+# tcgen05.mma kind::i8 M128 N256 K32 from resident smem, 148 CTAs, 1965 MHz);
+# MEASURED_PEAKS.json has no int8 entry
+PEAK_INT8_TOPS = 4346.0
+PEAK_INT8_SOURCE = ("measured: tcgen05.mma.kind::i8 issue loop on this pool's B200 "
+                    "(profiles/r01_i8_peak.txt)")
 PEAK_SOURCE = ("measured: DMMA.8x8x4 issue loop on this pool's B200 at 1965 MHz "
                "(profiles/r01_fp64_peak.txt; = 148 SM x 128 flop/clk x 1.965 GHz; "
                "MEASURED_PEAKS.json holds no FP64 figure)")

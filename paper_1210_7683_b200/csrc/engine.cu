@@ -253,6 +253,7 @@ int launch_i8(gwg_engine* e, const CUtensorMap& tx, const CUtensorMap& tb, int64
   a.tiles_m = int32_t(ceil_div(cols, I8Cfg::BM));
   a.tiles_r = int32_t(ceil_div(ncols, I8Cfg::RB));
   a.kstages = int32_t(kp / I8Cfg::BK);
+  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   GWG_CUDA_TRY(cudaFuncSetAttribute(gwg::rotate_i8_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,6 +442,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.tiles_m = int32_t(ceil_div(rows, I8Cfg::BM));
   a.tiles_r = int32_t(tiles_r);
   a.kstages = int32_t(kp / I8Cfg::BK);
+  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   GWG_CUDA_TRY(e->lops.launch(tx, tw, tout, a, int(std::min<int64_t>(tiles, e->sms)), e->comp));

@@ -250,20 +250,39 @@ __device__ __forceinline__ void i8_teardown(uint32_t tmem_base, int warp) {
                  : "memory");
 }
 
+// Tile rasterisation shared by producer and epilogues: groups of I8_GROUP_M
+// SNP tiles, and inside a group the SNP tile fastest, so the CTAs of one wave
+// cover ~148/16 slice-row tiles x 16 SNP tiles: both operands' working sets
+// stay in L2 even when they do not fit whole (n = 10,000: X int8 1 GB, Z
+// slices 0.8 GB, W slices 0.3 GB), and each B tile is fetched from HBM once
+// per group instead of once per SNP tile.
+constexpr int I8_GROUP_M = 16;
+__device__ __forceinline__ void i8_tile_coords(int tile, int tiles_m, int tiles_r, int& tm,
+                                               int& tr) {
+  const int per_group = I8_GROUP_M * tiles_r;
+  const int grp = tile / per_group;
+  const int rem = tile - grp * per_group;
+  const int rows = min(I8_GROUP_M, tiles_m - grp * I8_GROUP_M);
+  tr = rem / rows;
+  tm = grp * I8_GROUP_M + (rem - tr * rows);
+}
+
 // Warp 0, one thread: A = int8 SNP tile (box 128 k x 128 SNPs), B = RB rows
-// of all 8 slices (box 128 k x RB x 8).  Tiles: tm = tile / tiles_r (the rows
+// of all 8 slices (box 128 k x RB x 8).  Tiles: i8_tile_coords (the rows
 // of the sliced operand fastest, so the SNP tile is reused from L2).
 template <class C>
 __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMap* tmap_x,
-                                           const CUtensorMap* tmap_b, int my_tiles, int tiles_r,
-                                           int kstages) {
-  const uint64_t pol_x = policy_evict_first();
-  const uint64_t pol_b = policy_evict_last();
+                                           const CUtensorMap* tmap_b, int my_tiles, int tiles_m,
+                                           int tiles_r, int kstages, bool b_resident) {
+  // B small enough to stay in L2 for the whole launch: keep it (evict_last)
+  // and stream A; otherwise both ride the group rasterisation (evict_normal)
+  const uint64_t pol_x = b_resident ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_b = b_resident ? policy_evict_last() : policy_evict_normal();
   int g = 0;
   for (int lt = 0; lt < my_tiles; ++lt) {
     const int tile = blockIdx.x + lt * gridDim.x;
-    const int tm = tile / tiles_r;
-    const int tr = tile - tm * tiles_r;
+    int tm, tr;
+    i8_tile_coords(tile, tiles_m, tiles_r, tm, tr);
     for (int ks = 0; ks < kstages; ++ks, ++g) {
       const int s = g % C::STAGES;
       if (g >= C::STAGES) mbar_wait(&sm.empty[s], ((g / C::STAGES) - 1) & 1);

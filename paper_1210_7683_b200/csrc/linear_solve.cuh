@@ -61,6 +61,7 @@ struct LinArgs {
   int32_t tiles_m;
   int32_t tiles_r;      // ceil(t / KT)
   int32_t kstages;
+  int32_t b_resident;   // sliced operand fits L2: keep it resident
   unsigned long long* err_key;
 };
 
@@ -80,7 +81,8 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
   const uint32_t tmem_base = i8_setup<C>(sm, warp, 4);  // one warp per quarter per tile
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, my_tiles, a.tiles_r, a.kstages);
+    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, my_tiles, a.tiles_m, a.tiles_r, a.kstages,
+                                    a.b_resident != 0);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
   } else if (warp >= 4) {
@@ -95,8 +97,8 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     for (int lt = h; lt < my_tiles; lt += 2) {
       const int buf = lt & 1;
       const int tile = blockIdx.x + lt * gridDim.x;
-      const int tm = tile / a.tiles_r;
-      const int tr = tile - tm * a.tiles_r;
+      int tm, tr;
+      i8_tile_coords(tile, a.tiles_m, a.tiles_r, tm, tr);
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
       const bool iv = il < a.rows;
       const int j0 = tr * L::KT;  // first trait of the tile

@@ -36,6 +36,7 @@ struct I8Args {
   int32_t tiles_m;      // ceil(cols / 128)
   int32_t tiles_r;      // ceil(n / 32)
   int32_t kstages;      // kp / 128
+  int32_t b_resident;   // sliced operand fits L2: keep it resident
 };
 
 // ---- the rotation kernel -------------------------------------------------------
@@ -54,7 +55,8 @@ __global__ void __launch_bounds__(I8Cfg::THREADS, 1)
   const uint32_t tmem_base = i8_setup<C>(sm, warp);
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_z, my_tiles, a.tiles_r, a.kstages);
+    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_z, my_tiles, a.tiles_m, a.tiles_r, a.kstages,
+                                    a.b_resident != 0);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
   } else if (warp >= 4) {
@@ -69,8 +71,8 @@ __global__ void __launch_bounds__(I8Cfg::THREADS, 1)
     for (int lt = 0; lt < my_tiles; ++lt) {
       const int buf = lt & 1;
       const int tile = blockIdx.x + lt * gridDim.x;
-      const int tm = tile / a.tiles_r;
-      const int tr = tile - tm * a.tiles_r;
+      int tm, tr;
+      i8_tile_coords(tile, a.tiles_m, a.tiles_r, tm, tr);
       const int r0 = tr * C::RB + h * C::OUT_Q;
       double x[C::OUT_Q];
       mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);

@@ -71,7 +71,8 @@ def run(name, steps):
             "gls_per_s": m * t / (ms * 1e-3), "step_tflops_grid_convention": grid_flops / ms / 1e9,
             "grid_kernel_ms": kern, "grid_kernel_tflops": grid_flops / kern / 1e9,
             "grid_kernel_frac_of_peak": grid_flops / kern / 1e9 / PEAK,
-            "rotate_ms": c["rotate_ms"] / steps, "kinship_build_s": t1 - t0,
+            "rotate_ms": c["rotate_ms"] / steps, "sbr_ms": c["quad_ms"] / steps,
+            "linear_solve_ms": c["linear_ms"] / steps, "kinship_build_s": t1 - t0,
             "device_eig_s": t2 - t1, "nan": int(torch.isnan(b).sum().item())}
 
 
