@@ -51,7 +51,7 @@ SEED = 20261019
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--m", type=int, default=100_000, help="SNPs per GPU")
@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--snp-coding", default="genotypes", choices=["genotypes", "real"],
                     help="BASELINE X_R are genotype codes {0,1,2}: exact int8 tcgen05 rotation")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt-coding", dest="alt_coding", action="store_false",
+                    help="skip timing the other SNP coding on the same data")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -72,7 +74,7 @@ class Clocks:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int, period_s: float = 0.01):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
         self.samples, self.reasons, self.max_mhz = [], set(), None
 
@@ -257,6 +259,7 @@ def run_ours(args):
                               "traffic": load_traffic("linear_solve_kernel"),
                               "algorithmic_ops_per_launch": lin_ops,
                               "peak_source": PEAK_INT8_SOURCE},
+                "grid_fp64_equivalent_tflops": grid_flops_step / ((quad_ms + lin_ms) * 1e-3) / 1e12,
                 "step_breakdown_ms": {"rotate_snps": rotate_ms, "sbr": quad_ms,
                                       "linear_solve": lin_ms,
                                       "other (Y rotation, contexts, W)": ms_step - rotate_ms
@@ -271,6 +274,36 @@ def run_ours(args):
 
     # sanity: no NaN, finite results
     bad = int(torch.isnan(b_dev).sum().item())
+
+    # ---- the other SNP coding on the same data, for transparency: the all-FP64
+    # path (real coding) when the headline runs the genotype path -------------
+    alt = None
+    if args.alt_coding:
+        other = "real" if args.snp_coding == "genotypes" else "genotypes"
+        eng.set_snp_coding(other)
+        b_alt = torch.empty_like(b_dev)
+
+        def alt_step():
+            eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
+            eng.solve_snp_slab(x_dev, out=b_alt)
+
+        alt_step()
+        barrier()
+        eng.reset_counters()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            alt_step()
+        a1.record(stream)
+        barrier()
+        alt_ms = a0.elapsed_time(a1) / args.steps
+        acnt = eng.counters()
+        rel = ((b_alt - b_dev).norm(dim=2) / b_dev.norm(dim=2)).max().item()
+        alt = {"snp_coding": other, "value": cells / (alt_ms * 1e-3), "ms_per_step": alt_ms,
+               "grid_kernel_ms": acnt["grid_kernel_ms"] / args.steps,
+               "max_normwise_rel_diff_vs_headline": rel}
+        eng.set_snp_coding(args.snp_coding)
+        del b_alt
 
     # ---- e2e through gwg_run_grid with pinned host buffers ------------------
     e2e = None
@@ -324,8 +357,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (X_R %.1f GB per GPU per step)" % (n * m * 8 / 1e9),
                        "snp_coding": args.snp_coding,
                        "step": ("rotate Y (DMMA) and X_R (exact int8 tcgen05) + trait contexts "
-                                "+ split grid: linear terms x^T W exact on int8 tcgen05, quadratic "
-                                "term on DMMA fused with the bordered Cholesky"
+                                "+ split grid: S_BR = (X'.X')^T D on DMMA, linear terms x^T W exact "
+                                "on int8 tcgen05 fused with the bordered Cholesky"
                                 if split else
                                 "rotate Y and X_R (DMMA) + trait contexts + fused DMMA grid kernel")},
             "tflops": grid_flops_step * world / (ms_step * 1e-3) / 1e12,
@@ -337,6 +370,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "nan_cells": bad,
+            "other_coding": alt,
             "preloop_eig_s": shared.get("eig_s"),
         }
         print(json.dumps(line), flush=True)
