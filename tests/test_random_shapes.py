@@ -28,7 +28,7 @@ def exact_cells(lam, xl, xr, y, h2, s2):
     return out
 
 
-@settings(max_examples=40, deadline=None)
+@settings(max_examples=40, deadline=None, derandomize=True)
 @given(n=st.integers(2, 9), pm1=st.integers(0, 3), m=st.integers(1, 3),
        seed=st.integers(0, 2**32 - 1), h2=st.floats(0.0, 0.95), s2=st.floats(0.25, 4.0))
 def test_oracle_cells_match_exact_arithmetic(n, pm1, m, seed, h2, s2):
@@ -44,10 +44,13 @@ def test_oracle_cells_match_exact_arithmetic(n, pm1, m, seed, h2, s2):
         return
     got = orc.compute_grid(lam, xl, xr, y, [h2], [s2])[:, 0, :]
     ref = np.array(exact)
-    # relative to the cell norm, scaled by the conditioning of the tiny system
+    # relative to the cell norm, scaled by the conditioning of the weighted
+    # tiny system (the normal equations square it); small constant for the
+    # O(n p) rounding steps of the context + cell
     rel = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
-    cond = max(np.linalg.cond(np.column_stack([xl, xr[:, i]])) for i in range(m))
-    assert rel.max() <= 1e-14 * max(1.0, cond) ** 2
+    w = 1.0 / np.sqrt(s2 * (h2 * lam + (1.0 - h2)))
+    cond = max(np.linalg.cond(w[:, None] * np.column_stack([xl, xr[:, i]])) for i in range(m))
+    assert rel.max() <= 8e-14 * max(1.0, cond) ** 2
 
 
 def _shapes():
