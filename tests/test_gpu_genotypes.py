@@ -96,3 +96,37 @@ def test_genotype_check_rejects_non_integer_codes():
         run(dict(ds, snps=snps), basis, values, "genotypes")
     # the real-valued path accepts them
     assert np.isfinite(run(ds2, basis, values, "real")).all()
+
+
+@pytest.mark.parametrize("coding", ["genotypes", "real"])
+@pytest.mark.parametrize("layout", ["numpy", "stream"])
+@pytest.mark.parametrize("offset", [0, 1, 2])  # doubles: 1 = 8-byte aligned only (no TMA stores)
+def test_device_output_stays_inside_its_buffer(coding, layout, offset):
+    """Results written straight into a device tensor that is a window of a larger
+    sentinel-filled buffer: every cell written, nothing outside the window
+    touched (TMA stores clip at the tensor edges; misaligned windows take the
+    direct-store path)."""
+    n, p, m, t = 150, 4, 203, 27
+    ds = datagen.generate(n, p, m, t, seed=77)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    ref = run(ds, basis, values, coding)
+    size = m * t * p
+    guard = 4096
+    buf = torch.full((size + 2 * guard,), -7.25, dtype=torch.float64, device="cuda")
+    shape = (m, t, p) if layout == "numpy" else (t, m, p)
+    out = buf[guard + offset: guard + offset + size].view(shape)
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        x = torch.from_numpy(np.ascontiguousarray(ds["snps"].T)).cuda().t()
+        eng.solve_snp_slab(x, out=out, layout=layout)
+        torch.cuda.synchronize()
+    host = buf.cpu().numpy()
+    assert np.all(host[:guard + offset] == -7.25)
+    assert np.all(host[guard + offset + size:] == -7.25)
+    got = out.cpu().numpy()
+    if layout == "stream":
+        got = got.transpose(1, 0, 2)
+    assert np.array_equal(got, ref)

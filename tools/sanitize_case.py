@@ -1,4 +1,7 @@
-"""Small end-to-end case for compute-sanitizer runs (one tool per gpurun call)."""
+"""Small end-to-end case for compute-sanitizer runs (one tool per gpurun call).
+
+  python tools/sanitize_case.py [real|genotypes]
+"""
 import sys
 
 sys.path.insert(0, ".")
@@ -7,16 +10,21 @@ import numpy as np  # noqa: E402
 import paper_1210_7683_b200 as gw  # noqa: E402
 from paper_1210_7683_b200 import datagen  # noqa: E402
 
-for (n, p, m, t) in ((130, 4, 150, 37), (96, 1, 40, 9), (200, 8, 70, 20), (64, 20, 30, 9)):
+coding = sys.argv[1] if len(sys.argv) > 1 else "real"
+for (n, p, m, t) in ((130, 4, 150, 37), (96, 1, 40, 9), (200, 8, 70, 20), (64, 20, 30, 9),
+                     (300, 3, 260, 70)):
     ds = datagen.generate(n, p, m, t, seed=3)
     z, lam = gw.eigendecompose(ds["kinship"])
     with gw.Engine(n, p) as eng:
         eng.set_spectrum(z, lam)
         eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
         eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
         b = eng.run_grid(ds["snps"], mb=64)
         b2 = eng.solve_snp_slab(ds["snps"])
+        bs = eng.run_grid(ds["snps"], layout="stream", mb=100)
         assert np.array_equal(b, b2) and not np.isnan(b).any()
+        assert np.array_equal(bs.transpose(1, 0, 2), b)
     err = gw.verify_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
                          ds["sigma2"], b)
     print(n, p, m, t, "verify", err)
