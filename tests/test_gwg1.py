@@ -57,7 +57,8 @@ def test_native_stream_info_reads_headers_without_gpu(tmp_path):
 
 
 @pytest.mark.gpu
-def test_file_legs_match_in_memory_engine(tmp_path):
+@pytest.mark.parametrize("coding", ["real", "genotypes"])
+def test_file_legs_match_in_memory_engine(tmp_path, coding):
     ds = datagen.generate(300, 4, 1111, 45, seed=5)
     basis, values = gw.eigendecompose(ds["kinship"])
     snp_path, trait_path = str(tmp_path / "snps.gwg"), str(tmp_path / "traits.gwg")
@@ -67,6 +68,7 @@ def test_file_legs_match_in_memory_engine(tmp_path):
     with gw.Engine(300, 4) as eng:
         eng.set_spectrum(basis, values)
         eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
         eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
         mem = eng.run_grid(ds["snps"])
         eng.set_traits_file(trait_path)
@@ -84,7 +86,8 @@ def test_file_legs_match_in_memory_engine(tmp_path):
 
 
 @pytest.mark.gpu
-def test_failed_run_leaves_unreadable_output(tmp_path):
+@pytest.mark.parametrize("coding", ["real", "genotypes"])
+def test_failed_run_leaves_unreadable_output(tmp_path, coding):
     """test_grid.cpp:766-771: no output survives as a readable stream."""
     ds = datagen.generate(40, 3, 10, 4, seed=6)
     snps = ds["snps"].copy()
@@ -94,6 +97,7 @@ def test_failed_run_leaves_unreadable_output(tmp_path):
     with gw.Engine(40, 3) as eng:
         eng.set_spectrum(*gw.eigendecompose(ds["kinship"]))
         eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
         eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
         with pytest.raises(gw.NotPositiveDefiniteError) as e:
             eng.run_grid_files(snp_path, out_path)
