@@ -92,7 +92,7 @@ def load_manifest(data_dir: str) -> dict:
     return out
 
 
-def _engine_for(man: dict, device_eig: bool) -> Engine:
+def _engine_for(man: dict, device_eig: bool, snp_coding: str = "real") -> Engine:
     kin = gwg1.read_columns(man["kinship"], gwg1.KIND_OPERAND)
     xl = gwg1.read_columns(man["xl"], gwg1.KIND_OPERAND)
     eng = Engine(man["n"], man["p"])
@@ -101,6 +101,7 @@ def _engine_for(man: dict, device_eig: bool) -> Engine:
     else:
         eng.set_spectrum(*eigendecompose(kin))
     eng.set_covariates(xl)
+    eng.set_snp_coding(snp_coding)
     eng.set_traits_file(man["traits"])
     return eng
 
@@ -121,14 +122,14 @@ def cmd_solve(a) -> int:
     man = load_manifest(a.data)
     out = a.out or os.path.join(a.data, "b.gwg")
     t0 = time.perf_counter()
-    eng = _engine_for(man, a.device_eig)
+    eng = _engine_for(man, a.device_eig, a.snp_coding)
     t1 = time.perf_counter()
     try:
         c = eng.run_grid_files(man["snps"], out, mb=a.mb)
     finally:
         eng.close()
     t2 = time.perf_counter()
-    print(f"scheduler=gpu\nn={man['n']}\np={man['p']}\nm={man['m']}\nt={man['t']}")
+    print(f"scheduler=gpu\nsnp_coding={a.snp_coding}\nn={man['n']}\np={man['p']}\nm={man['m']}\nt={man['t']}")
     for k in ("preloop_flops", "loop_flops", "grid_flops", "context_builds", "bytes_loaded",
               "bytes_stored", "kernel_launches"):
         print(f"{k}={c[k]}")
@@ -186,7 +187,7 @@ def cmd_verify(a) -> int:
 def cmd_bench(a) -> int:
     man = load_manifest(a.data)
     out = a.out or os.path.join(a.data, "bench_b.gwg")
-    eng = _engine_for(man, False)
+    eng = _engine_for(man, False, a.snp_coding)
     rows = ["workers,scheduler,wall_time_s,loop_flops,stall_fraction"]
     try:
         for mode in ("files", "memory"):
@@ -228,6 +229,8 @@ def main(argv=None) -> int:
     s.add_argument("--out", default="")
     s.add_argument("--mb", type=int, default=0)
     s.add_argument("--device-eig", action="store_true")
+    s.add_argument("--snp-coding", choices=("real", "genotypes"), default="real",
+                   help="genotypes: integer codes on the exact int8 tensor-core path")
     v = sub.add_parser("verify", help="recheck result cells against the Cholesky route")
     v.add_argument("--data", required=True)
     v.add_argument("--results", default="")
@@ -239,6 +242,7 @@ def main(argv=None) -> int:
     b.add_argument("--data", required=True)
     b.add_argument("--out", default="")
     b.add_argument("--csv", default="")
+    b.add_argument("--snp-coding", choices=("real", "genotypes"), default="real")
     sub.add_parser("tune", help="(out of scope: the reference's CPU/disk tuner)")
     a = ap.parse_args(argv)
     if a.cmd == "tune":

@@ -66,6 +66,12 @@ def test_solve_verify_round_trip_and_failures(tmp_path):
     assert np.array_equal(b, ref["b"])
     rc, kv, _ = run("verify", "--data", d, "--sample", "200")
     assert rc == 0 and kv["status"] == "ok" and float(kv["max_rel_err"]) < 1e-10
+    # the genotype-coded path on the same dataset agrees to rounding
+    rc, kv, _ = run("solve", "--data", d, "--snp-coding", "genotypes", "--out",
+                    os.path.join(d, "bg.gwg"))
+    assert rc == 0 and kv["snp_coding"] == "genotypes"
+    bg = gwg1.read_result(kv["out"])
+    assert np.max(np.linalg.norm(bg - b, axis=2) / np.linalg.norm(b, axis=2)) < 1e-10
     rc, kv, _ = run("verify", "--data", d, "--exhaustive")
     assert rc == 0 and kv["mode"] == "exhaustive" and int(kv["checked"]) == 300 * 12
     # corrupt one cell (test_cli.cpp:199-226): verification fails with exit 3
