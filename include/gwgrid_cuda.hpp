@@ -121,6 +121,14 @@ class DeviceGrid {
     throw_if(st);
   }
 
+  // Integer genotype codes in every SNP slab from now on (GWG_SNP_GENOTYPES:
+  // exact int8 tensor-core rotation + split grid) or real values (default).
+  void set_snp_coding(int coding) {
+    gwg_status st{};
+    gwg_set_snp_coding(e_, coding, &st);
+    throw_if(st);
+  }
+
   // transform_trait_slab + build_trait_contexts for a raw trait slab n x t
   // (trait0 only tags errors in the reference; traits are 0-based here).
   void build_trait_contexts(const double* traits, std::int64_t t, const double* h2,

@@ -107,6 +107,23 @@ static void test_compute_tile_matches_oracle() {
   CHECK(std::memcmp(b.data(), tile.data.data(), b.size() * sizeof(double)) == 0);
 }
 
+static void test_genotype_coding_matches_oracle() {
+  Data d(200, 4, 150, 37, 5);  // the generator's SNPs are genotype codes {0,1,2}
+  gwgrid_cuda::DeviceGrid grid(0, d.n, d.p);
+  grid.precompute(d.basis.data(), d.values.data(), d.xl.data());
+  grid.set_snp_coding(GWG_SNP_GENOTYPES);
+  grid.build_trait_contexts(d.traits.data(), d.t, d.h2.data(), d.sigma2.data());
+  gwgrid_cuda::ResultTile tile;
+  tile.reset(0, 0, d.m, d.t, d.p);
+  grid.compute_tile(d.snps.data(), tile);
+  const double err = max_normwise(tile.data, d.oracle(), d.p);
+  std::printf("  genotype compute_tile vs oracle: max norm-wise rel err %.3e\n", err);
+  CHECK(err < 1e-12);
+  std::vector<double> b(d.m * d.t * d.p);
+  grid.run_grid(d.snps.data(), d.m, b.data(), false, 64);
+  CHECK(std::memcmp(b.data(), tile.data.data(), b.size() * sizeof(double)) == 0);
+}
+
 static void test_zero_column_npd_coordinates() {
   Data d(48, 3, 12, 6, 4);
   for (int64_t k = 0; k < d.n; ++k) d.snps[5 * d.n + k] = 0.0;
@@ -161,6 +178,8 @@ static void test_dimension_errors() {
 int main() {
   const std::pair<const char*, std::function<void()>> cases[] = {
       {"compute_tile matches the oracle; run_grid bitwise equal", test_compute_tile_matches_oracle},
+      {"genotype coding (int8 tensor-core path) matches the oracle",
+       test_genotype_coding_matches_oracle},
       {"zero variant column fails with coordinates", test_zero_column_npd_coordinates},
       {"trait weight failure surfaces the trait index", test_trait_weight_failure},
       {"dimension errors", test_dimension_errors},
