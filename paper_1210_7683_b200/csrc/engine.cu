@@ -329,7 +329,7 @@ int build_split(gwg_engine* e, gwg_status* st) {
     e->counters.kernel_launches += 1;
     e->basis_t_valid = true;
   }
-  const int64_t bt = gwg::SbrDefault::BT;
+  const int64_t bt = e->sops.bt;
   const int64_t tiles_t = ceil_div(t, bt);
   GWG_CUDA_TRY(e->dpanel.ensure(size_t(tiles_t) * np * bt * sizeof(double)));
   if (t % bt)  // padded traits of the last tile contribute zeros
@@ -380,7 +380,6 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
                  double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
   if (int rc = build_split(e, st)) return rc;
   using gwg::I8Cfg;
-  using S = gwg::SbrDefault;
   const int64_t t = e->t, p = e->p;
   const int64_t kp = round_up(e->n, I8Cfg::BK);
   const int64_t tiles_r = ceil_div(t, e->lops.kt);
@@ -390,20 +389,20 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
 
   // ---- S_BR = (X'.X')^T D ----
   CUtensorMap map_sq;
-  if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, S::BM, st)) return rc;
+  if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->sops.bm, st)) return rc;
   gwg::SbrArgs q;
   q.dpanel = e->dpanel.d();
   q.sbr = e->sbr.d();
   q.ld = ld_s;
   q.rows = rows;
   q.t = int32_t(t);
-  q.tiles_m = int32_t(ceil_div(rows, S::BM));
-  q.tiles_t = int32_t(ceil_div(t, S::BT));
-  q.kchunks = int32_t(e->np / S::BK);
+  q.tiles_m = int32_t(ceil_div(rows, e->sops.bm));
+  q.tiles_t = int32_t(ceil_div(t, e->sops.bt));
+  q.kchunks = int32_t(e->np / e->sops.bk);
   q.np = e->np;
   const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
-  GWG_CUDA_TRY(gwg::launch_sbr_default(map_sq, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
+  GWG_CUDA_TRY(e->sops.launch(map_sq, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[1], e->comp));
   e->counters.kernel_launches += 1;
 
@@ -574,6 +573,10 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   e->np = round_up(n, kBK);
   e->ops = ops;
   e->lops = lops;
+  {
+    const char* v = std::getenv("GWG_SBR_CFG");
+    e->sops = gwg::sbr_ops(v ? std::atoi(v) : 0);
+  }
   if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));

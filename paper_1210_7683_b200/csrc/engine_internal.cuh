@@ -70,6 +70,7 @@ struct gwg_engine {
   int64_t n = 0, p = 0, np = 0;
   gwg::KernelOps ops;
   gwg::LinOps lops;  // genotype split grid: per-p linear-solve kernel
+  gwg::SbrOps sops;  // genotype split grid: S_BR kernel configuration
   cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
 
   gwg_host::DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np

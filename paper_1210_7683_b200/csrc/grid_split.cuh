@@ -216,8 +216,21 @@ cudaError_t launch_sbr(const CUtensorMap& map_sq, const SbrArgs& a, int ctas, cu
   return cudaGetLastError();
 }
 
-// SbrDefault instantiation (kernels_lin_a.cu).
-cudaError_t launch_sbr_default(const CUtensorMap& map_sq, const SbrArgs& a, int ctas,
-                               cudaStream_t s);
+// Instantiated S_BR configurations (kernels_lin_a.cu): tile shape + launcher.
+struct SbrOps {
+  int bm = 0, bt = 0, bk = 0;
+  cudaError_t (*launch)(const CUtensorMap&, const SbrArgs&, int, cudaStream_t) = nullptr;
+};
+template <class Cfg>
+SbrOps make_sbr_ops() {
+  SbrOps o;
+  o.bm = Cfg::BM;
+  o.bt = Cfg::BT;
+  o.bk = Cfg::BK;
+  o.launch = &launch_sbr<Cfg>;
+  return o;
+}
+// variant 0 = SbrDefault (64 SNPs x 64 traits); 1 = 128 x 40; 2 = 64 x 40
+SbrOps sbr_ops(int variant);
 
 }  // namespace gwg

@@ -3,10 +3,13 @@
 #include "grid_split.cuh"
 namespace gwg {
 
-// The S_BR launch of the split grid is p-independent: one instantiation.
-cudaError_t launch_sbr_default(const CUtensorMap& map_sq, const SbrArgs& a, int ctas,
-                               cudaStream_t s) {
-  return launch_sbr<SbrDefault>(map_sq, a, ctas, s);
+// The S_BR launch of the split grid is p-independent.
+SbrOps sbr_ops(int variant) {
+  switch (variant) {
+    case 1: return make_sbr_ops<SbrCfg<4, 5, 4, 1, 16, 5>>();
+    case 2: return make_sbr_ops<SbrCfg<2, 5, 4, 1, 32, 4>>();
+    default: return make_sbr_ops<SbrDefault>();
+  }
 }
 
 bool lin_ops_for_a(int64_t p, LinOps* out) {
