@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     // warp w owns TMEM lane quarter w % 4; the two warps of a quarter take
     // alternate tiles (= alternate accumulator buffers), each doing all KT
     // cells of its tile, so two tiles' epilogues are in flight per quarter.
+    // (Warps per quarter must equal the number of accumulator buffers: each
+    // warp then waits on one buffer's acc_full phases strictly in order — a
+    // third warp per quarter could run two phases ahead and alias the parity.)
     const int ew = warp - 4;
     const int qd = warp & 3;
     const int h = ew >> 2;
