@@ -309,16 +309,27 @@ def _dims_of(kinship, xl, snps, traits, h2, sigma2):
     return kinship, xl, snps, traits, h2, sigma2, (n, p, m, t)
 
 
-def device_working_set_bytes(n: int, p: int, t: int, mb: int) -> int:
+def device_working_set_bytes(n: int, p: int, t: int, mb: int, snp_coding: str = "real") -> int:
     """Resident HBM bytes of a run_grid with mb-column slabs (the device
     analogue of working_set_bytes, grid.cpp:279-297): spectrum, covariates,
-    trait operands + contexts, two raw slabs, one rotated slab, two result
-    slabs."""
+    trait operands + contexts, two raw slabs, rotated slab(s), two result
+    slabs; for genotype coding also Z^T, the W build (V, W, 8 int8 slices),
+    the D panels, Z slices, the int8 slab and S_BR."""
     np_ = -(-n // 32) * 32
+    kp = -(-n // 128) * 128
     fixed = (n * n + n) * 8 + 2 * n * max(p - 1, 1) * 8
     traits = (2 * n * t + 2 * t) * 8 + (-(-t // 8) * 8) * np_ * (p + 1) * 8 + t * (2 * p + p * p // 2) * 8
-    per_snp = (2 * n + np_) * 8 + 2 * t * p * 8
-    return fixed + traits + mb * per_snp
+    per_snp = (2 * n + 2 * np_) * 8 + 2 * t * p * 8
+    total = fixed + traits + mb * per_snp
+    if snp_coding == "genotypes":
+        p8 = 1 << max(0, (p - 1).bit_length()) if p <= 8 else -(-p // 8) * 8
+        kt = max(1, 32 // p8)
+        wrows = -(-t // kt) * kt * p8
+        total += np_ * n * 8 + 8 * n * kp + n * 8             # Z^T, Z slices + scales
+        total += 2 * np_ * wrows * 8 + 8 * wrows * kp + wrows * 8  # V, W, W slices + scales
+        total += -(-t // 64) * 64 * np_ * 8                   # D panels
+        total += mb * (kp + t * 8)                            # int8 slab, S_BR
+    return total
 
 
 def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,
@@ -349,18 +360,18 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     if tbb and not 1 <= tbb <= (tb or t):
         raise DimensionError(f"tile parameter tbb (must be in [1, tb]) out of range (got {tbb})")
     if memory_budget is not None:
-        need1 = device_working_set_bytes(n, p, t, 1)
+        need1 = device_working_set_bytes(n, p, t, 1, snp_coding)
         if need1 > memory_budget:
             raise InfeasibleBudgetError(
                 f"memory budget of {memory_budget} bytes cannot hold even a 1-column slab "
                 f"(working set {need1} bytes)")
         if not mb:
-            per = device_working_set_bytes(n, p, t, 2) - device_working_set_bytes(n, p, t, 1)
-            mb = max(1, min(m, (memory_budget - device_working_set_bytes(n, p, t, 0)) // per))
-        elif device_working_set_bytes(n, p, t, mb) > memory_budget:
+            ws = [device_working_set_bytes(n, p, t, k, snp_coding) for k in (0, 1)]
+            mb = max(1, min(m, (memory_budget - ws[0]) // (ws[1] - ws[0])))
+        elif device_working_set_bytes(n, p, t, mb, snp_coding) > memory_budget:
+            need = device_working_set_bytes(n, p, t, mb, snp_coding)
             raise InfeasibleBudgetError(
-                f"working set of {device_working_set_bytes(n, p, t, mb)} bytes exceeds the "
-                f"memory budget of {memory_budget} bytes")
+                f"working set of {need} bytes exceeds the memory budget of {memory_budget} bytes")
     with Engine(n, p, device) as eng:
         if device_eig:
             eng.set_kinship(kinship)

@@ -93,6 +93,8 @@ def test_device_working_set_is_monotone():
     b = gw.device_working_set_bytes(1000, 4, 1000, 100)
     assert 0 < a < b
     assert gw.device_working_set_bytes(1000, 4, 1000, 0) < a
+    # the genotype path keeps W slices, S_BR and the int8 slab on top
+    assert gw.device_working_set_bytes(1000, 4, 1000, 100, "genotypes") > b
 
 
 def test_generator_is_deterministic_and_shaped():
