@@ -448,7 +448,10 @@ def run_reference(args):
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json generators, seed %d)" % SEED,
-        "config": {"workload": "c1", "n": n, "p": p, "m_sample": ms, "t": t},
+        "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": args.m, "t": t,
+                   "cells_per_step": ms * t, "m_sample_per_step": ms,
+                   "parallelism": "host threads x%d (rank 0)" % (os.cpu_count() or 1),
+                   "snp_coding": "real (the reference's double-precision CPU path)"},
         "cpu_baseline": {"value": value, "unit": "GLS/s", "cores": workers, "kind": "port",
                          "sample": f"{ms} SNPs x {t} traits of c1 per step (oracle/ restatement "
                                    "of gwgrid compute_tile CT + OpenBLAS rotation)"},
