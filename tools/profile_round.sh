@@ -6,7 +6,7 @@
 set -u
 R=${1:-r01}
 mkdir -p gpurun_out
-python bench.py --steps 5 --warmup 3 > gpurun_out/${R}_bench.log 2>&1
+python bench.py --steps 20 --warmup 3 > gpurun_out/${R}_bench.log 2>&1
 echo "bench rc=$?"
 python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/${R}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
