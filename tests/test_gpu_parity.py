@@ -170,19 +170,26 @@ def test_bitwise_invariance_across_slabs_layouts_and_entry_points():
         assert np.array_equal(np.concatenate(parts, axis=0), base)
 
 
-def test_zero_snp_column_fails_with_coordinates():
+CODINGS = pytest.mark.parametrize("coding", ["real", "genotypes"])
+
+
+@CODINGS
+def test_zero_snp_column_fails_with_coordinates(coding):
     """test_gls.cpp:274-292 / test_grid.cpp:689-730 on the device."""
     ds = datagen.generate(48, 3, 12, 6, seed=4)
     snps = ds["snps"].copy()
     snps[:, 5] = 0.0
     with pytest.raises(gw.NotPositiveDefiniteError, match="positive definite") as e:
-        gw.solve_grid(ds["kinship"], ds["xl"], snps, ds["traits"], ds["h2"], ds["sigma2"])
+        gw.solve_grid(ds["kinship"], ds["xl"], snps, ds["traits"], ds["h2"], ds["sigma2"],
+                      snp_coding=coding)
     assert (e.value.snp_index, e.value.trait_index) == (5, 0)
     with pytest.raises(ValueError):  # reference's Python mapping
-        gw.solve_grid(ds["kinship"], ds["xl"], snps, ds["traits"], ds["h2"], ds["sigma2"], mb=5)
+        gw.solve_grid(ds["kinship"], ds["xl"], snps, ds["traits"], ds["h2"], ds["sigma2"], mb=5,
+                      snp_coding=coding)
 
 
-def test_trait_weight_failure_reports_trait():
+@CODINGS
+def test_trait_weight_failure_reports_trait(coding):
     """test_grid.cpp:732-773: indefinite kinship + high h2 -> (-1, j)."""
     n = 8
     phi = np.diag(np.arange(n) - 0.5)
@@ -190,12 +197,13 @@ def test_trait_weight_failure_reports_trait():
     h2 = np.zeros(5)
     h2[3] = 0.9
     with pytest.raises(gw.NotPositiveDefiniteError) as e:
-        gw.solve_grid(phi, np.ones((n, 1)), rng.standard_normal((n, 4)),
-                      rng.standard_normal((n, 5)), h2, np.ones(5))
+        gw.solve_grid(phi, np.ones((n, 1)), rng.integers(0, 3, (n, 4)).astype(float),
+                      rng.standard_normal((n, 5)), h2, np.ones(5), snp_coding=coding)
     assert (e.value.snp_index, e.value.trait_index) == (-1, 3)
 
 
-def test_singular_covariates_fail_every_cell_of_the_trait():
+@CODINGS
+def test_singular_covariates_fail_every_cell_of_the_trait(coding):
     """S_TL singular (a zero covariate column): the reference's full LLT fails
     at the first cell of the trait; the device reports (first SNP, first
     trait)."""
@@ -203,24 +211,27 @@ def test_singular_covariates_fail_every_cell_of_the_trait():
     xl = ds["xl"].copy()
     xl[:, 2] = 0.0
     with pytest.raises(gw.NotPositiveDefiniteError) as e:
-        gw.solve_grid(ds["kinship"], xl, ds["snps"], ds["traits"], ds["h2"], ds["sigma2"])
+        gw.solve_grid(ds["kinship"], xl, ds["snps"], ds["traits"], ds["h2"], ds["sigma2"],
+                      snp_coding=coding)
     assert (e.value.snp_index, e.value.trait_index) == (0, 0)
 
 
-def test_h2_zero_is_ols_and_sigma2_invariance():
+@CODINGS
+def test_h2_zero_is_ols_and_sigma2_invariance(coding):
     ds = datagen.generate(60, 4, 20, 6, seed=12)
     x_all = ds["xl"]
     h2 = np.zeros(6)
-    b = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], h2, np.ones(6))["b"]
+    b = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], h2, np.ones(6),
+                      snp_coding=coding)["b"]
     for i in (0, 7, 19):
         x = np.column_stack([x_all, ds["snps"][:, i]])
         ols = np.linalg.lstsq(x, ds["traits"], rcond=None)[0].T
         rel = np.linalg.norm(b[i] - ols, axis=1) / np.linalg.norm(ols, axis=1)
         assert rel.max() < 1e-10
     b1 = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
-                       np.ones(6))["b"]
+                       np.ones(6), snp_coding=coding)["b"]
     b2 = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
-                       np.full(6, 64.0))["b"]
+                       np.full(6, 64.0), snp_coding=coding)["b"]
     assert (np.linalg.norm(b1 - b2, axis=2) / np.linalg.norm(b1, axis=2)).max() < 1e-12
 
 
@@ -234,17 +245,19 @@ def test_solve_cell_matches_partitioned_oracle():
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
 
 
-def test_config1_full_size_properties():
-    """BASELINE configs[1] at full size (n=1000, p=4, m=1e5, t=1e3):
-    size-independent properties — no NaN, bitwise-equal results for two slab
-    widths (checksum of checksums), and seeded random spot checks against the
-    oracle and the Cholesky route."""
+@CODINGS
+def test_config1_full_size_properties(coding):
+    """BASELINE configs[1] at full size (n=1000, p=4, m=1e5, t=1e3), both SNP
+    codings (genotypes = the bench path): size-independent properties — no
+    NaN, bitwise-equal results for two slab widths (checksum of checksums),
+    and seeded random spot checks against the oracle and the Cholesky route."""
     n, p, m, t = 1000, 4, 100_000, 1000
     ds = datagen.generate(n, p, m, t, seed=1)
     basis, values = gw.eigendecompose(ds["kinship"])
     with gw.Engine(n, p) as eng:
         eng.set_spectrum(basis, values)
         eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
         eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
         b = eng.run_grid(ds["snps"])
         b2 = eng.run_grid(ds["snps"], mb=4736)
