@@ -13,7 +13,7 @@ namespace gwg {
 // Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 8 slices x RB
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
-template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1>
+template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8>
 struct I8Tile {
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
@@ -26,7 +26,7 @@ struct I8Tile {
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
   static constexpr uint32_t B_BYTES = BN * BK;  // <= 32 KB
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_WARPS = 8;     // two per TMEM lane quarter
+  static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
   static constexpr int TMEM_COLS = 512;   // 2 accumulator buffers x BN (<= 256)
   static constexpr int OUT_Q = 16;        // output box: 16 doubles (128 B) x 32 SNPs

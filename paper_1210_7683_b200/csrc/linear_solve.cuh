@@ -27,21 +27,32 @@
 
 namespace gwg {
 
+#ifndef LIN_WIDE_MAXP
+#define LIN_WIDE_MAXP 8
+#endif
+
 template <int P>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
   static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
   static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
-  // 4 operand stages + one 4 KB staging tile per epilogue warp (3 stages +
-  // double-buffered staging measured slower on the B200: 3.21 vs 3.05 ms)
-  using Tile = I8Tile<RB, 4, 1>;
+  // WIDE (p <= 8): 16 epilogue warps (4 per TMEM lane quarter: 2 per
+  // accumulator buffer, each doing half of a tile's cells; 96 registers) with
+  // 3 operand stages — the epilogue is latency-bound, so more warps beat
+  // deeper operand buffering; otherwise (the O(p^2) solve needs registers)
+  // 8 epilogue warps (2 per quarter, all cells of alternate tiles) and 4
+  // stages.  One 4 KB staging tile per epilogue warp.
+  static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: 2.83 vs 3.15 ms at p = 4
+  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, WIDE ? 16 : 8>;
+  static constexpr int HALVES = WIDE && KT >= 2 ? 2 : 1;  // warps splitting one tile
+  static constexpr int CELLS = KT / HALVES;               // cells per warp per tile
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
-  static constexpr int ROW = KT * P;                      // results per SNP row per tile
+  static constexpr int ROW = CELLS * P;                   // results per warp row per tile
   static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
   static constexpr bool TMA_OUT = ROW % CHUNK == 0;       // whole 128-byte chunks
   // cells solved together (independent chains; KT is a power of two or 1)
-  static constexpr int GMAX = P <= 4 ? 4 : (P <= 16 ? 2 : 1);
-  static constexpr int GROUP = KT < GMAX ? KT : GMAX;
+  static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
+  static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
   static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
 };
 
@@ -78,7 +89,8 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.tiles_m * a.tiles_r;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint32_t tmem_base = i8_setup<C>(sm, warp, 4);  // one warp per quarter per tile
+  // one (or, WIDE, two) warp(s) per quarter release each tile's buffer
+  const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * (C::EPI_WARPS / 8));
 
   if (warp == 0) {
     if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, my_tiles, a.tiles_m, a.tiles_r, a.kstages,
@@ -94,7 +106,10 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     // third warp per quarter could run two phases ahead and alias the parity.)
     const int ew = warp - 4;
     const int qd = warp & 3;
-    const int h = ew >> 2;
+    const int h = (ew >> 2) & 1;           // accumulator buffer (tile parity) of this warp
+    const int hf = ew >> 3;                // WIDE: which half of the tile's cells
+    const int cell0 = hf * L::CELLS;
+    const bool active = cell0 < L::KT;
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
     int nchunk = 0;  // result chunks this warp has stored (staging tile = nchunk & 1)
     for (int lt = h; lt < my_tiles; lt += 2) {
@@ -105,10 +120,16 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
       const bool iv = il < a.rows;
       const int j0 = tr * L::KT;  // first trait of the tile
-      double sbr[L::KT];
+      if (!active) {  // KT = 1 under WIDE: nothing to do but keep the buffer protocol
+        mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);
+        continue;
+      }
+      double sbr[L::CELLS];
 #pragma unroll
-      for (int cc = 0; cc < L::KT; ++cc) {
-        const int j = j0 + cc;
+      for (int cc = 0; cc < L::CELLS; ++cc) {
+        const int j = j0 + cell0 + cc;
         sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
       }
       // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
@@ -123,7 +144,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
       // solve the group's independent cells together and store them.
       // EXP (timing experiments only): bit 1 = no solve, bit 2 = no stores,
       // 4 = release TMEM right after acc_full (no recombination)
-      auto recombine = [&](int cell0, int count, double(*dst)[P]) {
+      auto recombine = [&](int cb, int count, double(*dst)[P]) {
 #pragma unroll
         for (int u0 = 0; u0 < count; u0 += L::PAIR) {
 #pragma unroll
@@ -133,7 +154,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
             for (int u = 0; u < L::PAIR; ++u)
 #pragma unroll
               for (int sl = 0; sl < C::SLICES; ++sl)
-                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (cell0 + u0 + u) * L::P8 + c0),
+                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (cb + u0 + u) * L::P8 + c0),
                                 v[u][sl]);
             tmem_ld_wait();
 #pragma unroll
@@ -142,7 +163,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
               for (int r = 0; r < L::CW; ++r) {
                 if (c0 + r < P) {
                   const double sc =
-                      __shfl_sync(0xffffffffu, sc_lane, (cell0 + u0 + u) * L::P8 + c0 + r);
+                      __shfl_sync(0xffffffffu, sc_lane, (cb + u0 + u) * L::P8 + c0 + r);
                   dst[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
                                                      v[u][3][r], v[u][4][r], v[u][5][r],
                                                      v[u][6][r], v[u][7][r], sc);
@@ -161,15 +182,15 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
         continue;
       }
 #pragma unroll
-      for (int g0 = 0; g0 < L::KT; g0 += L::GROUP) {
+      for (int g0 = 0; g0 < L::CELLS; g0 += L::GROUP) {
         double lin[L::GROUP][P];
-        recombine(g0, L::GROUP, lin);
-        if (g0 + L::GROUP >= L::KT) release();
+        recombine(cell0 + g0, L::GROUP, lin);
+        if (g0 + L::GROUP >= L::CELLS) release();
         double beta[L::GROUP][P];
         bool ok[L::GROUP];
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {
-          const int j = j0 + g0 + u;
+          const int j = j0 + cell0 + g0 + u;
           const bool cv = j < a.t && iv;
           double cell[P + 1];
 #pragma unroll
@@ -186,7 +207,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {
           if (!ok[u]) {
-            const int j = j0 + g0 + u;
+            const int j = j0 + cell0 + g0 + u;
             atomicMin(a.err_key, (unsigned long long)(int64_t(j) * a.m_total + a.i0 + il));
 #pragma unroll
             for (int c = 0; c < P; ++c) beta[u][c] = __longlong_as_double(0x7ff8000000000000LL);
@@ -219,14 +240,14 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0)
-                  tma_store_2d(&tmap_out, tile_buf, j0 * P + (f / L::CHUNK) * L::CHUNK,
+                  tma_store_2d(&tmap_out, tile_buf, (j0 + cell0) * P + (f / L::CHUNK) * L::CHUNK,
                                tm * C::BM + qd * 32);
               }
             }
         } else if (iv && !(EXP & 2)) {
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u) {
-            const int j = j0 + g0 + u;
+            const int j = j0 + cell0 + g0 + u;
             if (j >= a.t) continue;
             double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
 #pragma unroll
