@@ -23,7 +23,6 @@
 #include "grid_kernel.cuh"
 #include "i8_core.cuh"
 
-#include <cstdlib>
 
 namespace gwg {
 
@@ -76,7 +75,7 @@ struct LinArgs {
   unsigned long long* err_key;
 };
 
-template <int P, int EXP>
+template <int P>
 __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const __grid_constant__ CUtensorMap tmap_w,
@@ -138,12 +137,10 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
       mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
-      const bool tma = L::TMA_OUT && a.use_tma && !(EXP & 2);
+      const bool tma = L::TMA_OUT && a.use_tma;
       // GROUP cells at a time: recombine their linear terms from TMEM (PAIR
       // cells per TMEM round trip), release TMEM after the last group, then
       // solve the group's independent cells together and store them.
-      // EXP (timing experiments only): bit 1 = no solve, bit 2 = no stores,
-      // 4 = release TMEM right after acc_full (no recombination)
       auto recombine = [&](int cb, int count, double(*dst)[P]) {
 #pragma unroll
         for (int u0 = 0; u0 < count; u0 += L::PAIR) {
@@ -177,10 +174,6 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for tile lt + 2
       };
-      if (EXP & 4) {
-        release();
-        continue;
-      }
 #pragma unroll
       for (int g0 = 0; g0 < L::CELLS; g0 += L::GROUP) {
         double lin[L::GROUP][P];
@@ -196,13 +189,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
           cell[P] = sbr[g0 + u];
-          if (EXP & 1) {
-            ok[u] = true;
-#pragma unroll
-            for (int c = 0; c < P; ++c) beta[u][c] = cell[c] + cell[P];
-          } else {
-            ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
-          }
+          ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
         }
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {
@@ -244,7 +231,7 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
                                tm * C::BM + qd * 32);
               }
             }
-        } else if (iv && !(EXP & 2)) {
+        } else if (iv) {
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u) {
             const int j = j0 + cell0 + g0 + u;
@@ -262,16 +249,16 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
   i8_teardown<C>(tmem_base, warp);
 }
 
-template <int P, int EXP>
+template <int P>
 cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int ctas,
                                 cudaStream_t s) {
   using C = typename LinCfg<P>::Tile;
-  cudaError_t e = cudaFuncSetAttribute(linear_solve_kernel<P, EXP>,
+  cudaError_t e = cudaFuncSetAttribute(linear_solve_kernel<P>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(C::SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  linear_solve_kernel<P, EXP><<<ctas, C::THREADS, C::SMEM_BYTES, s>>>(tx, tw, tout, a);
+  linear_solve_kernel<P><<<ctas, C::THREADS, C::SMEM_BYTES, s>>>(tx, tw, tout, a);
   return cudaGetLastError();
 }
 
@@ -288,18 +275,7 @@ LinOps make_lin_ops() {
   o.kt = LinCfg<P>::KT;
   o.p8 = LinCfg<P>::P8;
   o.rb = LinCfg<P>::RB;
-  o.launch = &launch_linear_solve<P, 0>;
-  if (P == 4) {  // timing experiments (GWG_LIN_EXP=bits), never in a shipped run
-    if (const char* v = std::getenv("GWG_LIN_EXP")) {
-      switch (std::atoi(v)) {
-        case 1: o.launch = &launch_linear_solve<P, 1>; break;
-        case 2: o.launch = &launch_linear_solve<P, 2>; break;
-        case 3: o.launch = &launch_linear_solve<P, 3>; break;
-        case 4: o.launch = &launch_linear_solve<P, 4>; break;
-        default: break;
-      }
-    }
-  }
+  o.launch = &launch_linear_solve<P>;
   return o;
 }
 
