@@ -130,3 +130,24 @@ def test_device_output_stays_inside_its_buffer(coding, layout, offset):
     if layout == "stream":
         got = got.transpose(1, 0, 2)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("n", [151, 152])  # odd n: padded leading dimension on the device
+@pytest.mark.parametrize("offset", [0, 1])  # 1: an 8-byte-aligned device operand
+def test_device_snp_operand_alignment_and_odd_n(n, offset):
+    p, m, t = 3, 77, 13
+    ds = datagen.generate(n, p, m, t, seed=n + offset)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    ref = run(ds, basis, values, "genotypes")
+    flat = torch.zeros(n * m + 8, dtype=torch.float64, device="cuda")
+    x = flat[offset: offset + n * m].view(m, n)
+    x.copy_(torch.from_numpy(np.ascontiguousarray(ds["snps"].T)))
+    out = torch.empty((m, t, p), dtype=torch.float64, device="cuda")
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_snp_coding("genotypes")
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        eng.solve_snp_slab(x.t(), out=out)
+        torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
