@@ -193,14 +193,18 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
                            const char* out_path, const gwg_run_options* opts,
                            gwg_counters* counters, gwg_status* st);
 
-/* How SNP slabs are coded.  GWG_SNP_REAL (default): any real values; the
- * rotation runs on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP
- * value is an integer code in [-127, 127] (e.g. genotypes 0/1/2); the rotation
- * then runs exactly on the int8 tensor cores (tcgen05.mma kind::i8, Z split
- * into eight 7-bit slices, FP64 recombination, ~1 ulp), and each slab is
- * checked on the device (violations fail with GWG_DIMENSION).  Results match
- * the real-valued path to rounding; both are bitwise independent of slab
- * geometry. */
+/* How SNP slabs are coded (no reference counterpart: the reference stores
+ * X_R as doubles and its generator draws genotype codes, datagen.cpp /
+ * BASELINE.json).  GWG_SNP_REAL (default): any real values; the rotation and
+ * the grid run on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP
+ * value is an integer code in [-127, 127] (e.g. genotypes 0/1/2), checked on
+ * the device (violations fail with GWG_DIMENSION); n < 262,000.  Then the
+ * rotation X'.X' and the p linear terms of every cell (x^T W, W = Z D [X_L' Y'])
+ * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, eight 7-bit
+ * slices, exact int64 recombination, one rounding) and only S_BR = (X'.X')^T D
+ * stays on DMMA — the same cells to rounding (~1e-14 norm-wise), ~3.5x faster
+ * at BASELINE config 1; results stay bitwise independent of slab geometry.
+ * Pre-rotated slabs (is_rotated = 1) always take the FP64 path. */
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
 
 /* Counters accumulated since the last reset. */
