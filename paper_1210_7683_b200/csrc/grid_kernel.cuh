@@ -53,7 +53,8 @@
 namespace gwg {
 
 // Per-trait epilogue context: 1/L_aa (p-1), strictly-lower L (packed by rows),
-// z = L^-1 b_T (p-1), flag (0 ok, else chol(S_TL) failed).
+// z = L^-1 b_T (p-1), flag (0 ok, else chol(S_TL) failed), then the full
+// lower triangle of L^-1 (packed by rows) for solve_cell_inv.
 template <int P>
 struct CtxLayout {
   static constexpr int P1 = P - 1;
@@ -62,8 +63,11 @@ struct CtxLayout {
   static constexpr int OFF = P1;
   static constexpr int Z = P1 + NOFF;
   static constexpr int FLAG = 2 * P1 + NOFF;
-  static constexpr int STRIDE = (FLAG + 2) & ~1;
+  static constexpr int LINV = FLAG + 1;
+  static constexpr int NLINV = P1 * (P1 + 1) / 2;
+  static constexpr int STRIDE = (LINV + NLINV + 1) & ~1;
   __host__ __device__ static constexpr int off_idx(int a, int c) { return a * (a - 1) / 2 + c; }
+  __host__ __device__ static constexpr int linv_idx(int a, int c) { return a * (a + 1) / 2 + c; }
 };
 
 template <int P_, int WM_OCT_, int WARPS_M_, int WARPS_T_, int BK_, int STAGES_,
@@ -171,6 +175,49 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
 #pragma unroll
     for (int c = a + 1; c < P1; ++c) r -= __ldg(cx + L::OFF + L::off_idx(c, a)) * beta[c];
     beta[a] = r * __ldg(cx + L::INVD + a);
+  }
+  return ok;
+}
+
+// The same bordered solve with the triangular solves done as products with
+// the precomputed L^-1 (trait_prep), so the p-1 components of l and of beta_T
+// are independent dot products instead of serial substitution chains: for
+// large p the epilogue is latency-bound on those chains.  Same algebra,
+// different rounding (well-conditioned S_TL); the pivot test is unchanged.
+//   l = L^-1 s_bl,  pivot = s_br - |l|^2,  beta_B = (b_B - l.z_T) / pivot,
+//   beta_T = L^-T (z_T - l beta_B)
+template <int P>
+__device__ __forceinline__ bool solve_cell_inv(const double* acc, const double* __restrict__ cx,
+                                               double* beta) {
+  using L = CtxLayout<P>;
+  constexpr int P1 = L::P1;
+  double l[P1 > 0 ? P1 : 1];
+#pragma unroll
+  for (int a = 0; a < P1; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c <= a; ++c) s = fma(__ldg(cx + L::LINV + L::linv_idx(a, c)), acc[c], s);
+    l[a] = s;
+  }
+  double sq = 0.0, lz = 0.0;
+#pragma unroll
+  for (int a = 0; a < P1; ++a) {
+    sq = fma(l[a], l[a], sq);
+    lz = fma(l[a], __ldg(cx + L::Z + a), lz);
+  }
+  const double pivot = acc[P] - sq;
+  const bool ok = !(pivot <= 0.0) && __ldg(cx + L::FLAG) == 0.0;
+  const double bb = (acc[P1] - lz) / pivot;
+  beta[P1] = bb;
+  double r[P1 > 0 ? P1 : 1];
+#pragma unroll
+  for (int a = 0; a < P1; ++a) r[a] = fma(-l[a], bb, __ldg(cx + L::Z + a));
+#pragma unroll
+  for (int c = 0; c < P1; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = c; a < P1; ++a) s = fma(__ldg(cx + L::LINV + L::linv_idx(a, c)), r[a], s);
+    beta[c] = s;
   }
   return ok;
 }

@@ -53,6 +53,12 @@ struct LinCfg {
   static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
   static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
+  // large p: triangular solves as products with L^-1 (independent dot
+  // products instead of serial substitution chains)
+#ifndef LIN_INV_MINP
+#define LIN_INV_MINP 9
+#endif
+  static constexpr bool INV_SOLVE = P >= LIN_INV_MINP;
 };
 
 struct LinArgs {
@@ -189,7 +195,9 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
           cell[P] = sbr[g0 + u];
-          ok[u] = solve_cell<P>(cell, a.ctx + size_t(cv ? j : 0) * CX::STRIDE, beta[u]) || !cv;
+          const double* cx = a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
+          ok[u] = (L::INV_SOLVE ? solve_cell_inv<P>(cell, cx, beta[u])
+                                : solve_cell<P>(cell, cx, beta[u])) || !cv;
         }
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {

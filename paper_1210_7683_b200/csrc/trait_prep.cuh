@@ -178,6 +178,14 @@ __global__ void __launch_bounds__(256) trait_prep_kernel(const PrepArgs a) {
         cx[L::Z + r] = z[r];
         for (int c = 0; c < r; ++c) cx[L::OFF + L::off_idx(r, c)] = l[r * LD + c];
       }
+      // L^-1, column by column (forward substitution on the unit vectors)
+      for (int c = 0; c < P1; ++c) {
+        for (int r = c; r < P1; ++r) {
+          double v = r == c ? 1.0 : 0.0;
+          for (int q = c; q < r; ++q) v -= l[r * LD + q] * cx[L::LINV + L::linv_idx(q, c)];
+          cx[L::LINV + L::linv_idx(r, c)] = v / l[r * LD + r];
+        }
+      }
     }
     cx[L::FLAG] = ok ? 0.0 : 1.0;
   }
