@@ -88,7 +88,8 @@ struct gwg_engine {
   bool slices_valid = false;
   gwg_host::DevBuf zslices, zscale, xi8;
   // Split grid for genotype slabs (grid_split.cuh): linear terms x_i^T W on
-  // the int8 tensor cores, quadratic term + solve on DMMA.  `split` = use it
+  // the int8 tensor cores fused with the solve, quadratic term S_BR on DMMA.
+  // `split` = use it
   // (GWG_SPLIT=0 in the environment turns it off for A/B timing);
   // `slab_i8` = the current slab was rotated from integer codes (xi8 valid).
   bool split = true, slab_i8 = false;
@@ -98,7 +99,7 @@ struct gwg_engine {
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
   cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
-  cudaEvent_t ev_s[3];     // split grid: before the linear launch, between, after quad
+  cudaEvent_t ev_s[3];     // split grid: before gls_sbr, before linear_solve, after it
   bool split_timed = false;
   std::vector<cudaEvent_t> slab_events;
 
