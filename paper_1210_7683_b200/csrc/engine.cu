@@ -189,7 +189,7 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
 // 2-D uint8 map over a K-major int8 operand (kp x cols) and 3-D map over
 // SLICES planes of (kp x ncols), both SWIZZLE_128B boxes for tcgen05.
 int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensorMap* tb,
-              const void* slices, int64_t ncols, int rb, gwg_status* st) {
+              const void* slices, int64_t ncols, int rb, int slices_box, gwg_status* st) {
   using gwg::I8Cfg;
   auto encode = get_encode();
   if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
@@ -207,7 +207,7 @@ int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensor
   {
     const cuuint64_t gdim[3] = {cuuint64_t(kp), cuuint64_t(ncols), cuuint64_t(I8Cfg::SLICES)};
     const cuuint64_t gstride[2] = {cuuint64_t(kp), cuuint64_t(ncols) * kp};
-    const cuuint32_t box[3] = {I8Cfg::BK, cuuint32_t(rb), I8Cfg::SLICES};
+    const cuuint32_t box[3] = {I8Cfg::BK, cuuint32_t(rb), cuuint32_t(slices_box)};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = encode(tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(slices), gdim,
                         gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -222,9 +222,8 @@ int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensor
 // rotate_i8_kernel over `cols` int8 SNP columns against the sliced columns
 // (scale, ncols): dst[i * ldd + r] (and dst_sq) for r < ncols, either may be
 // null.  Outputs leave through TMA stores: ldd even, 16-byte aligned bases.
-int launch_i8(gwg_engine* e, const CUtensorMap& tx, const CUtensorMap& tb, int64_t cols,
-              int64_t ncols, const double* scale, double* dst, double* dst_sq, int64_t ldd,
-              gwg_status* st) {
+int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, int64_t ncols,
+              const double* scale, double* dst, double* dst_sq, int64_t ldd, gwg_status* st) {
   using gwg::I8Cfg;
   auto encode = get_encode();
   if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
@@ -254,13 +253,20 @@ int launch_i8(gwg_engine* e, const CUtensorMap& tx, const CUtensorMap& tb, int64
   a.tiles_r = int32_t(ceil_div(ncols, I8Cfg::RB));
   a.kstages = int32_t(kp / I8Cfg::BK);
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
-  const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
-  GWG_CUDA_TRY(cudaFuncSetAttribute(gwg::rotate_i8_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(I8Cfg::SMEM_BYTES)));
-  gwg::rotate_i8_kernel<<<int(std::min<int64_t>(tiles, e->sms)), I8Cfg::THREADS,
-                          I8Cfg::SMEM_BYTES, e->comp>>>(tx, tb, td[0], td[1], a);
-  GWG_CUDA_TRY(cudaGetLastError());
+  // CTA pairs multicasting the B (Z-slice) tile when it streams from HBM
+  // (measured at n = 10,000: 69.2 -> 49.0 ms; neutral at n = 1000)
+  const int cl = e->i8_cluster ? e->i8_cluster : (e->n >= 4096 ? 2 : 1);
+  CUtensorMap tx, tb;
+  if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB, I8Cfg::SLICES / cl,
+                         st))
+    return rc;
+  const int64_t units = int64_t((a.tiles_m + cl - 1) / cl) * a.tiles_r;
+  if (cl == 2)
+    GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<2>>(gwg::rotate_i8_kernel<2>, units, e->sms,
+                                                  e->comp, tx, tb, td[0], td[1], a));
+  else
+    GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<1>>(gwg::rotate_i8_kernel<1>, units, e->sms,
+                                                  e->comp, tx, tb, td[0], td[1], a));
   e->counters.kernel_launches += 1;
   return GWG_OK;
 }
@@ -291,12 +297,9 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
   }
-  CUtensorMap tx, tz;
-  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, cols, &tz, e->zslices.ptr, n, I8Cfg::RB, st))
-    return rc;
   // the split grid needs only X'.X' (its linear terms come from the codes)
-  if (int rc = launch_i8(e, tx, tz, cols, n, e->zscale.d(), e->split ? nullptr : e->rot.d(),
-                         e->rot_sq.d(), e->np, st))
+  if (int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
+                         e->split ? nullptr : e->rot.d(), e->rot_sq.d(), e->np, st))
     return rc;
   e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
   e->slab_i8 = true;
@@ -407,8 +410,12 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   e->counters.kernel_launches += 1;
 
   // ---- linear terms (int8 tcgen05) + solve ----
+  // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
+  // c2 22.5 -> 20.9, c4 43.1 -> 40.4)
+  const int cl = e->i8_cluster ? e->i8_cluster : 2;
   CUtensorMap tx, tw, tout;
-  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb, st))
+  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb,
+                         e->lops.b_slices_box[cl - 1], st))
     return rc;
   // numpy layout with a 16-byte pitch and base: results leave by TMA store
   const bool use_tma = out_sj == 1 && (out_si * p) % 2 == 0 &&
@@ -444,7 +451,8 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
-  GWG_CUDA_TRY(e->lops.launch(tx, tw, tout, a, int(std::min<int64_t>(tiles, e->sms)), e->comp));
+  (void)tiles;
+  GWG_CUDA_TRY(e->lops.launch[cl - 1](tx, tw, tout, a, e->sms, e->comp));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[2], e->comp));
   e->split_timed = true;
   e->counters.kernel_launches += 1;
@@ -578,6 +586,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     e->sops = gwg::sbr_ops(v ? std::atoi(v) : 0);
   }
   if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
+  if (const char* cl = std::getenv("GWG_I8_CLUSTER")) e->i8_cluster = std::atoi(cl) == 2 ? 2 : (std::atoi(cl) == 1 ? 1 : 0);
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
     gwg_engine_destroy(e);

@@ -7,14 +7,22 @@
 
 #include "gwg_device.cuh"
 
+#include <algorithm>
+#include <utility>
+
 namespace gwg {
 
 
 // Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 8 slices x RB
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
-template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8>
+template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1>
 struct I8Tile {
+  // CLUSTER = 2: CTA pairs (a thread-block cluster) work on SNP tiles 2u and
+  // 2u+1 against the same B rows; each CTA loads half of the B tile (4 of the
+  // 8 slices) and multicasts it to both, halving the B operand's L2->SMEM
+  // traffic (used where B dominates: large n, one trait per tile).
+  static constexpr int CLUSTER = CLUSTER_;
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
   static constexpr int SLICES = 8;
@@ -25,6 +33,8 @@ struct I8Tile {
   static constexpr int OUT_BUFS = OUT_BUFS_;     // staging tiles per epilogue warp
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
   static constexpr uint32_t B_BYTES = BN * BK;  // <= 32 KB
+  static constexpr int B_SLICES_PER_CTA = SLICES / CLUSTER;
+  static constexpr uint32_t B_PART = B_BYTES / CLUSTER;  // loaded (and multicast) per CTA
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
@@ -118,6 +128,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
         "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
+}
+
+// 3-D TMA load multicast to the CTAs in cta_mask (same smem offset and
+// mbarrier offset in each destination CTA).
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int32_t c0,
+                                               int32_t c1, int32_t c2, uint64_t* bar,
+                                               uint16_t cta_mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+      "h"(cta_mask), "l"(policy)
+      : "memory");
+}
+
+// MMA completion -> arrive on the same-offset mbarrier of every CTA in cta_mask.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+
+// All threads of the cluster (release/acquire: barrier inits, smem writes).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // 8 consecutive TMEM columns of this warp's 32 lanes into 8 registers.
@@ -219,7 +258,7 @@ __device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp,
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
+      mbar_init(&sm.empty[s], C::CLUSTER);  // the MMA of every CTA reading this stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.acc_full[b], 1);
@@ -236,14 +275,20 @@ __device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp,
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (C::CLUSTER > 1)
+    cluster_sync_all();  // the peer's barriers exist before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   return *sm.tmem_slot;
 }
 
 template <class C>
 __device__ __forceinline__ void i8_teardown(uint32_t tmem_base, int warp) {
-  __syncthreads();
+  if (C::CLUSTER > 1)
+    cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
+  else
+    __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(C::TMEM_COLS)
@@ -267,29 +312,55 @@ __device__ __forceinline__ void i8_tile_coords(int tile, int tiles_m, int tiles_
   tm = grp * I8_GROUP_M + (rem - tr * rows);
 }
 
+// Persistent static schedule over scheduling units (one CTA, or one CTA pair
+// for CLUSTER = 2: the pair takes SNP tiles 2u and 2u+1 of one B tile).
+template <class C>
+struct I8Sched {
+  int rank, unit, units, tm_units, tiles_r, my_tiles;
+  __device__ I8Sched(int tiles_m, int tiles_r_) : tiles_r(tiles_r_) {
+    rank = C::CLUSTER > 1 ? int(blockIdx.x % C::CLUSTER) : 0;
+    unit = int(blockIdx.x / C::CLUSTER);
+    units = int(gridDim.x / C::CLUSTER);
+    tm_units = (tiles_m + C::CLUSTER - 1) / C::CLUSTER;
+    const int ntiles = tm_units * tiles_r;
+    my_tiles = unit < ntiles ? (ntiles - 1 - unit) / units + 1 : 0;
+  }
+  __device__ void coords(int lt, int& tm, int& tr) const {
+    int tu;
+    i8_tile_coords(unit + lt * units, tm_units, tiles_r, tu, tr);
+    tm = tu * C::CLUSTER + rank;
+  }
+};
+
 // Warp 0, one thread: A = int8 SNP tile (box 128 k x 128 SNPs), B = RB rows
 // of all 8 slices (box 128 k x RB x 8).  Tiles: i8_tile_coords (the rows
 // of the sliced operand fastest, so the SNP tile is reused from L2).
 template <class C>
 __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMap* tmap_x,
-                                           const CUtensorMap* tmap_b, int my_tiles, int tiles_m,
-                                           int tiles_r, int kstages, bool b_resident) {
+                                           const CUtensorMap* tmap_b, const I8Sched<C>& sch,
+                                           int kstages, bool b_resident) {
   // B small enough to stay in L2 for the whole launch: keep it (evict_last)
   // and stream A; otherwise both ride the group rasterisation (evict_normal)
   const uint64_t pol_x = b_resident ? policy_evict_first() : policy_evict_normal();
   const uint64_t pol_b = b_resident ? policy_evict_last() : policy_evict_normal();
   int g = 0;
-  for (int lt = 0; lt < my_tiles; ++lt) {
-    const int tile = blockIdx.x + lt * gridDim.x;
+  for (int lt = 0; lt < sch.my_tiles; ++lt) {
     int tm, tr;
-    i8_tile_coords(tile, tiles_m, tiles_r, tm, tr);
+    sch.coords(lt, tm, tr);
     for (int ks = 0; ks < kstages; ++ks, ++g) {
       const int s = g % C::STAGES;
+      // CLUSTER = 2: empty[s] completes only when BOTH CTAs' MMAs are done with
+      // stage s, since this CTA's multicast also writes the peer's stage
       if (g >= C::STAGES) mbar_wait(&sm.empty[s], ((g / C::STAGES) - 1) & 1);
       mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
       tma_load_2d(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
-      tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
+      if (C::CLUSTER > 1)
+        tma_load_3d_mc(st + C::A_BYTES + sch.rank * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
+                       sch.rank * C::B_SLICES_PER_CTA, &sm.full[s],
+                       uint16_t((1u << C::CLUSTER) - 1), pol_b);
+      else
+        tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
     }
   }
 }
@@ -298,6 +369,7 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
 template <class C>
 __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, int my_tiles,
                                        int kstages) {
+  constexpr uint16_t mask = uint16_t((1u << C::CLUSTER) - 1);
   constexpr uint32_t idesc = i8_instr_desc<C::BN, C::BM>();
   int g = 0;
   for (int lt = 0; lt < my_tiles; ++lt) {
@@ -315,10 +387,39 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
       for (int k = 0; k < C::BK / C::UK; ++k)
         umma_i8(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK), idesc,
                 (ks | k) != 0);
-      umma_commit(&sm.empty[s]);  // frees the smem stage when these MMAs finish
+      // frees the smem stage (in every CTA of the pair) when these MMAs finish
+      if (C::CLUSTER > 1)
+        umma_commit_mc(&sm.empty[s], mask);
+      else
+        umma_commit(&sm.empty[s]);
     }
     umma_commit(&sm.acc_full[buf]);  // accumulator ready for the epilogue
   }
+}
+
+// Host: launch an I8Tile kernel over `units` scheduling units (CTA pairs for
+// CLUSTER = 2) with at most `sms` CTAs, in clusters of C::CLUSTER CTAs.
+template <class C, typename... KArgs, typename... Args>
+cudaError_t i8_launch(void (*kern)(KArgs...), int64_t units, int sms, cudaStream_t s,
+                      Args&&... args) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(C::SMEM_BYTES));
+  if (e != cudaSuccess) return e;
+  const int64_t max_units = sms / C::CLUSTER;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, max_units))) * C::CLUSTER;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CLUSTER;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace gwg

@@ -30,7 +30,7 @@ namespace gwg {
 #define LIN_WIDE_MAXP 8
 #endif
 
-template <int P>
+template <int P, int CL = 1>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
   static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
@@ -42,7 +42,7 @@ struct LinCfg {
   // 8 epilogue warps (2 per quarter, all cells of alternate tiles) and 4
   // stages.  One 4 KB staging tile per epilogue warp.
   static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: 2.83 vs 3.15 ms at p = 4
-  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, WIDE ? 16 : 8>;
+  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, WIDE ? 16 : 8, CL>;
   static constexpr int HALVES = WIDE && KT >= 2 ? 2 : 1;  // warps splitting one tile
   static constexpr int CELLS = KT / HALVES;               // cells per warp per tile
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
@@ -81,24 +81,24 @@ struct LinArgs {
   unsigned long long* err_key;
 };
 
-template <int P>
-__global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
+template <int P, int CL>
+__global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const __grid_constant__ CUtensorMap tmap_w,
                         const __grid_constant__ CUtensorMap tmap_out, const LinArgs a) {
-  using L = LinCfg<P>;
+  using L = LinCfg<P, CL>;
   using C = typename L::Tile;
   using CX = CtxLayout<P>;
   extern __shared__ __align__(1024) unsigned char smem_ls[];
   const I8Smem<C> sm(smem_ls);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = a.tiles_m * a.tiles_r;
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const I8Sched<C> sch(a.tiles_m, a.tiles_r);
+  const int my_tiles = sch.my_tiles;
   // one (or, WIDE, two) warp(s) per quarter release each tile's buffer
   const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * (C::EPI_WARPS / 8));
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, my_tiles, a.tiles_m, a.tiles_r, a.kstages,
+    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, sch, a.kstages,
                                     a.b_resident != 0);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
@@ -119,9 +119,8 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
     int nchunk = 0;  // result chunks this warp has stored (staging tile = nchunk & 1)
     for (int lt = h; lt < my_tiles; lt += 2) {
       const int buf = lt & 1;
-      const int tile = blockIdx.x + lt * gridDim.x;
       int tm, tr;
-      i8_tile_coords(tile, a.tiles_m, a.tiles_r, tm, tr);
+      sch.coords(lt, tm, tr);
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
       const bool iv = il < a.rows;
       const int j0 = tr * L::KT;  // first trait of the tile
@@ -257,24 +256,22 @@ __global__ void __launch_bounds__(LinCfg<P>::Tile::THREADS, 1)
   i8_teardown<C>(tmem_base, warp);
 }
 
-template <int P>
+template <int P, int CL>
 cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
-                                const CUtensorMap& tout, const LinArgs& a, int ctas,
+                                const CUtensorMap& tout, const LinArgs& a, int sms,
                                 cudaStream_t s) {
-  using C = typename LinCfg<P>::Tile;
-  cudaError_t e = cudaFuncSetAttribute(linear_solve_kernel<P>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(C::SMEM_BYTES));
-  if (e != cudaSuccess) return e;
-  linear_solve_kernel<P><<<ctas, C::THREADS, C::SMEM_BYTES, s>>>(tx, tw, tout, a);
-  return cudaGetLastError();
+  using C = typename LinCfg<P, CL>::Tile;
+  const int64_t units = int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
+  return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a);
 }
 
 // Per-p entry of the split grid (kernels_lin_*.cu).
 struct LinOps {
   int kt = 0, p8 = 0, rb = 0;
-  cudaError_t (*launch)(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                        const LinArgs&, int, cudaStream_t) = nullptr;
+  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile
+  cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
+  int b_slices_box[2] = {8, 4};
 };
 
 template <int P>
@@ -283,7 +280,8 @@ LinOps make_lin_ops() {
   o.kt = LinCfg<P>::KT;
   o.p8 = LinCfg<P>::P8;
   o.rb = LinCfg<P>::RB;
-  o.launch = &launch_linear_solve<P>;
+  o.launch[0] = &launch_linear_solve<P, 1>;
+  o.launch[1] = &launch_linear_solve<P, 2>;
   return o;
 }
 

@@ -41,21 +41,25 @@ struct I8Args {
 
 // ---- the rotation kernel -------------------------------------------------------
 
-__global__ void __launch_bounds__(I8Cfg::THREADS, 1)
+template <int CL>
+using RotI8Cfg = I8Tile<32, 4, 1, 8, CL>;
+
+template <int CL>
+__global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
     rotate_i8_kernel(const __grid_constant__ CUtensorMap tmap_x,
                      const __grid_constant__ CUtensorMap tmap_z,
                      const __grid_constant__ CUtensorMap tmap_d,
                      const __grid_constant__ CUtensorMap tmap_d2, const I8Args a) {
-  using C = I8Cfg;
+  using C = RotI8Cfg<CL>;
   extern __shared__ __align__(1024) unsigned char smem_i8[];
   const I8Smem<C> sm(smem_i8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = a.tiles_m * a.tiles_r;
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const I8Sched<C> sch(a.tiles_m, a.tiles_r);
+  const int my_tiles = sch.my_tiles;
   const uint32_t tmem_base = i8_setup<C>(sm, warp);
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_z, my_tiles, a.tiles_m, a.tiles_r, a.kstages,
+    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_z, sch, a.kstages,
                                     a.b_resident != 0);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
@@ -70,9 +74,8 @@ __global__ void __launch_bounds__(I8Cfg::THREADS, 1)
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
     for (int lt = 0; lt < my_tiles; ++lt) {
       const int buf = lt & 1;
-      const int tile = blockIdx.x + lt * gridDim.x;
       int tm, tr;
-      i8_tile_coords(tile, a.tiles_m, a.tiles_r, tm, tr);
+      sch.coords(lt, tm, tr);
       const int r0 = tr * C::RB + h * C::OUT_Q;
       double x[C::OUT_Q];
       mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
