@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 
     // ---------------- fused epilogue: bordered Cholesky + store -----------------
     using L = CtxLayout<P>;
+    const uint64_t pol_out = policy_evict_first();
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int j = tt * Cfg::BT + wt * 8 + 2 * (lane & 3) + e;
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           for (int c = 0; c < P; ++c) beta[c] = __longlong_as_double(0x7ff8000000000000LL);
         }
 #pragma unroll
-        for (int c = 0; c < P; ++c) __stcs(dst + c, beta[c]);
+        for (int c = 0; c < P; ++c) st_evict_first(dst + c, beta[c], pol_out);
       }
     }
   }

@@ -83,6 +83,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Result store with an L2 evict_first hint: on the B200 plain stores of
+// results that are not re-read made L2 fetch the written lines from HBM first
+// (measured: ~0.5-1 GB of extra DRAM reads per launch at config 1).
+__device__ __forceinline__ void st_evict_first(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+               : "memory");
+}
+
 // FP64 tensor-core MMA, 8x8x4 (SASS DMMA.8x8x4): C[8x8] += A[8x4] B[4x8].
 // Fragment ownership (lane l): a = A[l>>2][l&3], b = B[l&3][l>>2],
 // c = C[l>>2][2(l&3) + {0,1}].

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     const int cell0 = hf * L::CELLS;
     const bool active = cell0 < L::KT;
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
+    const uint64_t pol_out = policy_evict_first();
     int nchunk = 0;  // result chunks this warp has stored (staging tile = nchunk & 1)
     for (int lt = h; lt < my_tiles; lt += 2) {
       const int buf = lt & 1;
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             if (j >= a.t) continue;
             double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
 #pragma unroll
-            for (int c = 0; c < P; ++c) __stcs(dst + c, beta[u][c]);
+            for (int c = 0; c < P; ++c) st_evict_first(dst + c, beta[u][c], pol_out);
           }
         }
       }

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(RotCfg::THREADS, 1)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     // store: acc[i][j][e] = dst[r][col], r = row octet i, col = 2(lane&3)+e of octet j
+    const uint64_t pol_out = policy_evict_first();
 #pragma unroll
     for (int i = 0; i < C::WM_OCT; ++i) {
       const int r = tm * C::BM + (wm * C::WM_OCT + i) * 8 + (lane >> 2);
@@ -160,8 +161,10 @@ __global__ void __launch_bounds__(RotCfg::THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           const int col = tn * C::BN + (wn * C::WN_OCT + j) * 8 + 2 * (lane & 3) + e;
           if (col < a.cols) {
-            a.dst[int64_t(col) * a.ldd + r] = acc[i][j][e];
-            if (a.dst_sq) a.dst_sq[int64_t(col) * a.ldd + r] = acc[i][j][e] * acc[i][j][e];
+            st_evict_first(a.dst + int64_t(col) * a.ldd + r, acc[i][j][e], pol_out);
+            if (a.dst_sq)
+              st_evict_first(a.dst_sq + int64_t(col) * a.ldd + r, acc[i][j][e] * acc[i][j][e],
+                             pol_out);
           }
         }
       }
