@@ -306,6 +306,10 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   return GWG_OK;
 }
 
+bool rotated_x_unused(const gwg_engine* e) {
+  return e->snp_coding == GWG_SNP_GENOTYPES && e->split;
+}
+
 void invalidate_derived(gwg_engine* e, bool spectrum) {
   e->split_valid = false;
   if (spectrum) {
@@ -791,7 +795,9 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
                       (long long)mb);
   const int64_t n = e->n, t = e->t, p = e->p;
   if (layout == GWG_LAYOUT_NUMPY) ldo = mb;
-  GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  // X' itself is only needed by the FP64 grid (the genotype split grid reads X'.X')
+  if (is_rotated || !rotated_x_unused(e))
+    GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
   if (is_rotated) {
@@ -909,7 +915,7 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
     GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));
     GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
   }
-  GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  if (!rotated_x_unused(e)) GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   const int64_t slabs = ceil_div(m, mb);
   while (int64_t(e->slab_events.size()) < 2 * slabs) {

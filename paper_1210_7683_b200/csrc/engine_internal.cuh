@@ -120,6 +120,8 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
            int64_t lds = 0, double* dst_sq = nullptr, const double* basis = nullptr);
 // Split-grid trait operands (W slices, D panels) for the current traits.
 int build_split(gwg_engine* e, gwg_status* st);
+// Genotype split grid on raw slabs: X' is never materialised (only X'.X').
+bool rotated_x_unused(const gwg_engine* e);
 // Invalidate everything derived from traits / spectrum.
 void invalidate_derived(gwg_engine* e, bool spectrum);
 // SNP slab -> e->rot / e->rot_sq with the engine's SNP coding (DMMA or int8).

@@ -258,7 +258,8 @@ int staged_pipeline(gwg_engine* e, int64_t m, int64_t mb, bool rotated, int out_
     GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));
     GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
   }
-  GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
+  if (rotated || !rotated_x_unused(e))
+    GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   if (int rc = reset_errors(e, st)) return rc;
   for (int b = 0; b < 2; ++b) {
