@@ -5,18 +5,21 @@
 // GEMM view per CTA tile: M = 128 SNPs (A = int8 genotype codes, K-major),
 // N = 8 slices x RB rows of W (B, K-major), K = samples; int32 accumulators in
 // TMEM, double-buffered (the TMA producer / MMA issuer / TMEM code is shared
-// with rotate_i8_kernel).  W is laid out per tile of KT traits, each trait's p
-// columns padded to P8 (a power of two <= 8, else a multiple of 8) so that a
-// trait's columns are one aligned tcgen05.ld.
+// with rotate_i8_kernel); CTA pairs (cluster of 2) take SNP tiles 2u, 2u+1 of
+// the same W rows and multicast halves of the W-slice tile.  W is laid out per
+// tile of KT traits, each trait's p columns padded to P8 (a power of two <= 8,
+// else a multiple of 8) so that a trait's columns are one aligned tcgen05.ld.
 //
-// Epilogue (8 warps, two per TMEM lane quarter taking alternate tiles; thread
-// = SNP row): per cell
-// (i, j) the p linear terms x_i^T W_{j,c} are recombined exactly from the
-// eight slice products (i8_recombine, one rounding), S_BR[j][i] comes from
-// gls_sbr_kernel (prefetched before the accumulator wait), and solve_cell<P>
-// — the same bordered Cholesky as the all-FP64 kernel — produces b_ij, which
-// leaves through a 128B-swizzled staging tile and a TMA store (numpy layout)
-// or direct stores (stream layout).  Failed cells: NaN + the min error key,
+// Epilogue (thread = SNP row): 16 warps for p <= 8 (two per accumulator
+// buffer and TMEM lane quarter, each half of a tile's cells), else 8 (one per
+// buffer and quarter, all cells).  Per cell (i, j) the p linear terms
+// x_i^T W_{j,c} are recombined exactly from the eight slice products
+// (i8_recombine, one rounding), S_BR[j][i] comes from gls_sbr_kernel
+// (prefetched before the accumulator wait), and the bordered Cholesky —
+// solve_cell<P> as in the all-FP64 kernel, or solve_cell_inv<P> with the
+// precomputed L^-1 for p >= 9 — produces b_ij, which leaves through a
+// 128B-swizzled staging tile and an evict_first TMA store (numpy layout) or
+// direct stores (stream layout).  Failed cells: NaN + the min error key,
 // exactly like gls_grid_kernel.
 #pragma once
 
