@@ -10,7 +10,7 @@
 // tile of KT traits, each trait's p columns padded to P8 (a power of two <= 8,
 // else a multiple of 8) so that a trait's columns are one aligned tcgen05.ld.
 //
-// Epilogue (thread = SNP row): 16 warps for p <= 8 (two per accumulator
+// Epilogue (thread = SNP row): 16 warps for p <= 16 (two per accumulator
 // buffer and TMEM lane quarter, each half of a tile's cells), else 8 (one per
 // buffer and quarter, all cells).  Per cell (i, j) the p linear terms
 // x_i^T W_{j,c} are recombined exactly from the eight slice products
@@ -30,7 +30,7 @@
 namespace gwg {
 
 #ifndef LIN_WIDE_MAXP
-#define LIN_WIDE_MAXP 8
+#define LIN_WIDE_MAXP 16
 #endif
 
 template <int P, int CL = 1>
@@ -38,13 +38,13 @@ struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
   static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
   static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
-  // WIDE (p <= 8): 16 epilogue warps (4 per TMEM lane quarter: 2 per
+  // WIDE (p <= 16): 16 epilogue warps (4 per TMEM lane quarter: 2 per
   // accumulator buffer, each doing half of a tile's cells; 96 registers) with
   // 3 operand stages — the epilogue is latency-bound, so more warps beat
   // deeper operand buffering; otherwise (the O(p^2) solve needs registers)
   // 8 epilogue warps (2 per quarter, all cells of alternate tiles) and 4
   // stages.  One 4 KB staging tile per epilogue warp.
-  static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: 2.83 vs 3.15 ms at p = 4
+  static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: p=4 3.15 -> 2.83 ms, p=12 8.56 -> 7.95
   using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, WIDE ? 16 : 8, CL>;
   static constexpr int HALVES = WIDE && KT >= 2 ? 2 : 1;  // warps splitting one tile
   static constexpr int CELLS = KT / HALVES;               // cells per warp per tile
