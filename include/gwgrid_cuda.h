@@ -69,9 +69,13 @@ typedef struct gwg_counters {
   double wall_ms;              /* host wall time of the last run_grid                */
   /* genotype split grid (gwg_solve_snp_slab only), both inside grid_kernel_ms:
    * linear_ms = int8 linear terms + Cholesky solve (linear_solve_kernel),
-   * quad_ms = S_BR = (X'.X')^T D on DMMA (gls_sbr_kernel) */
+   * quad_ms = S_BR on DMMA (gls_sbr_kernel launches) */
   double linear_ms;
   double quad_ms;
+  /* S_BR work actually issued on DMMA: 2 n t per SNP direct, 2 r (n + t) per
+   * SNP factorised; sbr_terms = r of the last slab (0 = direct contraction) */
+  uint64_t sbr_flops;
+  int64_t sbr_terms;
 } gwg_counters;
 
 typedef struct gwg_run_options {
@@ -217,6 +221,15 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st);
 /* The engine's compute stream (cudaStream_t as void*), so callers can order
  * their own device work (timing events, torch streams) against it. */
 void* gwg_compute_stream(gwg_engine* e);
+
+/* Positive exponential sum for 1/x on [x_min, x_max] (the low-rank
+ * factorisation of the GLS weights behind the genotype grid's S_BR term, see
+ * csrc/expsum.cpp):  1/x ~= sum_r w[r] exp(-s[r] x),  s[0] = 0, all w > 0,
+ * relative error <= ~2^-52 uniformly.  *terms = r, a multiple of `multiple`;
+ * s / w may be NULL to query r.  GWG_DIMENSION if x_min <= 0, x_max < x_min,
+ * or r would exceed max_terms.  Host-only (no device needed). */
+int32_t gwg_exp_sum_design(double x_min, double x_max, int32_t multiple, int32_t max_terms,
+                           double* s, double* w, int32_t* terms);
 
 /* Seeded synthetic inputs with BASELINE.json's generators (counter-based
  * splitmix64 per (seed, matrix, column, row), so any column range is

@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "gwg_stream_info",
     "gwg_set_traits_file",
     "gwg_run_grid_files",
+    "gwg_exp_sum_design",
     "gwg_gen_genotypes",
     "gwg_gen_normals",
     "gwg_gen_uniform",
@@ -78,6 +79,8 @@ class Counters(ctypes.Structure):
         ("wall_ms", ctypes.c_double),
         ("linear_ms", ctypes.c_double),
         ("quad_ms", ctypes.c_double),
+        ("sbr_flops", ctypes.c_uint64),
+        ("sbr_terms", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -135,6 +138,7 @@ def load() -> ctypes.CDLL:
         "gwg_gen_genotypes": (None, [U64, I32, I64, I64, I64, I32, P, I64]),
         "gwg_gen_normals": (None, [U64, I32, I64, I64, I64, P, I64]),
         "gwg_gen_uniform": (None, [U64, I32, I64, D, D, P]),
+        "gwg_exp_sum_design": (I32, [D, D, I32, I32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

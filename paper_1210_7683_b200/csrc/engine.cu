@@ -318,6 +318,69 @@ void invalidate_derived(gwg_engine* e, bool spectrum) {
   }
 }
 
+// E and F of the low-rank S_BR (expsum.cpp) for the current traits, or
+// sbr_terms = 0 when D is outside the factorisation's range: some
+// h lambda + 1 - h <= 0 (the trait check reports those), non-finite scales,
+// or x_max / x_min so wide that more than kMaxTerms terms would be needed.
+constexpr int32_t kMaxTerms = 512;
+int build_expsum(gwg_engine* e, gwg_status* st) {
+  e->sbr_terms = 0;
+  if (!e->lowrank) return GWG_OK;
+  const int64_t n = e->n, np = e->np, t = e->t;
+  GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * kMaxTerms) * sizeof(double)));
+  double* dx = e->exps.d();
+  gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(), e->sigma2.d(),
+                                                    int32_t(t), dx);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  double rg[6];
+  GWG_CUDA_TRY(cudaMemcpyAsync(rg, dx, sizeof(rg), cudaMemcpyDeviceToHost, e->comp));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  if (rg[5] != 0.0) return GWG_OK;
+  double x_min = 1.0, x_max = 1.0;  // all h = 0: only the constant term is used
+  if (rg[4] > 0.0) {
+    x_min = rg[0] + rg[2];
+    x_max = rg[1] + rg[3];
+  }
+  // r: a whole number of S_BR column tiles (GEMM 1) and k-chunks (GEMM 2)
+  const int32_t mult = std::lcm(e->sops.bt, e->sops.bk);
+  int32_t r = 0;
+  if (gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nullptr, nullptr, &r) != GWG_OK)
+    return GWG_OK;
+  std::vector<double> nodes(2 * size_t(r));
+  gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nodes.data(), nodes.data() + r, &r);
+  GWG_CUDA_TRY(cudaMemcpyAsync(dx + 8, nodes.data(), nodes.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, e->comp));
+  const int64_t bt = e->sops.bt;
+  const int64_t t_pad = round_up(t, bt);
+  GWG_CUDA_TRY(e->epanel.ensure(size_t(r) * np * sizeof(double)));
+  GWG_CUDA_TRY(e->fpanel.ensure(size_t(t_pad) * r * sizeof(double)));
+  if (t_pad != t)  // padded traits of the last tile contribute zeros
+    GWG_CUDA_TRY(cudaMemsetAsync(e->fpanel.d() + size_t(t_pad - bt) * r, 0,
+                                 size_t(bt) * r * sizeof(double), e->comp));
+  gwg::ExpSumArgs a;
+  a.n = n;
+  a.np = np;
+  a.t = int32_t(t);
+  a.r = r;
+  a.bt = int32_t(bt);
+  a.lambda = e->lambda.d();
+  a.h2 = e->h2.d();
+  a.sigma2 = e->sigma2.d();
+  a.s = dx + 8;
+  a.w = dx + 8 + r;
+  a.lam0 = rg[0];
+  a.epanel = e->epanel.d();
+  a.fpanel = e->fpanel.d();
+  gwg::expsum_e_kernel<<<r, 256, 0, e->comp>>>(a);
+  GWG_CUDA_TRY(cudaGetLastError());
+  gwg::expsum_f_kernel<<<int(t), 128, 0, e->comp>>>(a);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 2;
+  e->sbr_terms = r;
+  return GWG_OK;
+}
+
 // Trait operands of the split grid: V = [D_j.X_L'_c, D_j.Y'_j] in the padded
 // linear-solve layout, W = Z V by the DMMA rotation kernel against Z^T, 8 int8
 // slices of W per column, and the D panels of gls_sbr_kernel.
@@ -377,6 +440,7 @@ int build_split(gwg_engine* e, gwg_status* st) {
                                                           e->wscale.d());
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
+  if (int rc = build_expsum(e, st)) return rc;
   e->split_valid = true;
   return GWG_OK;
 }
@@ -394,24 +458,48 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   const int64_t ld_s = round_up(rows, 2);
   GWG_CUDA_TRY(e->sbr.ensure(size_t(ld_s) * t * sizeof(double)));
 
-  // ---- S_BR = (X'.X')^T D ----
-  CUtensorMap map_sq;
-  if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->sops.bm, st)) return rc;
-  gwg::SbrArgs q;
-  q.dpanel = e->dpanel.d();
-  q.sbr = e->sbr.d();
-  q.ld = ld_s;
-  q.rows = rows;
-  q.t = int32_t(t);
-  q.tiles_m = int32_t(ceil_div(rows, e->sops.bm));
-  q.tiles_t = int32_t(ceil_div(t, e->sops.bt));
-  q.kchunks = int32_t(e->np / e->sops.bk);
-  q.np = e->np;
-  const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
+  // ---- S_BR = (X'.X')^T D: directly, or as ((X'.X')^T E) F (two DMMA GEMMs
+  // of inner size n and r, expsum.cpp) ----
+  const gwg::SbrOps& so = e->sops;
+  // dst = A^T P: A (kext x rows, ld lda) by TMA, P the D-panel operand with K
+  // extent pk (a multiple of bk) over `cols` columns
+  auto sbr_gemm = [&](const double* a_op, int64_t kext, int64_t lda, const double* panel,
+                      int64_t pk, int64_t cols, double* dst, int64_t ldd, bool rowmajor) -> int {
+    CUtensorMap map;
+    if (int rc = encode_kmajor(&map, a_op, kext, rows, lda, so.bm, st)) return rc;
+    gwg::SbrArgs q;
+    q.dpanel = panel;
+    q.sbr = dst;
+    q.ld = ldd;
+    q.rows = rows;
+    q.t = int32_t(cols);
+    q.tiles_m = int32_t(ceil_div(rows, so.bm));
+    q.tiles_t = int32_t(ceil_div(cols, so.bt));
+    q.kchunks = int32_t(pk / so.bk);
+    q.np = pk;
+    q.rowmajor = rowmajor ? 1 : 0;
+    const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
+    GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
+    e->counters.kernel_launches += 1;
+    return GWG_OK;
+  };
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
-  GWG_CUDA_TRY(e->sops.launch(map_sq, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
+  e->counters.sbr_terms = e->sbr_terms;
+  e->counters.sbr_flops += uint64_t(rows) * 2ull *
+                           (e->sbr_terms ? uint64_t(e->sbr_terms) * uint64_t(e->n + t)
+                                         : uint64_t(e->n) * uint64_t(t));
+  if (const int64_t r = e->sbr_terms) {
+    GWG_CUDA_TRY(e->gmat.ensure(size_t(rows) * r * sizeof(double)));
+    if (int rc = sbr_gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true))
+      return rc;
+    if (int rc = sbr_gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false))
+      return rc;
+  } else {
+    if (int rc =
+            sbr_gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false))
+      return rc;
+  }
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[1], e->comp));
-  e->counters.kernel_launches += 1;
 
   // ---- linear terms (int8 tcgen05) + solve ----
   // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
@@ -590,6 +678,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     e->sops = gwg::sbr_ops(v ? std::atoi(v) : 0);
   }
   if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
+  if (const char* sd = std::getenv("GWG_SBR_DIRECT")) e->lowrank = std::atoi(sd) == 0;
   if (const char* cl = std::getenv("GWG_I8_CLUSTER")) e->i8_cluster = std::atoi(cl) == 2 ? 2 : (std::atoi(cl) == 1 ? 1 : 0);
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
@@ -640,7 +729,8 @@ void gwg_engine_destroy(gwg_engine* e) {
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
-                    &e->wslices, &e->wscale, &e->dpanel, &e->sbr})
+                    &e->wslices, &e->wscale, &e->dpanel, &e->sbr, &e->epanel, &e->fpanel,
+                    &e->gmat, &e->exps})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   for (int b = 0; b < 2; ++b) {

@@ -96,6 +96,13 @@ struct gwg_engine {
   int i8_cluster = 0;  // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs (GWG_I8_CLUSTER)
   bool basis_t_valid = false, split_valid = false;
   gwg_host::DevBuf basis_t, vmat, wmat, wslices, wscale, dpanel, sbr;
+  // S_BR = ((X'.X')^T E) F, the positive exponential-sum factorisation of D
+  // (expsum.cpp): `sbr_terms` = r for the current traits, 0 = direct DMMA
+  // contraction against D (inputs outside the factorisation's range, or
+  // GWG_SBR_DIRECT=1 in the environment: `lowrank` = false).
+  bool lowrank = true;
+  int32_t sbr_terms = 0;
+  gwg_host::DevBuf epanel, fpanel, gmat, exps;
   unsigned long long* err_host = nullptr;
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];

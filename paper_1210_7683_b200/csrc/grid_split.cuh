@@ -67,7 +67,8 @@ struct SbrArgs {
   int32_t tiles_m;
   int32_t tiles_t;
   int32_t kchunks;
-  int64_t np;
+  int64_t np;        // K extent of one D panel (its stride between trait tiles)
+  int32_t rowmajor;  // 1: store out[i * ld + j] instead (j < t, t a multiple of BT)
 };
 
 template <class Cfg>
@@ -188,6 +189,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
 
+    if (args.rowmajor) {
+      // out[i][j]: each lane holds a trait pair -> one 16-byte store
+#pragma unroll
+      for (int w = 0; w < TW; ++w) {
+        const int j = tt * Cfg::BT + (wt * TW + w) * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int o = 0; o < WO; ++o) {
+          const int64_t il = int64_t(tm) * Cfg::BM + (wm * WO + o) * 8 + (lane >> 2);
+          if (il < args.rows)
+            *reinterpret_cast<double2*>(args.sbr + il * args.ld + j) =
+                make_double2(acc[o][w][0], acc[o][w][1]);
+        }
+      }
+      continue;
+    }
     // store S_BR[j][i]: lanes cover 8 SNPs x 4 trait pairs per accumulator block
 #pragma unroll
     for (int w = 0; w < TW; ++w) {

@@ -66,4 +66,119 @@ __global__ void transpose_kernel(const double* __restrict__ src, double* __restr
   }
 }
 
+
+// ---- low-rank S_BR (expsum.cpp): D = E F with positive factors ------------------
+
+// Range of the factorisation, one CTA of 1024 threads:
+//   out[0] = min lambda, out[1] = max lambda,
+//   out[2] / out[3] = min / max of gamma_j = (1 - h_j) / h_j over traits with h_j != 0,
+//   out[4] = number of such traits, out[5] = 1 if some trait's scale
+//   1 / (sigma2 h) (or 1 / sigma2 at h = 0) or gamma is not finite.
+__global__ void __launch_bounds__(1024) expsum_range_kernel(const double* __restrict__ lambda,
+                                                            int64_t n, const double* __restrict__ h2,
+                                                            const double* __restrict__ sigma2,
+                                                            int32_t t, double* __restrict__ out) {
+  __shared__ double red[5][32];
+  double v[5] = {INFINITY, -INFINITY, INFINITY, -INFINITY, 0.0};
+  bool bad = false;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    v[0] = fmin(v[0], lambda[k]);
+    v[1] = fmax(v[1], lambda[k]);
+    bad |= !isfinite(lambda[k]);
+  }
+  for (int j = threadIdx.x; j < t; j += blockDim.x) {
+    const double h = h2[j], s2 = sigma2[j];
+    if (h != 0.0) {
+      const double g = (1.0 - h) / h;
+      v[2] = fmin(v[2], g);
+      v[3] = fmax(v[3], g);
+      v[4] += 1.0;
+      bad |= !isfinite(g) || !isfinite(1.0 / (s2 * h));
+    } else {
+      bad |= !isfinite(1.0 / s2);
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int off = 16; off > 0; off >>= 1) {
+    v[0] = fmin(v[0], __shfl_xor_sync(0xffffffffu, v[0], off));
+    v[1] = fmax(v[1], __shfl_xor_sync(0xffffffffu, v[1], off));
+    v[2] = fmin(v[2], __shfl_xor_sync(0xffffffffu, v[2], off));
+    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], off));
+    v[4] += __shfl_xor_sync(0xffffffffu, v[4], off);
+  }
+  const bool any_bad = __syncthreads_or(bad);
+  if (lane == 0)
+    for (int q = 0; q < 5; ++q) red[q][warp] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+      v[0] = fmin(v[0], red[0][w]);
+      v[1] = fmax(v[1], red[1][w]);
+      v[2] = fmin(v[2], red[2][w]);
+      v[3] = fmax(v[3], red[3][w]);
+      v[4] += red[4][w];
+    }
+    for (int q = 0; q < 5; ++q) out[q] = v[q];
+    out[5] = any_bad ? 1.0 : 0.0;
+  }
+}
+
+struct ExpSumArgs {
+  int64_t n;
+  int64_t np;
+  int32_t t;
+  int32_t r;            // terms (multiple of bt)
+  int32_t bt;           // gls_sbr_kernel panel width
+  const double* lambda;
+  const double* h2;
+  const double* sigma2;
+  const double* s;      // nodes s_r (s_0 = 0)
+  const double* w;      // weights w_r
+  double lam0;          // min lambda
+  double* epanel;       // E[k][r] = exp(-s_r (lambda_k - lam0)) as D panels over r
+  double* fpanel;       // F[r][j] = w_r exp(-s_r (lam0 + gamma_j)) / (sigma2_j h_j)
+};
+
+// D-panel index ([tile][k/8][column octet][column%8][k%8]) of (k, column c).
+__device__ __forceinline__ size_t panel_index(int64_t k, int64_t c, int32_t bt, int64_t kext) {
+  return size_t(c / bt) * size_t(kext) * bt + size_t(k >> 3) * (size_t(bt) * 8) +
+         size_t((c % bt) >> 3) * 64 + size_t(c & 7) * 8 + size_t(k & 7);
+}
+
+// exp(-s x) with the rounding of the product s x compensated: exp is
+// conditioned by s x (up to ~39 on the terms that matter), so an
+// uncompensated product would cost ~39 ulps per term; the errors of x itself
+// are common to all terms of a sum and cost only their own size.
+__device__ __forceinline__ double exp_neg_prod(double s, double x) {
+  const double hi = s * x;
+  const double lo = fma(s, x, -hi);  // s x = hi + lo exactly
+  return exp(-hi) * (1.0 - lo);
+}
+
+// One CTA per term r: column r of E, the K operand of GEMM 1 (K = eigen-rows).
+__global__ void __launch_bounds__(256) expsum_e_kernel(const ExpSumArgs a) {
+  const int r = blockIdx.x;
+  const double s = a.s[r];
+  for (int64_t k = threadIdx.x; k < a.np; k += blockDim.x)
+    a.epanel[panel_index(k, r, a.bt, a.np)] =
+        k < a.n ? exp_neg_prod(s, a.lambda[k] - a.lam0) : 0.0;
+}
+
+// One CTA per trait j: column j of F, the K operand of GEMM 2 (K = terms).
+// h_j = 0 (D constant 1 / sigma2) uses only the constant term (s_0 = 0).
+__global__ void __launch_bounds__(128) expsum_f_kernel(const ExpSumArgs a) {
+  const int j = blockIdx.x;
+  const double h = a.h2[j], s2 = a.sigma2[j];
+  const double coef = h != 0.0 ? 1.0 / (s2 * h) : 1.0 / s2;
+  const double beta = h != 0.0 ? a.lam0 + (1.0 - h) / h : 0.0;
+  for (int r = threadIdx.x; r < a.r; r += blockDim.x) {
+    double f;
+    if (h != 0.0)
+      f = (a.w[r] * coef) * exp_neg_prod(a.s[r], beta);
+    else
+      f = r == 0 ? coef : 0.0;
+    a.fpanel[panel_index(r, j, a.bt, a.r)] = f;
+  }
+}
+
 }  // namespace gwg

@@ -329,7 +329,27 @@ def device_working_set_bytes(n: int, p: int, t: int, mb: int, snp_coding: str = 
         total += 2 * np_ * wrows * 8 + 8 * wrows * kp + wrows * 8  # V, W, W slices + scales
         total += -(-t // 64) * 64 * np_ * 8                   # D panels
         total += mb * (kp + t * 8)                            # int8 slab, S_BR
+        r = 512                                               # low-rank S_BR: E, F, G (max)
+        total += r * np_ * 8 + (-(-t // 64) * 64) * r * 8 + mb * r * 8
     return total
+
+
+def exp_sum_design(x_min: float, x_max: float, multiple: int = 64,
+                   max_terms: int = 512) -> tuple[np.ndarray, np.ndarray]:
+    """Nodes s and weights w of the positive exponential sum
+    1/x ~= sum_r w[r] exp(-s[r] x) on [x_min, x_max] that factorises the GLS
+    weights D for the genotype grid's S_BR term (csrc/expsum.cpp)."""
+    lib = nat.load()
+    r = ctypes.c_int32(0)
+    rc = lib.gwg_exp_sum_design(float(x_min), float(x_max), int(multiple), int(max_terms),
+                                None, None, ctypes.byref(r))
+    if rc != 0:
+        raise DimensionError(f"no exponential sum for [{x_min}, {x_max}] within {max_terms} terms")
+    s = np.empty(r.value)
+    w = np.empty(r.value)
+    lib.gwg_exp_sum_design(float(x_min), float(x_max), int(multiple), int(max_terms),
+                           s.ctypes.data, w.ctypes.data, ctypes.byref(r))
+    return s, w
 
 
 def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,

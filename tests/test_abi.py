@@ -37,7 +37,7 @@ def test_struct_layouts_match_header():
     # gwg_status: int32 code, int64 snp, int64 trait, char[256]
     assert ctypes.sizeof(nat.Status) == 8 + 8 + 8 + 256
     assert nat.Status.snp_index.offset == 8
-    assert ctypes.sizeof(nat.Counters) == 7 * 8 + 5 * 8
+    assert ctypes.sizeof(nat.Counters) == 7 * 8 + 5 * 8 + 2 * 8
     assert ctypes.sizeof(nat.RunOptions) == 16
 
 

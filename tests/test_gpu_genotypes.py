@@ -151,3 +151,65 @@ def test_device_snp_operand_alignment_and_odd_n(n, offset):
         eng.solve_snp_slab(x.t(), out=out)
         torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("case", ["config", "edge_h", "wide_spectrum"])
+def test_low_rank_sbr_matches_direct_contraction(case, monkeypatch):
+    """S_BR = ((X'.X')^T E) F (positive exponential sum, csrc/expsum.cpp)
+    against the direct DMMA contraction (X'.X')^T D (GWG_SBR_DIRECT=1) and
+    the oracle, including h2 = 0 (D constant), h2 = 1 and a spectrum spanning
+    nine decades."""
+    n, p, m, t = 400, 4, 500, 40
+    ds = datagen.generate(n, p, m, t, seed=41)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    h2 = ds["h2"].copy()
+    if case == "edge_h":
+        h2[:6] = [0.0, 1.0, 1e-9, 1 - 1e-9, 0.5, 0.0]
+    if case == "wide_spectrum":
+        values = np.geomspace(1e-7, 1e2, n)
+    ds = dict(ds, h2=h2)
+    b_low = run(ds, basis, values, "genotypes")
+    monkeypatch.setenv("GWG_SBR_DIRECT", "1")
+    b_dir = run(ds, basis, values, "genotypes")
+    assert not np.isnan(b_low).any()
+    rel = np.linalg.norm(b_low - b_dir, axis=2) / np.linalg.norm(b_dir, axis=2)
+    assert rel.max() < 1e-11, rel.max()
+    ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"]),
+                           orc.rotate(basis, ds["traits"]), h2, ds["sigma2"], workers=8)
+    assert_parity(b_low, ref)
+
+
+def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
+    """The engine takes the factorised S_BR on BASELINE-like inputs (two
+    gls_sbr launches per slab instead of one) and the direct contraction
+    when D is outside the factorisation's range: h2 = 3, sigma2 = -1 and a
+    spectrum in [0.1, 0.6] give weights sigma2 (h2 lambda + 1 - h2) > 0 that
+    the reference accepts, but h2 lambda + 1 - h2 < 0 everywhere."""
+    ds = datagen.generate(200, 3, 100, 8, seed=5)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    n, p, t = 200, 3, 8
+
+    def launches(values, h2, sigma2):
+        with gw.Engine(n, p) as eng:
+            eng.set_spectrum(basis, values)
+            eng.set_covariates(ds["xl"])
+            eng.set_snp_coding("genotypes")
+            eng.set_traits(ds["traits"], h2, sigma2)
+            eng.run_grid(ds["snps"])  # builds the trait operands
+            eng.reset_counters()
+            b = eng.run_grid(ds["snps"])
+            return eng.counters()["kernel_launches"], b
+
+    odd = (np.linspace(0.1, 0.6, n), np.full(t, 3.0), np.full(t, -1.0))
+    k_low, b_low = launches(values, ds["h2"], ds["sigma2"])
+    k_odd, b_odd = launches(*odd)
+    monkeypatch.setenv("GWG_SBR_DIRECT", "1")
+    k_dir, b_dir = launches(values, ds["h2"], ds["sigma2"])
+    k_odd_dir, b_odd_dir = launches(*odd)
+    assert k_low == k_dir + 1 and k_odd == k_odd_dir == k_dir
+    rel = np.linalg.norm(b_low - b_dir, axis=2) / np.linalg.norm(b_dir, axis=2)
+    assert rel.max() < 1e-11, rel.max()
+    assert np.array_equal(b_odd, b_odd_dir)
+    ref = orc.compute_grid(odd[0], orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"]),
+                           orc.rotate(basis, ds["traits"]), odd[1], odd[2], workers=8)
+    assert_parity(b_odd, ref)
