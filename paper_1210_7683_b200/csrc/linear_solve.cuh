@@ -36,8 +36,15 @@ namespace gwg {
 template <int P, int CL = 1>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
-  static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
-  static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
+  // CL = 4 (p <= 16): CTA pairs running one cta_group::2 MMA (M = 256) on
+  // half-width tiles (16 W rows, N = 128) with FOUR accumulator buffers in
+  // TMEM, one epilogue warp per buffer and lane quarter: the MMA runs up to
+  // three tiles ahead of the epilogue instead of one, and each CTA keeps half
+  // of B per stage (same L2 operand traffic as the 32-row multicast tiles).
+  static constexpr bool Q4 = CL == 4;
+  static_assert(!Q4 || P8 <= 16, "four accumulator buffers need N <= 128");
+  static constexpr int KT = Q4 ? 16 / P8 : (32 / P8 >= 1 ? 32 / P8 : 1);  // traits per tile
+  static constexpr int RB = KT * P8;                      // W rows per tile (16, 24 or 32)
   // WIDE (p <= 16): 16 epilogue warps (4 per TMEM lane quarter: 2 per
   // accumulator buffer, each doing half of a tile's cells; 96 registers) with
   // 3 operand stages — the epilogue is latency-bound, so more warps beat
@@ -45,15 +52,26 @@ struct LinCfg {
   // 8 epilogue warps (2 per quarter, all cells of alternate tiles) and 4
   // stages.  One 4 KB staging tile per epilogue warp.
   static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: p=4 3.15 -> 2.83 ms, p=12 8.56 -> 7.95
-  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, WIDE ? 16 : 8, CL>;
-  static constexpr int HALVES = WIDE && KT >= 2 ? 2 : 1;  // warps splitting one tile
+  static constexpr int EPI = WIDE || Q4 ? 16 : 8;
+  // CL = 3 / 4: each CTA holds half of B per stage, so as many stages as
+  // shared memory takes (<= 8)
+  static constexpr int PAIR_STAGES_ =
+      int((227 * 1024 - EPI * 4096 - 1280) / (128 * 128 + RB * 8 * 128 / 2));
+  static constexpr int PAIR_STAGES = PAIR_STAGES_ < 8 ? PAIR_STAGES_ : 8;
+  using Tile = std::conditional_t<
+      Q4, I8Tile<RB, PAIR_STAGES, 1, EPI, 2, true, 4>,
+      std::conditional_t<CL == 3, I8Tile<RB, PAIR_STAGES, 1, EPI, 2, true>,
+                         I8Tile<RB, WIDE ? 3 : 4, 1, EPI, CL>>>;
+  static constexpr int ACC = Tile::ACC_BUFS;
+  static constexpr int HMAX = EPI / 4 / ACC;              // warps per quarter and buffer
+  static constexpr int HALVES = KT >= HMAX ? HMAX : 1;    // warps splitting one tile
   static constexpr int CELLS = KT / HALVES;               // cells per warp per tile
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
   static constexpr int ROW = CELLS * P;                   // results per warp row per tile
   static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
   static constexpr bool TMA_OUT = ROW % CHUNK == 0;       // whole 128-byte chunks
   // cells solved together (independent chains; KT is a power of two or 1)
-  static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
+  static constexpr int GMAX = WIDE || Q4 ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
   static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
   // large p: triangular solves as products with L^-1 (independent dot
@@ -97,8 +115,8 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const I8Sched<C> sch(a.tiles_m, a.tiles_r);
   const int my_tiles = sch.my_tiles;
-  // one (or, WIDE, two) warp(s) per quarter release each tile's buffer
-  const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * (C::EPI_WARPS / 8));
+  // HMAX warps per quarter release each tile's buffer
+  const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * L::HMAX);
 
   if (warp == 0) {
     if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, sch, a.kstages,
@@ -114,24 +132,25 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     // third warp per quarter could run two phases ahead and alias the parity.)
     const int ew = warp - 4;
     const int qd = warp & 3;
-    const int h = (ew >> 2) & 1;           // accumulator buffer (tile parity) of this warp
-    const int hf = ew >> 3;                // WIDE: which half of the tile's cells
+    const int h = (ew >> 2) % L::ACC;      // accumulator buffer (tile index mod ACC) of this warp
+    const int hf = (ew >> 2) / L::ACC;     // which share of the tile's cells (HMAX > 1)
     const int cell0 = hf * L::CELLS;
     const bool active = cell0 < L::KT;
     unsigned char* stg = sm.staging + ew * C::OUT_BYTES;
     const uint64_t pol_out = policy_evict_first();
     int nchunk = 0;  // result chunks this warp has stored (staging tile = nchunk & 1)
-    for (int lt = h; lt < my_tiles; lt += 2) {
-      const int buf = lt & 1;
+    for (int lt = h; lt < my_tiles; lt += L::ACC) {
+      const int buf = lt % L::ACC;
+      const uint32_t par = uint32_t(lt / L::ACC) & 1;
       int tm, tr;
       sch.coords(lt, tm, tr);
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
       const bool iv = il < a.rows;
       const int j0 = tr * L::KT;  // first trait of the tile
       if (!active) {  // KT = 1 under WIDE: nothing to do but keep the buffer protocol
-        mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
+        mbar_wait(&sm.acc_full[buf], par);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);
+        if (lane == 0) i8_acc_release<C>(sm, buf);
         continue;
       }
       double sbr[L::CELLS];
@@ -143,7 +162,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
       // to the recombination below: no per-column memory round trip
       const double sc_lane = lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
-      mbar_wait(&sm.acc_full[buf], (lt >> 1) & 1);
+      mbar_wait(&sm.acc_full[buf], par);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
       const bool tma = L::TMA_OUT && a.use_tma;
@@ -181,7 +200,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       auto release = [&]() {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for tile lt + 2
+        if (lane == 0) i8_acc_release<C>(sm, buf);  // TMEM buffer free for tile lt + ACC
       };
 #pragma unroll
       for (int g0 = 0; g0 < L::CELLS; g0 += L::GROUP) {
@@ -265,17 +284,21 @@ cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int sms,
                                 cudaStream_t s) {
   using C = typename LinCfg<P, CL>::Tile;
-  const int64_t units = int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
+  const int64_t units = int64_t((a.tiles_m + C::CLUSTER - 1) / C::CLUSTER) * a.tiles_r;
   return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a);
 }
 
 // Per-p entry of the split grid (kernels_lin_*.cu).
 struct LinOps {
   int kt = 0, p8 = 0, rb = 0;
-  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile
-  cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
-  int b_slices_box[2] = {8, 4};
+  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile;
+  // [2]: CTA pairs running one cta_group::2 MMA (each CTA loads its half of B);
+  // [3]: the same on 16-row tiles with four accumulator buffers (p <= 16)
+  cudaError_t (*launch[4])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr, nullptr,
+                                                                 nullptr};
+  int b_slices_box[4] = {8, 4, 4, 4};
+  int kt_q4 = 0, rb_q4 = 0;  // tile geometry of launch[3] (W row layout j * p8 + c is shared)
 };
 
 template <int P>
@@ -286,6 +309,12 @@ LinOps make_lin_ops() {
   o.rb = LinCfg<P>::RB;
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
+  o.launch[2] = &launch_linear_solve<P, 3>;
+  if constexpr (LinCfg<P>::P8 <= 16) {
+    o.launch[3] = &launch_linear_solve<P, 4>;
+    o.kt_q4 = LinCfg<P, 4>::KT;
+    o.rb_q4 = LinCfg<P, 4>::RB;
+  }
   return o;
 }
 

@@ -41,8 +41,10 @@ struct I8Args {
 
 // ---- the rotation kernel -------------------------------------------------------
 
+// CL: 1 single CTAs, 2 CTA pairs multicasting B, 3 CTA pairs running one
+// cta_group::2 MMA (half the B shared memory per stage: 6 stages)
 template <int CL>
-using RotI8Cfg = I8Tile<32, 4, 1, 8, CL>;
+using RotI8Cfg = std::conditional_t<CL == 3, I8Tile<32, 6, 1, 8, 2, true>, I8Tile<32, 4, 1, 8, CL>>;
 
 template <int CL>
 __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmap_d,
                      const __grid_constant__ CUtensorMap tmap_d2, const I8Args a) {
   using C = RotI8Cfg<CL>;
+  static_assert(C::ACC_BUFS == 2, "epilogue alternates two accumulator buffers");
   extern __shared__ __align__(1024) unsigned char smem_i8[];
   const I8Smem<C> sm(smem_i8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.acc_empty[buf]);  // TMEM buffer free for the next tile
+      if (lane == 0) i8_acc_release<C>(sm, buf);  // TMEM buffer free for the next tile
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
         if (!(o == 0 ? a.has_d : a.has_d2)) continue;
