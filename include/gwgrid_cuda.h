@@ -206,8 +206,11 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
  * rotation X'.X' and the p linear terms of every cell (x^T W, W = Z D [X_L' Y'])
  * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, eight 7-bit
  * slices, exact int64 recombination, one rounding) and only S_BR = (X'.X')^T D
- * stays on DMMA — the same cells to rounding (~1e-14 norm-wise), ~3.5x faster
- * at BASELINE config 1; results stay bitwise independent of slab geometry.
+ * stays on DMMA, factorised as ((X'.X')^T E) F through a positive exponential
+ * sum of D (gwg_exp_sum_design; GWG_SBR_DIRECT=1 in the environment forces the
+ * direct contraction) — the same cells to rounding (~1e-14 norm-wise), ~6x
+ * faster than the all-FP64 path at BASELINE config 1; results stay bitwise
+ * independent of slab geometry.
  * Pre-rotated slabs (is_rotated = 1) always take the FP64 path. */
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
 

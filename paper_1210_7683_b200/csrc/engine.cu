@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -322,6 +323,25 @@ void invalidate_derived(gwg_engine* e, bool spectrum) {
   }
 }
 
+// min / max of the eigenvalues, once per spectrum (expsum_range_kernel with
+// no traits, one round trip): the exponential sum's range needs them.
+int spectrum_range(gwg_engine* e, gwg_status* st) {
+  GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
+  double* dx = e->exps.d();
+  gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, nullptr, nullptr, 0,
+                                                    dx);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  double rg[6];
+  GWG_CUDA_TRY(cudaMemcpyAsync(rg, dx, sizeof(rg), cudaMemcpyDeviceToHost, e->comp));
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  e->lam_lo = rg[0];
+  e->lam_hi = rg[1];
+  e->lam_bad = rg[5] != 0.0;
+  e->ex_hi = -1.0;  // nodes must be redesigned
+  return GWG_OK;
+}
+
 // E and F of the low-rank S_BR (expsum.cpp) for the current traits, or
 // sbr_terms = 0 when D is outside the factorisation's range: some
 // h lambda + 1 - h <= 0 (the trait check reports those), non-finite scales,
@@ -333,13 +353,33 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   const int64_t n = e->n, np = e->np, t = e->t;
   GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * kMaxTerms) * sizeof(double)));
   double* dx = e->exps.d();
-  gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(), e->sigma2.d(),
-                                                    int32_t(t), dx);
-  GWG_CUDA_TRY(cudaGetLastError());
-  e->counters.kernel_launches += 1;
   double rg[6];
-  GWG_CUDA_TRY(cudaMemcpyAsync(rg, dx, sizeof(rg), cudaMemcpyDeviceToHost, e->comp));
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  if (e->traits_host_valid) {
+    // the same reduction as expsum_range_kernel: the spectrum's range was
+    // found with the spectrum, the traits' from the host copies
+    rg[0] = e->lam_lo, rg[1] = e->lam_hi, rg[2] = INFINITY, rg[3] = -INFINITY, rg[4] = 0.0;
+    bool bad = e->lam_bad;
+    for (int64_t j = 0; j < t; ++j) {
+      const double h = e->h2_host[j], s2 = e->s2_host[j];
+      if (h != 0.0) {
+        const double g = (1.0 - h) / h;
+        rg[2] = std::fmin(rg[2], g);
+        rg[3] = std::fmax(rg[3], g);
+        rg[4] += 1.0;
+        bad |= !std::isfinite(g) || !std::isfinite(1.0 / (s2 * h));
+      } else {
+        bad |= !std::isfinite(1.0 / s2);
+      }
+    }
+    rg[5] = bad ? 1.0 : 0.0;
+  } else {  // device-resident inputs: one small reduction and a round trip
+    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(),
+                                                      e->sigma2.d(), int32_t(t), dx);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    GWG_CUDA_TRY(cudaMemcpyAsync(rg, dx, sizeof(rg), cudaMemcpyDeviceToHost, e->comp));
+    GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  }
   if (rg[5] != 0.0) return GWG_OK;
   double x_min = 1.0, x_max = 1.0;  // all h = 0: only the constant term is used
   if (rg[4] > 0.0) {
@@ -349,12 +389,18 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   // r: a whole number of S_BR column tiles (GEMM 1) and k-chunks (GEMM 2)
   const int32_t mult = std::lcm(e->sops.bt, e->sops.bk);
   int32_t r = 0;
-  if (gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nullptr, nullptr, &r) != GWG_OK)
-    return GWG_OK;
-  std::vector<double> nodes(2 * size_t(r));
-  gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nodes.data(), nodes.data() + r, &r);
-  GWG_CUDA_TRY(cudaMemcpyAsync(dx + 8, nodes.data(), nodes.size() * sizeof(double),
-                               cudaMemcpyHostToDevice, e->comp));
+  if (x_min == e->ex_lo && x_max == e->ex_hi && mult == e->ex_mult) {
+    r = e->ex_r;  // same range as the nodes already on the device
+  } else {
+    if (gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nullptr, nullptr, &r) != GWG_OK)
+      return GWG_OK;
+    std::vector<double> nodes(2 * size_t(r));
+    gwg_exp_sum_design(x_min, x_max, mult, kMaxTerms, nodes.data(), nodes.data() + r, &r);
+    GWG_CUDA_TRY(cudaMemcpyAsync(dx + 8, nodes.data(), nodes.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, e->comp));
+    GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));  // `nodes` is pageable and local
+    e->ex_lo = x_min, e->ex_hi = x_max, e->ex_mult = mult, e->ex_r = r;
+  }
   const int64_t bt = e->sops.bt;
   const int64_t t_pad = round_up(t, bt);
   GWG_CUDA_TRY(e->epanel.ensure(size_t(r) * np * sizeof(double)));
@@ -774,7 +820,7 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
   if (!basis || !lambda) return set_status(st, GWG_DIMENSION, -1, -1, "null spectrum operand");
   if (int rc = upload_cols(e, e->basis, basis, e->n, e->n, where, e->comp, st)) return rc;
   if (int rc = upload(e, e->lambda, lambda, size_t(e->n), where, st)) return rc;
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  if (int rc = spectrum_range(e, st)) return rc;
   e->have_spectrum = true;
   e->have_covariates = false;
   e->have_traits = false;
@@ -795,6 +841,7 @@ int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_sta
   GWG_CUDA_TRY(e->lambda.ensure(size_t(e->n) * sizeof(double)));
   if (int rc = gwg_internal_device_eig(e->basis.d(), e->n, e->np, e->lambda.d(), e->comp, st))
     return rc;
+  if (int rc = spectrum_range(e, st)) return rc;
   invalidate_derived(e, true);
   e->have_spectrum = true;
   return GWG_OK;
@@ -842,6 +889,11 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   }
   if (int rc = upload(e, e->h2, h2, size_t(t), where, st)) return rc;
   if (int rc = upload(e, e->sigma2, sigma2, size_t(t), where, st)) return rc;
+  e->traits_host_valid = where == GWG_HOST;
+  if (e->traits_host_valid) {
+    e->h2_host.assign(h2, h2 + t);
+    e->s2_host.assign(sigma2, sigma2 + t);
+  }
   const int64_t tiles_t = ceil_div(t, e->ops.bt);
   const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
   GWG_CUDA_TRY(e->bops.ensure(bops_doubles * sizeof(double)));

@@ -105,6 +105,16 @@ struct gwg_engine {
   bool lowrank = true;
   int32_t sbr_terms = 0;
   gwg_host::DevBuf epanel, fpanel, gmat, exps;
+  // host copies of lambda / h2 / sigma2 when they were passed from the host:
+  // the factorisation's range is then found without a device round trip
+  std::vector<double> h2_host, s2_host;
+  bool traits_host_valid = false;
+  // min / max of the spectrum (found once per spectrum); lam_bad = non-finite
+  double lam_lo = 0.0, lam_hi = 0.0;
+  bool lam_bad = false;
+  // the nodes on the device (exps + 8) were designed for this range
+  double ex_lo = 0.0, ex_hi = -1.0;
+  int32_t ex_mult = 0, ex_r = 0;
   unsigned long long* err_host = nullptr;
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];

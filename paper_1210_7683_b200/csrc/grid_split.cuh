@@ -6,9 +6,12 @@
 //     S_BL[i,j,c] = X'_i^T (D_j.X_L'_c) = x_i^T W_{j,c},  W_{j,c} = Z (D_j.X_L'_c)
 //     b_B[i,j]    = X'_i^T (D_j.Y'_j)   = x_i^T W_{j,p-1}, W_{j,p-1} = Z (D_j.Y'_j)
 //     S_BR[i,j]   = (X'_i.X'_i)^T D_j                       (quadratic in x_i)
-// Two launches per slab:
-//   gls_sbr_kernel (this file): S_BR = (X'.X')^T D on the FP64 tensor pipe
-//       (DMMA.8x8x4) — 2n of the cell's 2n(p+1) flops — stored [trait][SNP].
+// Launches per slab:
+//   gls_sbr_kernel (this file), a DMMA.8x8x4 GEMM: S_BR = (X'.X')^T D
+//       directly (2n flop per cell), or — the default — twice, through the
+//       positive exponential-sum factorisation D = E F (expsum.cpp):
+//       G = (X'.X')^T E stored [SNP][r] (rowmajor), then S_BR = G F, 2r(n+t)
+//       flop per SNP; S_BR is stored [trait][SNP].
 //   linear_solve_kernel<P> (linear_solve.cuh): x_i^T W exactly on the int8
 //       tensor cores against eight 7-bit slices of W (tcgen05.mma kind::i8,
 //       TMEM accumulators, exact int64 recombination), and in the same

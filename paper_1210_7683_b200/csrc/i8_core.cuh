@@ -8,8 +8,13 @@
 #include "gwg_device.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <type_traits>
 #include <utility>
+
+#ifndef I8_PROFILE
+#define I8_PROFILE 0
+#endif
 
 namespace gwg {
 
@@ -456,6 +461,9 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
   const uint64_t pol_x = policy_evict_normal();
   const uint64_t pol_b = b_resident ? policy_evict_last() : policy_evict_normal();
   int g = 0;
+#if I8_PROFILE
+  long long t_empty = 0, t0 = clock64();
+#endif
   for (int lt = 0; lt < sch.my_tiles; ++lt) {
     int tm, tr;
     sch.coords(lt, tm, tr);
@@ -463,7 +471,13 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
       const int s = g % C::STAGES;
       // CLUSTER = 2: empty[s] completes only when BOTH CTAs' MMAs are done with
       // stage s, since this CTA's multicast also writes the peer's stage
+#if I8_PROFILE
+      long long te = clock64();
+#endif
       if (g >= C::STAGES) mbar_wait(&sm.empty[s], ((g / C::STAGES) - 1) & 1);
+#if I8_PROFILE
+      t_empty += clock64() - te;
+#endif
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
       if constexpr (C::MMA2) {
         // both CTAs' loads complete on the leader's full[s]; the leader
@@ -486,6 +500,11 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
         tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
     }
   }
+#if I8_PROFILE
+  if (blockIdx.x < 4)
+    printf("I8PROF producer cta %d total %lld wait_empty %lld\n", int(blockIdx.x), clock64() - t0,
+           t_empty);
+#endif
 }
 
 // Warp 1, one thread: BK/UK tcgen05.mma per stage into the tile's TMEM buffer.
@@ -527,14 +546,29 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
   constexpr uint16_t mask = uint16_t((1u << C::CLUSTER) - 1);
   constexpr uint32_t idesc = i8_instr_desc<C::BN, C::BM>();
   int g = 0;
+#if I8_PROFILE
+  long long t_acc = 0, t_full = 0, t0 = clock64();
+#endif
   for (int lt = 0; lt < my_tiles; ++lt) {
     const int buf = lt % C::ACC_BUFS;
+#if I8_PROFILE
+    long long ta = clock64();
+#endif
     if (lt >= C::ACC_BUFS) mbar_wait(&sm.acc_empty[buf], ((lt / C::ACC_BUFS) - 1) & 1);
+#if I8_PROFILE
+    t_acc += clock64() - ta;
+#endif
     tc_fence_after();
     const uint32_t tmem_d = tmem_base + uint32_t(buf * C::BN);
     for (int ks = 0; ks < kstages; ++ks, ++g) {
       const int s = g % C::STAGES;
+#if I8_PROFILE
+      long long tf = clock64();
+#endif
       mbar_wait(&sm.full[s], (g / C::STAGES) & 1);
+#if I8_PROFILE
+      t_full += clock64() - tf;
+#endif
       tc_fence_after();
       const uint32_t sa = smem_u32(sm.base + s * C::STAGE_BYTES);
       const uint32_t sb = sa + C::A_BYTES;
@@ -550,6 +584,11 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
     }
     umma_commit(&sm.acc_full[buf]);  // accumulator ready for the epilogue
   }
+#if I8_PROFILE
+  if (blockIdx.x < 4)
+    printf("I8PROF mma cta %d tiles %d total %lld wait_acc_empty %lld wait_full %lld\n",
+           int(blockIdx.x), my_tiles, clock64() - t0, t_acc, t_full);
+#endif
 }
 
 // Host: launch an I8Tile kernel over `units` scheduling units (CTA pairs for

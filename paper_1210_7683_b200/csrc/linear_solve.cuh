@@ -29,6 +29,14 @@
 
 namespace gwg {
 
+// Timing ablations only (never in a shipped build): 1 = no result stores,
+// 2 = no S_BR loads, 3 = no solve, 4 = neither solve nor stores, 5 = 4 and
+// no S_BR loads and a plain sum for the recombination, 6 = 5 without the
+// TMEM loads.
+#ifndef LIN_EXPERIMENT
+#define LIN_EXPERIMENT 0
+#endif
+
 #ifndef LIN_WIDE_MAXP
 #define LIN_WIDE_MAXP 16
 #endif
@@ -157,7 +165,10 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
       for (int cc = 0; cc < L::CELLS; ++cc) {
         const int j = j0 + cell0 + cc;
-        sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
+        if (LIN_EXPERIMENT == 2 || LIN_EXPERIMENT >= 5)
+          sbr[cc] = 1e6 + lane;
+        else
+          sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
       }
       // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
       // to the recombination below: no per-column memory round trip
@@ -178,10 +189,16 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
             for (int u = 0; u < L::PAIR; ++u)
 #pragma unroll
-              for (int sl = 0; sl < C::SLICES; ++sl)
-                tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (cb + u0 + u) * L::P8 + c0),
-                                v[u][sl]);
-            tmem_ld_wait();
+              for (int sl = 0; sl < C::SLICES; ++sl) {
+                if (LIN_EXPERIMENT == 6) {
+#pragma unroll
+                  for (int r = 0; r < L::CW; ++r) v[u][sl][r] = lane + sl + r + u;
+                } else {
+                  tmem_ldw<L::CW>(taddr + uint32_t(sl * C::RB + (cb + u0 + u) * L::P8 + c0),
+                                  v[u][sl]);
+                }
+              }
+            if (LIN_EXPERIMENT != 6) tmem_ld_wait();
 #pragma unroll
             for (int u = 0; u < L::PAIR; ++u)
 #pragma unroll
@@ -189,9 +206,14 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
                 if (c0 + r < P) {
                   const double sc =
                       __shfl_sync(0xffffffffu, sc_lane, (cb + u0 + u) * L::P8 + c0 + r);
-                  dst[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
-                                                     v[u][3][r], v[u][4][r], v[u][5][r],
-                                                     v[u][6][r], v[u][7][r], sc);
+                  if (LIN_EXPERIMENT == 5)
+                    dst[u0 + u][c0 + r] = double(v[u][0][r] + v[u][1][r] + v[u][2][r] +
+                                                 v[u][3][r] + v[u][4][r] + v[u][5][r] +
+                                                 v[u][6][r] + v[u][7][r]) * sc;
+                  else
+                    dst[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
+                                                       v[u][3][r], v[u][4][r], v[u][5][r],
+                                                       v[u][6][r], v[u][7][r], sc);
                 }
               }
           }
@@ -218,8 +240,14 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
           cell[P] = sbr[g0 + u];
           const double* cx = a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
-          ok[u] = (L::INV_SOLVE ? solve_cell_inv<P>(cell, cx, beta[u])
-                                : solve_cell<P>(cell, cx, beta[u])) || !cv;
+          if (LIN_EXPERIMENT >= 3) {
+#pragma unroll
+            for (int c = 0; c < P; ++c) beta[u][c] = cell[c] + cell[P];
+            ok[u] = true;
+          } else {
+            ok[u] = (L::INV_SOLVE ? solve_cell_inv<P>(cell, cx, beta[u])
+                                  : solve_cell<P>(cell, cx, beta[u])) || !cv;
+          }
         }
 #pragma unroll
         for (int u = 0; u < L::GROUP; ++u) {
@@ -230,7 +258,15 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             for (int c = 0; c < P; ++c) beta[u][c] = __longlong_as_double(0x7ff8000000000000LL);
           }
         }
-        if (tma) {
+        if (LIN_EXPERIMENT == 1 || LIN_EXPERIMENT >= 4) {
+          // keep the results live without storing them
+          double acc = 0.0;
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) acc += beta[u][c];
+          if (acc == 1.2345e300) a.out[il] = acc;
+        } else if (tma) {
           // flat index f = (g0+u)*P + c of this row; 128-byte chunks of 16
           // doubles, 16-byte units XOR-swizzled by row (SWIZZLE_128B), one
           // TMA store per chunk

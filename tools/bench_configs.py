@@ -67,12 +67,13 @@ def run(name, steps):
         c = eng.counters()
     kern = c["grid_kernel_ms"] / steps
     grid_flops = m * t * 2 * n * (p + 1)
-    return {"config": name, "n": n, "p": p, "t": t, "m_slab": m, "ms_per_step": ms,
+    return {"build": os.environ.get("GWG_BUILD_TAG", ""), "config": name, "n": n, "p": p, "t": t, "m_slab": m, "ms_per_step": ms,
             "gls_per_s": m * t / (ms * 1e-3), "step_tflops_grid_convention": grid_flops / ms / 1e9,
             "grid_kernel_ms": kern, "grid_kernel_tflops": grid_flops / kern / 1e9,
             "grid_kernel_frac_of_peak": grid_flops / kern / 1e9 / PEAK,
             "rotate_ms": c["rotate_ms"] / steps, "sbr_ms": c["quad_ms"] / steps,
-            "linear_solve_ms": c["linear_ms"] / steps, "kinship_build_s": t1 - t0,
+            "linear_solve_ms": c["linear_ms"] / steps, "sbr_terms": c["sbr_terms"],
+            "kinship_build_s": t1 - t0,
             "device_eig_s": t2 - t1, "nan": int(torch.isnan(b).sum().item())}
 
 
