@@ -202,9 +202,9 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
  * BASELINE.json).  GWG_SNP_REAL (default): any real values; the rotation and
  * the grid run on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP
  * value is an integer code in [-127, 127] (e.g. genotypes 0/1/2), checked on
- * the device (violations fail with GWG_DIMENSION); n < 262,000.  Then the
+ * the device (violations fail with GWG_DIMENSION); n < 132,000.  Then the
  * rotation X'.X' and the p linear terms of every cell (x^T W, W = Z D [X_L' Y'])
- * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, eight 7-bit
+ * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, seven 8-bit
  * slices, exact int64 recombination, one rounding) and only S_BR = (X'.X')^T D
  * stays on DMMA, factorised as ((X'.X')^T E) F through a positive exponential
  * sum of D (gwg_exp_sum_design; GWG_SBR_DIRECT=1 in the environment forces the

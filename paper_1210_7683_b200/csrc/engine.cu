@@ -256,17 +256,13 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   // CTA pairs multicasting the B (Z-slice) tile when it streams from HBM
   // (measured at n = 10,000: 69.2 -> 49.0 ms; neutral at n = 1000)
-  int cl = e->i8_cluster ? e->i8_cluster : (e->n >= 4096 ? 2 : 1);
-  if (cl == 4) cl = 3;  // the rotation has one geometry for CTA-pair MMAs
+  const int cl = e->i8_cluster ? e->i8_cluster : (e->n >= 4096 ? 2 : 1);
   CUtensorMap tx, tb;
   if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB,
-                         I8Cfg::SLICES / (cl > 1 ? 2 : 1), st))
+                         I8Cfg::SLOTS / cl, st))
     return rc;
-  const int64_t units = int64_t((a.tiles_m + (cl > 1 ? 1 : 0)) / (cl > 1 ? 2 : 1)) * a.tiles_r;
-  if (cl == 3)
-    GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<3>>(gwg::rotate_i8_kernel<3>, units, e->sms,
-                                                  e->comp, tx, tb, td[0], td[1], a));
-  else if (cl == 2)
+  const int64_t units = int64_t((a.tiles_m + cl - 1) / cl) * a.tiles_r;
+  if (cl == 2)
     GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<2>>(gwg::rotate_i8_kernel<2>, units, e->sms,
                                                   e->comp, tx, tb, td[0], td[1], a));
   else
@@ -503,21 +499,8 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   using gwg::I8Cfg;
   const int64_t t = e->t, p = e->p;
   const int64_t kp = round_up(e->n, I8Cfg::BK);
-  // linear-solve variant (GWG_I8_CLUSTER): 2 (default) = CTA pairs
-  // multicasting the 32-row W tile; 1 = single CTAs; 3 = CTA pairs running
-  // one cta_group::2 MMA on 32-row tiles; 4 = the same on 16-row tiles with
-  // four accumulator buffers (p <= 16).  All give identical bits; measured at
-  // c1: 2.68 ms (2), 2.73 (3), 3.31 (4) — the kernel is bound by its
-  // epilogue, not by how far the MMA can run ahead, and 16-row tiles cost
-  // 1.5x the L2 operand traffic.  The W rows are j * p8 + c for every variant.
-  int cl = e->i8_cluster ? e->i8_cluster : 2;
-  if (cl == 4 && !e->lops.launch[3]) cl = 2;
-  const int64_t kt = cl == 4 ? e->lops.kt_q4 : e->lops.kt;
-  const int64_t rb = cl == 4 ? e->lops.rb_q4 : e->lops.rb;
-  const int64_t tiles_r = ceil_div(t, kt);
-  // W-slice planes are laid out for the base tiles (build_split): their
-  // row count is the tensor map's, whatever tile height this variant reads
-  const int64_t ncols = ceil_div(t, e->lops.kt) * e->lops.rb;
+  const int64_t tiles_r = ceil_div(t, e->lops.kt);
+  const int64_t ncols = tiles_r * e->lops.rb;
   const int64_t ld_s = round_up(rows, 2);
   GWG_CUDA_TRY(e->sbr.ensure(size_t(ld_s) * t * sizeof(double)));
 
@@ -566,9 +549,10 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
 
   // ---- linear terms (int8 tcgen05) + solve ----
   // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
-  // c2 22.5 -> 20.9, c4 43.1 -> 40.4)
+  // c2 22.5 -> 20.9, c4 43.1 -> 40.4; GWG_I8_CLUSTER=1 forces single CTAs)
+  const int cl = e->i8_cluster ? e->i8_cluster : 2;
   CUtensorMap tx, tw, tout;
-  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, rb,
+  if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb,
                          e->lops.b_slices_box[cl - 1], st))
     return rc;
   // numpy layout with a 16-byte pitch and base: results leave by TMA store
@@ -743,7 +727,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   if (const char* sd = std::getenv("GWG_SBR_DIRECT")) e->lowrank = std::atoi(sd) == 0;
   if (const char* cl = std::getenv("GWG_I8_CLUSTER")) {
     const int v = std::atoi(cl);
-    e->i8_cluster = v >= 1 && v <= 4 ? v : 0;
+    e->i8_cluster = v == 1 || v == 2 ? v : 0;
   }
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
@@ -1150,9 +1134,9 @@ int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
   if (int rc = check_engine(e, st)) return rc;
   if (coding != GWG_SNP_REAL && coding != GWG_SNP_GENOTYPES)
     return set_status(st, GWG_DIMENSION, -1, -1, "unknown SNP coding %d", coding);
-  if (coding == GWG_SNP_GENOTYPES && e->n >= 262000)
+  if (coding == GWG_SNP_GENOTYPES && e->n >= 132000)
     return set_status(st, GWG_DIMENSION, -1, -1,
-                      "genotype coding needs n < 262,000 (exact int32 accumulation)");
+                      "genotype coding needs n < 132,000 (exact int32 accumulation)");
   e->snp_coding = coding;
   return GWG_OK;
 }

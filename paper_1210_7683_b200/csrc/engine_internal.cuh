@@ -93,8 +93,8 @@ struct gwg_engine {
   // (GWG_SPLIT=0 in the environment turns it off for A/B timing);
   // `slab_i8` = the current slab was rotated from integer codes (xi8 valid).
   bool split = true, slab_i8 = false;
-  // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs multicasting B, 3 CTA
-  // pairs with one cta_group::2 MMA (GWG_I8_CLUSTER)
+  // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs multicasting B
+  // (GWG_I8_CLUSTER)
   int i8_cluster = 0;
   bool basis_t_valid = false, split_valid = false;
   gwg_host::DevBuf basis_t, vmat, wmat, wslices, wscale, dpanel, sbr;

@@ -1,7 +1,7 @@
 // i8_core.cuh — shared machinery of the int8 tensor-core kernels (sm_100a):
 // tile geometry, tcgen05 / TMEM / TMA primitives, the TMA producer and the
 // single-thread MMA issuer of a persistent warp-specialised kernel, and the
-// exact int64 recombination of eight 7-bit slice products.  Used by
+// exact int64 recombination of seven 8-bit slice products.  Used by
 // rotate_i8_kernel (rotate_i8.cuh) and linear_solve_kernel (linear_solve.cuh).
 #pragma once
 
@@ -20,42 +20,37 @@ namespace gwg {
 
 
 
-// Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 8 slices x RB
+// Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 7 slices x RB
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
-template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1,
-          bool MMA2_ = false, int ACC_BUFS_ = 2>
+template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1>
 struct I8Tile {
   // CLUSTER = 2: CTA pairs (a thread-block cluster) work on SNP tiles 2u and
   // 2u+1 against the same B rows; each CTA loads half of the B tile (4 of the
-  // 8 slices) and multicasts it to both, halving the B operand's L2->SMEM
-  // traffic (used where B dominates: large n, one trait per tile).
-  // MMA2 (CLUSTER = 2): the pair runs ONE tcgen05.mma.cta_group::2 of
-  // M = 256 issued by the even CTA: each CTA keeps only its own half of B
-  // (N/2 rows) in shared memory, the MMA reads both halves, and each CTA's
-  // TMEM receives its own 128 SNP rows x N — same L2 traffic as multicast,
-  // half the B shared memory per stage, so deeper operand pipelines.
+  // 8 slice slots) and multicasts it to both, halving the B operand's
+  // L2->SMEM traffic (used where B dominates: large n, one trait per tile).
   static constexpr int CLUSTER = CLUSTER_;
-  static constexpr bool MMA2 = MMA2_;
-  static_assert(!MMA2 || CLUSTER == 2, "pair MMA needs a CTA pair");
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
-  static constexpr int SLICES = 8;
-  static constexpr int BN = SLICES * RB;  // UMMA N (<= 256, multiple of 16)
+  // Seven signed 8-bit slices (base-256 digits of a 55-bit integer, see
+  // slice_basis_kernel) in eight shared-memory slots: the 3-D TMA box covers
+  // whole slots, the eighth is zero-filled out of bounds and never multiplied.
+  static constexpr int SLICES = 7;
+  static constexpr int SLOTS = 8;
+  static constexpr int BN = (SLICES * RB + 15) / 16 * 16;  // UMMA N = TMEM columns per buffer
   static constexpr int BK = 128;          // int8 K per stage = one 128B swizzle row
   static constexpr int UK = 32;           // K per tcgen05.mma (int8)
   static constexpr int STAGES = STAGES_;
   static constexpr int OUT_BUFS = OUT_BUFS_;     // staging tiles per epilogue warp
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
-  static constexpr uint32_t B_BYTES = BN * BK;  // <= 32 KB
-  static constexpr int B_SLICES_PER_CTA = SLICES / CLUSTER;
+  static constexpr uint32_t B_BYTES = SLOTS * RB * BK;  // <= 32 KB of smem (slots)
+  static constexpr int B_SLICES_PER_CTA = SLOTS / CLUSTER;
   static constexpr uint32_t B_PART = B_BYTES / CLUSTER;  // loaded (and multicast) per CTA
-  static constexpr uint32_t B_SMEM = MMA2 ? B_PART : B_BYTES;  // B bytes held per CTA
-  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_SMEM;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
   static constexpr int TMEM_COLS = 512;   // ACC_BUFS accumulator buffers x BN
-  static constexpr int ACC_BUFS = ACC_BUFS_;  // MMA runs up to ACC_BUFS - 1 tiles ahead
+  static constexpr int ACC_BUFS = 2;      // MMA runs up to one tile ahead
   static_assert(ACC_BUFS * BN <= TMEM_COLS, "accumulator buffers fit TMEM");
   static constexpr int OUT_Q = 16;        // output box: 16 doubles (128 B) x 32 SNPs
   static constexpr uint32_t OUT_TILE = OUT_Q * 32 * 8;     // one 4 KB staging tile
@@ -64,6 +59,7 @@ struct I8Tile {
       size_t(STAGES) * STAGE_BYTES + size_t(EPI_WARPS) * OUT_BYTES + 1024 + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(BN % 16 == 0 && BN <= 256 && RB % 8 == 0, "UMMA N / swizzle atoms");
+  static_assert(BN <= SLOTS * RB, "the MMA reads only loaded (or zero-filled) slot rows");
 };
 using I8Cfg = I8Tile<32>;
 
@@ -171,71 +167,6 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask)
       : "memory");
 }
 
-// ---- CTA-pair (cta_group::2) primitives ----
-
-__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
-                                             uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(cta_mask)
-      : "memory");
-}
-
-// shared::cluster address of the same-offset location in CTA `rank`
-__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra.uni WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// TMA loads into this CTA's shared memory completing on an mbarrier that may
-// live in the peer CTA of the pair (cluster address, cta_group::2).
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int32_t c0,
-                                                 int32_t c1, uint32_t bar_cluster,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int32_t c0,
-                                                 int32_t c1, int32_t c2, uint32_t bar_cluster,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster),
-      "l"(policy)
-      : "memory");
-}
-
 // All threads of the cluster (release/acquire: barrier inits, smem writes).
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -269,16 +200,22 @@ __device__ __forceinline__ void tmem_ldw(uint32_t taddr, int32_t (&v)[W]) {
   }
 }
 
-// Exact recombination of the eight slice products of one output column:
-// hi = slices 0-3, lo = slices 4-7 as int64 (|hi|, |lo| < 2^53), one rounding.
+// Exact recombination of the seven slice products of one output column.
+// The sliced value is sigma 2^-55 N, N = sum_s d_s 256^(6-s) (|d_s| <= 128),
+// so the column is sigma 2^-55 sum_s P_s 256^(6-s) with P_s the int32 slice
+// products: hi = P0 2^16 + P1 2^8 + P2 and lo = P3 2^24 + ... + P6 are exact
+// int64 (< 2^48, < 2^56); lo's bits above 2^32 move into hi (both then below
+// 2^53, exactly convertible), and one FMA rounds hi 2^32 + lo once.
 __device__ __forceinline__ double i8_recombine(const int32_t a0, const int32_t a1, const int32_t a2,
                                                const int32_t a3, const int32_t a4, const int32_t a5,
-                                               const int32_t a6, const int32_t a7, double sc) {
-  const long long hi = (long long)a0 * (1ll << 21) + (long long)a1 * (1ll << 14) +
-                       (long long)a2 * (1ll << 7) + (long long)a3;
-  const long long lo = (long long)a4 * (1ll << 21) + (long long)a5 * (1ll << 14) +
-                       (long long)a6 * (1ll << 7) + (long long)a7;
-  return fma(double(lo), sc * 0x1p-56, double(hi) * (sc * 0x1p-28));
+                                               const int32_t a6, double sc) {
+  long long hi = (long long)a0 * (1ll << 16) + (long long)a1 * (1ll << 8) + (long long)a2;
+  long long lo = (long long)a3 * (1ll << 24) + (long long)a4 * (1ll << 16) +
+                 (long long)a5 * (1ll << 8) + (long long)a6;
+  const long long carry = lo >> 32;  // floor(lo / 2^32)
+  hi += carry;
+  lo -= carry * (1ll << 32);         // in [0, 2^32)
+  return fma(double(lo), sc * 0x1p-55, double(hi) * (sc * 0x1p-23));
 }
 
 // TMA 2-D store shared -> global (bulk async group of the issuing thread).
@@ -346,32 +283,21 @@ __device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp,
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
-      // the MMA of every CTA reading this stage (MMA2: the pair's one MMA)
-      mbar_init(&sm.empty[s], C::MMA2 ? 1 : C::CLUSTER);
+      mbar_init(&sm.empty[s], C::CLUSTER);  // the MMA of every CTA reading this stage
     }
     for (int b = 0; b < C::ACC_BUFS; ++b) {
       mbar_init(&sm.acc_full[b], 1);
-      // one arrive per epilogue warp using it (MMA2: of both CTAs, at the leader)
-      mbar_init(&sm.acc_empty[b], C::MMA2 ? 2 * acc_arrivals : acc_arrivals);
+      mbar_init(&sm.acc_empty[b], acc_arrivals);  // one arrive per epilogue warp using it
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    if constexpr (C::MMA2) {  // both CTAs of the pair, collectively
-      asm volatile(
-          "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-              smem_u32(sm.tmem_slot)),
-          "n"(C::TMEM_COLS)
-          : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile(
-          "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-              smem_u32(sm.tmem_slot)),
-          "n"(C::TMEM_COLS)
-          : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(sm.tmem_slot)),
+        "n"(C::TMEM_COLS)
+        : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   if (C::CLUSTER > 1)
@@ -388,26 +314,16 @@ __device__ __forceinline__ void i8_teardown(uint32_t tmem_base, int warp) {
     cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
   else
     __syncthreads();
-  if (warp == 1) {
-    if constexpr (C::MMA2)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                   "n"(C::TMEM_COLS)
-                   : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                   "n"(C::TMEM_COLS)
-                   : "memory");
-  }
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
 }
 
-// Epilogue warp: this tile's accumulator buffer may be overwritten (MMA2: the
-// arrival goes to the leader CTA, whose thread issues the pair's MMAs).
+// Epilogue warp: this tile's accumulator buffer may be overwritten.
 template <class C>
 __device__ __forceinline__ void i8_acc_release(const I8Smem<C>& sm, int buf) {
-  if constexpr (C::MMA2)
-    mbar_arrive_cluster(mapa_u32(&sm.acc_empty[buf], 0));
-  else
-    mbar_arrive(&sm.acc_empty[buf]);
+  mbar_arrive(&sm.acc_empty[buf]);
 }
 
 // Tile rasterisation shared by producer and epilogues: groups of I8_GROUP_M
@@ -479,17 +395,6 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
       t_empty += clock64() - te;
 #endif
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
-      if constexpr (C::MMA2) {
-        // both CTAs' loads complete on the leader's full[s]; the leader
-        // expects the pair's bytes (a peer transfer landing first only drives
-        // the transaction count negative until then)
-        if (sch.rank == 0) mbar_arrive_expect_tx(&sm.full[s], 2 * C::STAGE_BYTES);
-        const uint32_t fb = mapa_u32(&sm.full[s], 0);
-        tma_load_2d_pair(st, tmap_x, ks * C::BK, tm * C::BM, fb, pol_x);
-        tma_load_3d_pair(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB,
-                         sch.rank * C::B_SLICES_PER_CTA, fb, pol_b);
-        continue;
-      }
       mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
       tma_load_2d(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
       if (C::CLUSTER > 1)
@@ -509,40 +414,8 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
 
 // Warp 1, one thread: BK/UK tcgen05.mma per stage into the tile's TMEM buffer.
 template <class C>
-__device__ __forceinline__ void i8_mma_pair(const I8Smem<C>& sm, uint32_t tmem_base,
-                                            int my_tiles, int kstages) {
-  // leader CTA only: M = 256 (128 SNP rows per CTA), N = BN (BN/2 rows of B
-  // per CTA), same shared-memory offsets in both CTAs
-  constexpr uint32_t idesc = i8_instr_desc<C::BN, 2 * C::BM>();
-  int g = 0;
-  for (int lt = 0; lt < my_tiles; ++lt) {
-    const int buf = lt % C::ACC_BUFS;
-    if (lt >= C::ACC_BUFS) mbar_wait_cluster(&sm.acc_empty[buf], ((lt / C::ACC_BUFS) - 1) & 1);
-    tc_fence_after();
-    const uint32_t tmem_d = tmem_base + uint32_t(buf * C::BN);
-    for (int ks = 0; ks < kstages; ++ks, ++g) {
-      const int s = g % C::STAGES;
-      mbar_wait(&sm.full[s], (g / C::STAGES) & 1);
-      tc_fence_after();
-      const uint32_t sa = smem_u32(sm.base + s * C::STAGE_BYTES);
-      const uint32_t sb = sa + C::A_BYTES;
-#pragma unroll
-      for (int k = 0; k < C::BK / C::UK; ++k)
-        umma_i8_pair(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK),
-                     idesc, (ks | k) != 0);
-      umma_commit_pair(&sm.empty[s], 3);  // frees stage s in both CTAs
-    }
-    umma_commit_pair(&sm.acc_full[buf], 3);  // both CTAs' accumulators ready
-  }
-}
-
-template <class C>
 __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, int my_tiles,
                                        int kstages) {
-  if constexpr (C::MMA2) {
-    if (blockIdx.x % 2 == 0) i8_mma_pair<C>(sm, tmem_base, my_tiles, kstages);
-    return;
-  }
   constexpr uint16_t mask = uint16_t((1u << C::CLUSTER) - 1);
   constexpr uint32_t idesc = i8_instr_desc<C::BN, C::BM>();
   int g = 0;

@@ -44,15 +44,8 @@ namespace gwg {
 template <int P, int CL = 1>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
-  // CL = 4 (p <= 16): CTA pairs running one cta_group::2 MMA (M = 256) on
-  // half-width tiles (16 W rows, N = 128) with FOUR accumulator buffers in
-  // TMEM, one epilogue warp per buffer and lane quarter: the MMA runs up to
-  // three tiles ahead of the epilogue instead of one, and each CTA keeps half
-  // of B per stage (same L2 operand traffic as the 32-row multicast tiles).
-  static constexpr bool Q4 = CL == 4;
-  static_assert(!Q4 || P8 <= 16, "four accumulator buffers need N <= 128");
-  static constexpr int KT = Q4 ? 16 / P8 : (32 / P8 >= 1 ? 32 / P8 : 1);  // traits per tile
-  static constexpr int RB = KT * P8;                      // W rows per tile (16, 24 or 32)
+  static constexpr int KT = 32 / P8 >= 1 ? 32 / P8 : 1;  // traits per tile
+  static constexpr int RB = KT * P8;                      // W rows per tile (24 or 32)
   // WIDE (p <= 16): 16 epilogue warps (4 per TMEM lane quarter: 2 per
   // accumulator buffer, each doing half of a tile's cells; 96 registers) with
   // 3 operand stages — the epilogue is latency-bound, so more warps beat
@@ -60,16 +53,8 @@ struct LinCfg {
   // 8 epilogue warps (2 per quarter, all cells of alternate tiles) and 4
   // stages.  One 4 KB staging tile per epilogue warp.
   static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: p=4 3.15 -> 2.83 ms, p=12 8.56 -> 7.95
-  static constexpr int EPI = WIDE || Q4 ? 16 : 8;
-  // CL = 3 / 4: each CTA holds half of B per stage, so as many stages as
-  // shared memory takes (<= 8)
-  static constexpr int PAIR_STAGES_ =
-      int((227 * 1024 - EPI * 4096 - 1280) / (128 * 128 + RB * 8 * 128 / 2));
-  static constexpr int PAIR_STAGES = PAIR_STAGES_ < 8 ? PAIR_STAGES_ : 8;
-  using Tile = std::conditional_t<
-      Q4, I8Tile<RB, PAIR_STAGES, 1, EPI, 2, true, 4>,
-      std::conditional_t<CL == 3, I8Tile<RB, PAIR_STAGES, 1, EPI, 2, true>,
-                         I8Tile<RB, WIDE ? 3 : 4, 1, EPI, CL>>>;
+  static constexpr int EPI = WIDE ? 16 : 8;
+  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, EPI, CL>;
   static constexpr int ACC = Tile::ACC_BUFS;
   static constexpr int HMAX = EPI / 4 / ACC;              // warps per quarter and buffer
   static constexpr int HALVES = KT >= HMAX ? HMAX : 1;    // warps splitting one tile
@@ -79,7 +64,7 @@ struct LinCfg {
   static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
   static constexpr bool TMA_OUT = ROW % CHUNK == 0;       // whole 128-byte chunks
   // cells solved together (independent chains; KT is a power of two or 1)
-  static constexpr int GMAX = WIDE || Q4 ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
+  static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
   static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
   // large p: triangular solves as products with L^-1 (independent dot
@@ -209,11 +194,11 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
                   if (LIN_EXPERIMENT == 5)
                     dst[u0 + u][c0 + r] = double(v[u][0][r] + v[u][1][r] + v[u][2][r] +
                                                  v[u][3][r] + v[u][4][r] + v[u][5][r] +
-                                                 v[u][6][r] + v[u][7][r]) * sc;
+                                                 v[u][6][r]) * sc;
                   else
                     dst[u0 + u][c0 + r] = i8_recombine(v[u][0][r], v[u][1][r], v[u][2][r],
                                                        v[u][3][r], v[u][4][r], v[u][5][r],
-                                                       v[u][6][r], v[u][7][r], sc);
+                                                       v[u][6][r], sc);
                 }
               }
           }
@@ -320,21 +305,17 @@ cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int sms,
                                 cudaStream_t s) {
   using C = typename LinCfg<P, CL>::Tile;
-  const int64_t units = int64_t((a.tiles_m + C::CLUSTER - 1) / C::CLUSTER) * a.tiles_r;
+  const int64_t units = int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
   return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a);
 }
 
 // Per-p entry of the split grid (kernels_lin_*.cu).
 struct LinOps {
   int kt = 0, p8 = 0, rb = 0;
-  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile;
-  // [2]: CTA pairs running one cta_group::2 MMA (each CTA loads its half of B);
-  // [3]: the same on 16-row tiles with four accumulator buffers (p <= 16)
-  cudaError_t (*launch[4])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr, nullptr,
-                                                                 nullptr};
-  int b_slices_box[4] = {8, 4, 4, 4};
-  int kt_q4 = 0, rb_q4 = 0;  // tile geometry of launch[3] (W row layout j * p8 + c is shared)
+  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile
+  cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
+  int b_slices_box[2] = {8, 4};  // slice slots per TMA box
 };
 
 template <int P>
@@ -345,12 +326,6 @@ LinOps make_lin_ops() {
   o.rb = LinCfg<P>::RB;
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
-  o.launch[2] = &launch_linear_solve<P, 3>;
-  if constexpr (LinCfg<P>::P8 <= 16) {
-    o.launch[3] = &launch_linear_solve<P, 4>;
-    o.kt_q4 = LinCfg<P, 4>::KT;
-    o.rb_q4 = LinCfg<P, 4>::RB;
-  }
   return o;
 }
 

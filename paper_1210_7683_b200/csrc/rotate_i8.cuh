@@ -3,24 +3,26 @@
 //
 // X' = Z^T X_R where X_R holds integer genotype codes (BASELINE.json: {0,1,2}).
 // Each eigenvector z_r (column r of Z) is scaled by a power of two sigma_r
-// (|z_r / sigma_r| <= 1/2) and split into eight 7-bit signed slices,
-//     z_r / sigma_r = sum_{s<8} q_{s,r} 2^{-7(s+1)} + O(2^{-57}),  |q| <= 64,
-// so  X'[r, i] = sigma_r sum_s 2^{-7(s+1)} (q_{s,r} . x_i)  where every inner
-// product is an EXACT int32 dot product of int8 vectors (|q x| <= 64*127, so
-// exact for n < 262,000).  The eight partial results are combined exactly in
-// int64 and converted with a single rounding, so X' is the correctly rounded
-// value of sigma_r (56-bit slice expansion of z_r) . x_i — below a DGEMM's
-// error — and each column depends only on (Z, x_i): bitwise identical for any
-// slab width, like rotate_kernel.  The DMMA rotation (rotate_kernel.cuh) remains the
-// general path for real-valued SNP data.
+// (|z_r / sigma_r| <= 1/2), rounded to N_r = rint(2^55 z_r / sigma_r) and
+// written as seven signed 8-bit base-256 digits (slice_basis_kernel),
+//     z_r / sigma_r = 2^-55 sum_{s<7} d_{s,r} 256^(6-s) + O(2^-56),  |d| <= 128,
+// so  X'[r, i] = sigma_r 2^-55 sum_s 256^(6-s) (d_{s,r} . x_i)  where every
+// inner product is an EXACT int32 dot product of int8 vectors (|d x| <=
+// 128*127, so exact for n < 132,000).  The seven partial results are combined
+// exactly in int64 and converted with a single rounding, so X' is the
+// correctly rounded value of sigma_r (55-bit expansion of z_r) . x_i — below a
+// DGEMM's error — and each column depends only on (Z, x_i): bitwise identical
+// for any slab width, like rotate_kernel.  The DMMA rotation
+// (rotate_kernel.cuh) remains the general path for real-valued SNP data.
 //
-// GEMM view per CTA tile: M = 128 SNPs (A = X int8, K-major), N = 256 =
-// 8 slices x 32 eigen-rows (B = slices, K-major), K = samples, int32 D in TMEM.
-// Warp roles: warp 0 = TMA producer (SWIZZLE_128B boxes, 4-stage mbarrier
-// ring), warp 1 = MMA issuer (one thread, 4 x tcgen05.mma M128 N256 K32 per
-// stage) and TMEM owner (2 x 256 columns: double-buffered accumulators),
-// warps 4-11 = epilogue (tcgen05.ld 32x32b, exact int64 recombination, X'
-// and/or X'.X' tiles out through 128B-swizzled staging + TMA stores).
+// GEMM view per CTA tile: M = 128 SNPs (A = X int8, K-major), N = 224 =
+// 7 slices x 32 eigen-rows (B = slices in 8 smem slots, K-major), K = samples,
+// int32 D in TMEM.  Warp roles: warp 0 = TMA producer (SWIZZLE_128B boxes,
+// 4-stage mbarrier ring), warp 1 = MMA issuer (one thread, 4 x tcgen05.mma
+// M128 N224 K32 per stage) and TMEM owner (2 x 224 columns: double-buffered
+// accumulators), warps 4-11 = epilogue (tcgen05.ld 32x32b, exact int64
+// recombination, X' and/or X'.X' tiles out through 128B-swizzled staging +
+// TMA stores).
 #pragma once
 
 #include "i8_core.cuh"
@@ -41,10 +43,9 @@ struct I8Args {
 
 // ---- the rotation kernel -------------------------------------------------------
 
-// CL: 1 single CTAs, 2 CTA pairs multicasting B, 3 CTA pairs running one
-// cta_group::2 MMA (half the B shared memory per stage: 6 stages)
+// CL: 1 single CTAs, 2 CTA pairs multicasting B
 template <int CL>
-using RotI8Cfg = std::conditional_t<CL == 3, I8Tile<32, 6, 1, 8, 2, true>, I8Tile<32, 4, 1, 8, CL>>;
+using RotI8Cfg = I8Tile<32, 4, 1, 8, CL>;
 
 template <int CL>
 __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r)
           x[c * 8 + r] = i8_recombine(v[0][r], v[1][r], v[2][r], v[3][r], v[4][r], v[5][r],
-                                      v[6][r], v[7][r], sc[r]);
+                                      v[6][r], sc[r]);
       }
       tc_fence_before();
       __syncwarp();
@@ -163,6 +164,10 @@ __global__ void __launch_bounds__(256) snp_to_i8_kernel(const double* __restrict
 
 // Z (n x ncols, ld ldz) -> slices [s][r][kp] int8 and scale[r] = sigma_r: one
 // block per column r (an eigenvector of Z, or a column of W for the split grid).
+// v = z / sigma (exact, |v| <= 1/2), N = rint(v 2^55) (|N| <= 2^54), written
+// in balanced base 256: N = sum_s d_s 256^(6-s) with d_6..d_1 in [-128, 127]
+// and |d_0| <= 65, so every digit is an int8 and the column is sigma 2^-55 N
+// (relative to sigma, within 2^-56 of z / sigma).
 __global__ void slice_basis_kernel(const double* __restrict__ z, int64_t ldz, int32_t n,
                                    int32_t ncols, int32_t kp, int8_t* __restrict__ slices,
                                    double* __restrict__ scale) {
@@ -187,13 +192,13 @@ __global__ void slice_basis_kernel(const double* __restrict__ z, int64_t ldz, in
   const double inv = 1.0 / red[0];  // exact: power of two
   const int64_t plane = int64_t(ncols) * kp;
   for (int k = threadIdx.x; k < kp; k += blockDim.x) {
-    double v = k < n ? col[k] * inv : 0.0;  // exact scaling
+    const double v = k < n ? col[k] * inv : 0.0;  // exact scaling
+    long long q = llrint(v * 0x1p55);             // exact scaling, one rounding
 #pragma unroll
-    for (int s = 0; s < I8Cfg::SLICES; ++s) {
-      const double t = v * 128.0;          // exact
-      const double qd = rint(t);
-      slices[s * plane + int64_t(r) * kp + k] = int8_t(qd);
-      v = t - qd;                          // exact (Sterbenz), |v| <= 1/2
+    for (int s = I8Cfg::SLICES - 1; s >= 0; --s) {
+      const long long d = ((q + 128) & 255) - 128;
+      slices[s * plane + int64_t(r) * kp + k] = int8_t(d);
+      q = (q - d) >> 8;  // exact: q - d is a multiple of 256
     }
   }
 }

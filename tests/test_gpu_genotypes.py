@@ -218,16 +218,14 @@ def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
 @pytest.mark.parametrize("n,p,m,t", [(200, 4, 300, 20), (1000, 4, 1000, 64), (300, 12, 129, 17),
                                      (257, 20, 333, 7)])
 def test_int8_kernel_variants_bitwise_identical(n, p, m, t, monkeypatch):
-    """Every int8 launch geometry (GWG_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
-    multicasting B, 3 CTA pairs with one cta_group::2 MMA, 4 the same on
-    16-row tiles with four TMEM accumulator buffers) gives the same bits:
-    the int32 slice products are exact and the recombination order fixed."""
+    """Both int8 launch geometries (GWG_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
+    multicasting B) give the same bits: the int32 slice products are exact
+    and the recombination order fixed."""
     ds = datagen.generate(n, p, m, t, seed=n + p)
     basis, values = gw.eigendecompose(ds["kinship"])
     out = {}
-    for cl in ("1", "2", "3", "4"):
+    for cl in ("1", "2"):
         monkeypatch.setenv("GWG_I8_CLUSTER", cl)
         out[cl] = run(ds, basis, values, "genotypes")
     assert not np.isnan(out["2"]).any()
-    for cl in ("1", "3", "4"):
-        assert np.array_equal(out[cl], out["2"]), cl
+    assert np.array_equal(out["1"], out["2"])
