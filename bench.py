@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GLS problems solved/sec (m·t/s) at n=1000,p=4; FP64 TFLOP/s vs B200 peak"
 PEAK_FP64_TFLOPS = 37.15  # measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.txt
-I8_SLICES = 8  # int8 slices of W per linear term (rotate_i8.cuh)
+I8_SLICES = 7  # int8 slices of W per linear term (i8_core.cuh, slice_basis_kernel)
 # int8 dense tensor peak measured on this pool's B200 (tools/i8_peak.cu:
 # tcgen05.mma kind::i8 M128 N256 K32 from resident smem, 148 CTAs, 1965 MHz);
 # MEASURED_PEAKS.json has no int8 entry
@@ -240,7 +240,7 @@ def run_ours(args):
         #    exponential-sum terms, 2 r (n + t) flop per SNP (or the direct
         #    contraction, 2 n flop per cell, when sbr_terms = 0);
         #  * linear_solve_kernel: the p linear terms exactly on the int8 tensor
-        #    cores (8 slices of W, 2 n p ops per slice per cell) + the solve.
+        #    cores (7 slices of W, 2 n p ops per slice per cell) + the solve.
         # The primary roofline entry is the stage with the larger share.
         quad_ms = cnt["quad_ms"] / args.steps
         lin_ms = cnt["linear_ms"] / args.steps
@@ -261,11 +261,11 @@ def run_ours(args):
         lin_entry = {"bound": "tensor", "achieved": lin_achieved, "peak": PEAK_INT8_TOPS,
                      "unit": "TOP/s", "frac": lin_achieved / PEAK_INT8_TOPS,
                      "traffic": load_traffic("linear_solve_kernel"),
-                     "kernel": "linear_solve_kernel<P=%d> (x^T W on 8 int8 slices + bordered "
+                     "kernel": "linear_solve_kernel<P=%d> (x^T W on 7 int8 slices + bordered "
                                "Cholesky)" % p,
                      "kernel_ms": lin_ms, "peak_source": PEAK_INT8_SOURCE,
                      "algorithmic_ops_per_launch": lin_ops,
-                     "algorithmic_unit": "2 n p int8 ops per slice per cell, 8 slices"}
+                     "algorithmic_unit": "2 n p int8 ops per slice per cell, 7 slices"}
         primary, secondary = (lin_entry, sbr_entry) if lin_ms >= quad_ms else (sbr_entry, lin_entry)
         roof = dict(primary)
         roof["secondary"] = secondary
