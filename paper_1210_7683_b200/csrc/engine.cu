@@ -368,6 +368,9 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
       }
     }
     rg[5] = bad ? 1.0 : 0.0;
+  } else if (e->range_pending) {  // queued by gwg_set_traits
+    GWG_CUDA_TRY(cudaEventSynchronize(e->ev_range));
+    std::copy(e->range_host, e->range_host + 6, rg);
   } else {  // device-resident inputs: one small reduction and a round trip
     gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(),
                                                       e->sigma2.d(), int32_t(t), dx);
@@ -766,6 +769,9 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     return bail("cudaMalloc", err);
   if ((err = cudaMallocHost(&e->err_host, 3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMallocHost", err);
+  if ((err = cudaMallocHost(&e->range_host, 8 * sizeof(double))) != cudaSuccess)
+    return bail("cudaMallocHost", err);
+  cudaEventCreateWithFlags(&e->ev_range, cudaEventDisableTiming);
   return e;
 }
 
@@ -782,6 +788,8 @@ void gwg_engine_destroy(gwg_engine* e) {
                     &e->gmat, &e->exps})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
+  if (e->range_host) cudaFreeHost(e->range_host);
+  if (e->ev_range) cudaEventDestroy(e->ev_range);
   for (int b = 0; b < 2; ++b) {
     if (e->ev_h2d[b]) cudaEventDestroy(e->ev_h2d[b]);
     if (e->ev_rot_done[b]) cudaEventDestroy(e->ev_rot_done[b]);
@@ -874,9 +882,22 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   if (int rc = upload(e, e->h2, h2, size_t(t), where, st)) return rc;
   if (int rc = upload(e, e->sigma2, sigma2, size_t(t), where, st)) return rc;
   e->traits_host_valid = where == GWG_HOST;
+  e->range_pending = false;
   if (e->traits_host_valid) {
     e->h2_host.assign(h2, h2 + t);
     e->s2_host.assign(sigma2, sigma2 + t);
+  } else if (e->snp_coding == GWG_SNP_GENOTYPES && e->split && e->lowrank) {
+    // queue the exponential sum's range now: by the time the split grid is
+    // built the 48-byte answer is on the host and no round trip stalls it
+    GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
+    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
+                                                      e->sigma2.d(), int32_t(t), e->exps.d());
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    GWG_CUDA_TRY(cudaMemcpyAsync(e->range_host, e->exps.d(), 6 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, e->comp));
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_range, e->comp));
+    e->range_pending = true;
   }
   const int64_t tiles_t = ceil_div(t, e->ops.bt);
   const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;

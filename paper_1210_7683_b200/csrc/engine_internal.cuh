@@ -109,6 +109,11 @@ struct gwg_engine {
   // the factorisation's range is then found without a device round trip
   std::vector<double> h2_host, s2_host;
   bool traits_host_valid = false;
+  // device-resident traits: the range reduction is queued by gwg_set_traits
+  // (pinned range_host, ev_range) and read when the split grid is built
+  double* range_host = nullptr;
+  cudaEvent_t ev_range = nullptr;
+  bool range_pending = false;
   // min / max of the spectrum (found once per spectrum); lam_bad = non-finite
   double lam_lo = 0.0, lam_hi = 0.0;
   bool lam_bad = false;

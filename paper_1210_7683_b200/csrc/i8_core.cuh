@@ -205,17 +205,18 @@ __device__ __forceinline__ void tmem_ldw(uint32_t taddr, int32_t (&v)[W]) {
 // so the column is sigma 2^-55 sum_s P_s 256^(6-s) with P_s the int32 slice
 // products: hi = P0 2^16 + P1 2^8 + P2 and lo = P3 2^24 + ... + P6 are exact
 // int64 (< 2^48, < 2^56); lo's bits above 2^32 move into hi (both then below
-// 2^53, exactly convertible), and one FMA rounds hi 2^32 + lo once.
+// 2^53, exactly convertible), one FMA rounds hi 2^32 + lo once, and the
+// power-of-two scale sc55 = sigma 2^-55 is applied exactly.
 __device__ __forceinline__ double i8_recombine(const int32_t a0, const int32_t a1, const int32_t a2,
                                                const int32_t a3, const int32_t a4, const int32_t a5,
-                                               const int32_t a6, double sc) {
+                                               const int32_t a6, double sc55) {
   long long hi = (long long)a0 * (1ll << 16) + (long long)a1 * (1ll << 8) + (long long)a2;
   long long lo = (long long)a3 * (1ll << 24) + (long long)a4 * (1ll << 16) +
                  (long long)a5 * (1ll << 8) + (long long)a6;
   const long long carry = lo >> 32;  // floor(lo / 2^32)
   hi += carry;
   lo -= carry * (1ll << 32);         // in [0, 2^32)
-  return fma(double(lo), sc * 0x1p-55, double(hi) * (sc * 0x1p-23));
+  return fma(double(hi), 0x1p32, double(lo)) * sc55;
 }
 
 // TMA 2-D store shared -> global (bulk async group of the issuing thread).

@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       }
       // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
       // to the recombination below: no per-column memory round trip
-      const double sc_lane = lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
+      const double sc_lane =
+          lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) * 0x1p-55 : 0.0;  // sigma 2^-55, exact
       mbar_wait(&sm.acc_full[buf], par);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);

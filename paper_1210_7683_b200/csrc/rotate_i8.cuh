@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int row = r0 + c * 8 + r;
-          sc[r] = row < a.n ? __ldg(a.scale + row) : 0.0;
+          sc[r] = row < a.n ? __ldg(a.scale + row) * 0x1p-55 : 0.0;  // exact
         }
         int32_t v[C::SLICES][8];
 #pragma unroll
