@@ -210,13 +210,11 @@ __device__ __forceinline__ void tmem_ldw(uint32_t taddr, int32_t (&v)[W]) {
 __device__ __forceinline__ double i8_recombine(const int32_t a0, const int32_t a1, const int32_t a2,
                                                const int32_t a3, const int32_t a4, const int32_t a5,
                                                const int32_t a6, double sc55) {
-  long long hi = (long long)a0 * (1ll << 16) + (long long)a1 * (1ll << 8) + (long long)a2;
-  long long lo = (long long)a3 * (1ll << 24) + (long long)a4 * (1ll << 16) +
-                 (long long)a5 * (1ll << 8) + (long long)a6;
-  const long long carry = lo >> 32;  // floor(lo / 2^32)
-  hi += carry;
-  lo -= carry * (1ll << 32);         // in [0, 2^32)
-  return fma(double(hi), 0x1p32, double(lo)) * sc55;
+  const long long hi = (long long)a0 * (1ll << 16) + (long long)a1 * (1ll << 8) + (long long)a2;
+  const long long lo = (long long)a3 * (1ll << 24) + (long long)a4 * (1ll << 16) +
+                       (long long)a5 * (1ll << 8) + (long long)a6;
+  // lo = (lo >> 32) 2^32 + its low word (two's complement): the carry joins hi
+  return fma(double(hi + (lo >> 32)), 0x1p32, double(uint32_t(lo))) * sc55;
 }
 
 // TMA 2-D store shared -> global (bulk async group of the issuing thread).
