@@ -45,7 +45,7 @@ enum gwg_code {
 
 enum gwg_where { GWG_HOST = 0, GWG_DEVICE = 1 };
 enum gwg_layout { GWG_LAYOUT_NUMPY = 0, GWG_LAYOUT_STREAM = 1 };
-enum gwg_snp_coding { GWG_SNP_REAL = 0, GWG_SNP_GENOTYPES = 1 };
+enum gwg_snp_coding { GWG_SNP_REAL = 0, GWG_SNP_GENOTYPES = 1, GWG_SNP_AUTO = 2 };
 
 typedef struct gwg_status {
   int32_t code;
@@ -199,18 +199,21 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
 
 /* How SNP slabs are coded (no reference counterpart: the reference stores
  * X_R as doubles and its generator draws genotype codes, datagen.cpp /
- * BASELINE.json).  GWG_SNP_REAL (default): any real values; the rotation and
- * the grid run on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP
- * value is an integer code in [-127, 127] (e.g. genotypes 0/1/2), checked on
- * the device (violations fail with GWG_DIMENSION); n < 132,000.  Then the
+ * BASELINE.json).  GWG_SNP_REAL: any real values; the rotation and the grid
+ * run on the FP64 tensor pipe (DMMA).  GWG_SNP_GENOTYPES: every SNP value is
+ * an integer code in [-127, 127] (e.g. genotypes 0/1/2), checked on the
+ * device (violations fail with GWG_DIMENSION); n < 132,000.  Then the
  * rotation X'.X' and the p linear terms of every cell (x^T W, W = Z D [X_L' Y'])
  * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, seven 8-bit
  * slices, exact int64 recombination, one rounding) and only S_BR = (X'.X')^T D
  * stays on DMMA, factorised as ((X'.X')^T E) F through a positive exponential
- * sum of D (gwg_exp_sum_design; GWG_SBR_DIRECT=1 in the environment forces the
- * direct contraction) — the same cells to rounding (~1e-14 norm-wise), ~6x
- * faster than the all-FP64 path at BASELINE config 1; results stay bitwise
- * independent of slab geometry.
+ * sum of D (gwg_exp_sum_design; GWG_SNP_GENOTYPES with GWG_SBR_DIRECT=1 in the
+ * environment forces the direct contraction) — the same cells to rounding
+ * (~1e-14 norm-wise), ~6.5x faster than the all-FP64 path at BASELINE config
+ * 1; results stay bitwise independent of slab geometry.  GWG_SNP_AUTO (the
+ * default): per slab, the device check decides — a slab of codes takes the
+ * genotype path, any other slab the FP64 path (both are queued; the kernels
+ * of the path not taken return at once, no host round trip), never an error.
  * Pre-rotated slabs (is_rotated = 1) always take the FP64 path. */
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
 

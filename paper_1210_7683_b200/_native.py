@@ -27,6 +27,7 @@ GWG_LAYOUT_NUMPY = 0
 GWG_LAYOUT_STREAM = 1
 GWG_SNP_REAL = 0
 GWG_SNP_GENOTYPES = 1
+GWG_SNP_AUTO = 2
 
 # Every symbol include/gwgrid_cuda.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (

@@ -92,7 +92,7 @@ def load_manifest(data_dir: str) -> dict:
     return out
 
 
-def _engine_for(man: dict, device_eig: bool, snp_coding: str = "real") -> Engine:
+def _engine_for(man: dict, device_eig: bool, snp_coding: str = "auto") -> Engine:
     kin = gwg1.read_columns(man["kinship"], gwg1.KIND_OPERAND)
     xl = gwg1.read_columns(man["xl"], gwg1.KIND_OPERAND)
     eng = Engine(man["n"], man["p"])
@@ -229,8 +229,9 @@ def main(argv=None) -> int:
     s.add_argument("--out", default="")
     s.add_argument("--mb", type=int, default=0)
     s.add_argument("--device-eig", action="store_true")
-    s.add_argument("--snp-coding", choices=("real", "genotypes"), default="real",
-                   help="genotypes: integer codes on the exact int8 tensor-core path")
+    s.add_argument("--snp-coding", choices=("auto", "real", "genotypes"), default="auto",
+                   help="auto: per slab, the exact int8 tensor-core path when every value "
+                        "is an integer code; genotypes: codes required; real: FP64 path")
     v = sub.add_parser("verify", help="recheck result cells against the Cholesky route")
     v.add_argument("--data", required=True)
     v.add_argument("--results", default="")
@@ -242,7 +243,7 @@ def main(argv=None) -> int:
     b.add_argument("--data", required=True)
     b.add_argument("--out", default="")
     b.add_argument("--csv", default="")
-    b.add_argument("--snp-coding", choices=("real", "genotypes"), default="real")
+    b.add_argument("--snp-coding", choices=("auto", "real", "genotypes"), default="auto")
     sub.add_parser("tune", help="(out of scope: the reference's CPU/disk tuner)")
     a = ap.parse_args(argv)
     if a.cmd == "tune":

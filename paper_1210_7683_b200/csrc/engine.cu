@@ -164,6 +164,8 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
   a.tiles_m = int32_t(ceil_div(e->n, gwg::RotCfg::BM));
   a.tiles_n = int32_t(ceil_div(cols, gwg::RotCfg::BN));
   a.kchunks = int32_t(e->np / gwg::RotCfg::BK);
+  a.gate = gate_word(e);
+  a.gate_codes = e->gate_want;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_n;
   GWG_CUDA_TRY(gwg::launch_rotate(tz, tx, a, int(std::min<int64_t>(tiles, e->sms)), e->comp));
   e->counters.kernel_launches += 1;
@@ -175,7 +177,7 @@ int read_errors(gwg_engine* e, gwg_status* st, bool trait_only) {
   GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 3 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
-  if (!trait_only && e->err_host[2] != ~0ull)
+  if (!trait_only && e->snp_coding == GWG_SNP_GENOTYPES && e->err_host[2] != ~0ull)
     return set_status(st, GWG_DIMENSION, -1, -1,
                       "SNP values are not integer genotype codes in [-127, 127] "
                       "(gwg_set_snp_coding(GENOTYPES)); use real-valued coding");
@@ -254,6 +256,8 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   a.tiles_r = int32_t(ceil_div(ncols, I8Cfg::RB));
   a.kstages = int32_t(kp / I8Cfg::BK);
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
+  a.gate = gate_word(e);
+  a.gate_codes = e->gate_want;
   // CTA pairs multicasting the B (Z-slice) tile when it streams from HBM
   // (measured at n = 10,000: 69.2 -> 49.0 ms; neutral at n = 1000)
   const int cl = e->i8_cluster ? e->i8_cluster : (e->n >= 4096 ? 2 : 1);
@@ -274,8 +278,15 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
 
 int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st) {
   e->slab_i8 = false;
-  if (e->snp_coding == 0) return rotate(e, src, cols, e->rot.d(), st, lds, e->rot_sq.d());
+  e->slab_auto = false;
+  const bool i8_ok = e->n < kMaxGenotypeN;
+  if (e->snp_coding == GWG_SNP_REAL || (e->snp_coding == GWG_SNP_AUTO && !i8_ok))
+    return rotate(e, src, cols, e->rot.d(), st, lds, e->rot_sq.d());
   if (cols <= 0) return GWG_OK;
+  const bool autom = e->snp_coding == GWG_SNP_AUTO;
+  if (autom)  // this slab's verdict alone decides its path
+    GWG_CUDA_TRY(cudaMemsetAsync(static_cast<unsigned long long*>(e->err.ptr) + 2, 0xff,
+                                 sizeof(unsigned long long), e->comp));
   NvtxRange nvtx_("rotate_i8");
   using gwg::I8Cfg;
   const int64_t n = e->n, kp = round_up(n, I8Cfg::BK);
@@ -299,11 +310,18 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
     e->counters.kernel_launches += 1;
   }
   // the split grid needs only X'.X' (its linear terms come from the codes)
-  if (int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
-                         e->split ? nullptr : e->rot.d(), e->rot_sq.d(), e->np, st))
-    return rc;
+  if (autom) e->gate_want = 1;
+  int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
+                     e->split ? nullptr : e->rot.d(), e->rot_sq.d(), e->np, st);
+  if (autom && rc == GWG_OK) {  // the FP64 rotation for a slab with non-code values
+    e->gate_want = 0;
+    rc = rotate(e, src, cols, e->rot.d(), st, lds, e->rot_sq.d());
+  }
+  e->gate_want = -1;
+  if (rc) return rc;
   e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
   e->slab_i8 = true;
+  e->slab_auto = autom;
   return GWG_OK;
 }
 
@@ -527,6 +545,8 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     q.kchunks = int32_t(pk / so.bk);
     q.np = pk;
     q.rowmajor = rowmajor ? 1 : 0;
+    q.gate = gate_word(e);
+    q.gate_codes = e->gate_want;
     const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
     GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
     e->counters.kernel_launches += 1;
@@ -590,6 +610,8 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.tiles_r = int32_t(tiles_r);
   a.kstages = int32_t(kp / I8Cfg::BK);
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
+  a.gate = gate_word(e);
+  a.gate_codes = e->gate_want;
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   (void)tiles;
@@ -607,8 +629,24 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
   const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
   e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
   e->counters.loop_flops += cells * uint64_t(e->n) * (5 + 2 * uint64_t(e->p - 1));
+  if (e->slab_auto) {  // both paths queued, each gated on the slab's verdict
+    e->gate_want = e->split ? 1 : -1;
+    int rc = e->split ? launch_split(e, rot_sq, rows, i0, m_total, dev_out, out_si, out_sj, st)
+                      : GWG_OK;
+    e->gate_want = e->split ? 0 : -1;
+    if (rc == GWG_OK) rc = launch_fused(e, rot, rot_sq, rows, i0, m_total, dev_out, out_si, out_sj, st);
+    e->gate_want = -1;
+    return rc;
+  }
   if (e->slab_i8 && e->split)
     return launch_split(e, rot_sq, rows, i0, m_total, dev_out, out_si, out_sj, st);
+  return launch_fused(e, rot, rot_sq, rows, i0, m_total, dev_out, out_si, out_sj, st);
+}
+
+// The all-FP64 fused grid kernel over one rotated slab.
+int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
+                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
+                 gwg_status* st) {
   CUtensorMap map, map_sq;
   if (int rc = encode_kmajor(&map, rot, e->n, rows, e->np, e->ops.bm, st)) return rc;
   if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->ops.bm, st)) return rc;
@@ -627,6 +665,8 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
   a.kchunks = int32_t(e->np / e->ops.bk);
   a.np = e->np;
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
+  a.gate = gate_word(e);
+  a.gate_codes = e->gate_want;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_t;
   const int ctas = int(std::min<int64_t>(tiles, e->sms));
   GWG_CUDA_TRY(e->ops.grid(map, map_sq, a, ctas, e->comp));
@@ -636,6 +676,7 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
 
 int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st) {
   e->slab_i8 = false;
+  e->slab_auto = false;
   GWG_CUDA_TRY(gwg::launch_square(e->rot.d(), e->rot_sq.d(), size_t(e->np) * cols, e->comp));
   e->counters.kernel_launches += 1;
   return GWG_OK;
@@ -886,7 +927,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   if (e->traits_host_valid) {
     e->h2_host.assign(h2, h2 + t);
     e->s2_host.assign(sigma2, sigma2 + t);
-  } else if (e->snp_coding == GWG_SNP_GENOTYPES && e->split && e->lowrank) {
+  } else if (e->snp_coding != GWG_SNP_REAL && e->split && e->lowrank) {
     // queue the exponential sum's range now: by the time the split grid is
     // built the 48-byte answer is on the host and no round trip stalls it
     GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
@@ -1153,9 +1194,9 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
-  if (coding != GWG_SNP_REAL && coding != GWG_SNP_GENOTYPES)
-    return set_status(st, GWG_DIMENSION, -1, -1, "unknown SNP coding %d", coding);
-  if (coding == GWG_SNP_GENOTYPES && e->n >= 132000)
+  if (coding != GWG_SNP_REAL && coding != GWG_SNP_GENOTYPES && coding != GWG_SNP_AUTO)
+    return set_status(st, GWG_DIMENSION, -1, -1, "unknown SNP coding %d", int(coding));
+  if (coding == GWG_SNP_GENOTYPES && e->n >= kMaxGenotypeN)
     return set_status(st, GWG_DIMENSION, -1, -1,
                       "genotype coding needs n < 132,000 (exact int32 accumulation)");
   e->snp_coding = coding;

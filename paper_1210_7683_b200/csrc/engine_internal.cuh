@@ -84,7 +84,7 @@ struct gwg_engine {
   gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key, [2] genotype check
   // SNP coding: 0 = real-valued (DMMA rotation), 1 = integer genotype codes
   // (exact int8 tcgen05 rotation); slices of Z are rebuilt after a new spectrum.
-  int snp_coding = 0;
+  int snp_coding = GWG_SNP_AUTO;
   bool slices_valid = false;
   gwg_host::DevBuf zslices, zscale, xi8;
   // Split grid for genotype slabs (grid_split.cuh): linear terms x_i^T W on
@@ -93,6 +93,11 @@ struct gwg_engine {
   // (GWG_SPLIT=0 in the environment turns it off for A/B timing);
   // `slab_i8` = the current slab was rotated from integer codes (xi8 valid).
   bool split = true, slab_i8 = false;
+  // GWG_SNP_AUTO: the current slab queued both paths, each gated on its
+  // verdict (err word 2); gate_want = path of the launches being queued
+  // (1 genotype, 0 FP64, -1 ungated)
+  bool slab_auto = false;
+  int gate_want = -1;
   // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs multicasting B
   // (GWG_I8_CLUSTER)
   int i8_cluster = 0;
@@ -146,6 +151,15 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
 int build_split(gwg_engine* e, gwg_status* st);
 // Genotype split grid on raw slabs: X' is never materialised (only X'.X').
 bool rotated_x_unused(const gwg_engine* e);
+// exact int32 slice products need n * 127 * 128 < 2^31
+constexpr int64_t kMaxGenotypeN = 132000;
+// the path gate for the launches being queued (null = ungated)
+inline const unsigned long long* gate_word(const gwg_engine* e) {
+  return e->gate_want >= 0 ? static_cast<const unsigned long long*>(e->err.ptr) + 2 : nullptr;
+}
+int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
+                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
+                 gwg_status* st);
 // Invalidate everything derived from traits / spectrum.
 void invalidate_derived(gwg_engine* e, bool spectrum);
 // SNP slab -> e->rot / e->rot_sq with the engine's SNP coding (DMMA or int8).

@@ -124,6 +124,8 @@ struct GridArgs {
   int32_t kchunks;      // NP / BK
   int64_t np;           // padded n (multiple of BK)
   unsigned long long* err_key;  // min over failing cells of j*m_total + i
+  const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
+  int32_t gate_codes = 0;
 };
 
 // Bordered Cholesky solve of one cell.  The leading (p-1) block of chol(S) is
@@ -258,6 +260,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     gls_grid_kernel(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_q, const GridArgs args) {
+  if (gate_closed(args.gate, args.gate_codes)) return;
   constexpr int P = Cfg::P;
   constexpr int NC = Cfg::NC;
   constexpr int KO = Cfg::BK / 8;  // k-octets per stage

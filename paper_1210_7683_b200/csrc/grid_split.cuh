@@ -72,6 +72,8 @@ struct SbrArgs {
   int32_t kchunks;
   int64_t np;        // K extent of one D panel (its stride between trait tiles)
   int32_t rowmajor;  // 1: store out[i * ld + j] instead (j < t, t a multiple of BT)
+  const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
+  int32_t gate_codes = 0;
 };
 
 template <class Cfg>
@@ -102,6 +104,7 @@ __device__ __forceinline__ void sbr_issue(const CUtensorMap* tmap_q, const SbrAr
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     gls_sbr_kernel(const __grid_constant__ CUtensorMap tmap_q, const SbrArgs args) {
+  if (gate_closed(args.gate, args.gate_codes)) return;
   constexpr int KO = Cfg::BK / 8;
   constexpr int WO = Cfg::WO;
   constexpr int TW = Cfg::TW;

@@ -45,6 +45,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Slab-path gate (GWG_SNP_AUTO): *word = ~0 when every SNP value of the slab
+// is an integer genotype code (snp_to_i8_kernel), 0 otherwise.  A kernel of
+// one path returns at once when the slab belongs to the other (want_codes =
+// 1: genotype path, 0: FP64 path); word = null means ungated.  Uniform per
+// CTA, checked before any barrier or TMEM setup.
+__device__ __forceinline__ bool gate_closed(const unsigned long long* word, int32_t want_codes) {
+  if (word == nullptr) return false;
+  const bool codes = *reinterpret_cast<const volatile unsigned long long*>(word) == ~0ull;
+  return codes != (want_codes != 0);
+}
+
 // 2-D TMA tile load into shared memory, completing on an mbarrier.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar, uint64_t policy) {

@@ -93,6 +93,8 @@ struct LinArgs {
   int32_t kstages;
   int32_t b_resident;   // sliced operand fits L2: keep it resident
   unsigned long long* err_key;
+  const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
+  int32_t gate_codes = 0;
 };
 
 template <int P, int CL>
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const __grid_constant__ CUtensorMap tmap_w,
                         const __grid_constant__ CUtensorMap tmap_out, const LinArgs a) {
+  if (gate_closed(a.gate, a.gate_codes)) return;
   using L = LinCfg<P, CL>;
   using C = typename L::Tile;
   using CX = CtxLayout<P>;

@@ -39,6 +39,8 @@ struct I8Args {
   int32_t tiles_r;      // ceil(n / 32)
   int32_t kstages;      // kp / 128
   int32_t b_resident;   // sliced operand fits L2: keep it resident
+  const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
+  int32_t gate_codes = 0;
 };
 
 // ---- the rotation kernel -------------------------------------------------------
@@ -53,6 +55,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmap_z,
                      const __grid_constant__ CUtensorMap tmap_d,
                      const __grid_constant__ CUtensorMap tmap_d2, const I8Args a) {
+  if (gate_closed(a.gate, a.gate_codes)) return;
   using C = RotI8Cfg<CL>;
   static_assert(C::ACC_BUFS == 2, "epilogue alternates two accumulator buffers");
   extern __shared__ __align__(1024) unsigned char smem_i8[];

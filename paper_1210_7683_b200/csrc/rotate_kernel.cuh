@@ -54,6 +54,8 @@ struct RotArgs {
   int32_t tiles_m;    // ceil(n / BM)
   int32_t tiles_n;    // ceil(cols / BN)
   int32_t kchunks;    // ceil(n / BK)
+  const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
+  int32_t gate_codes = 0;
 };
 
 __device__ __forceinline__ void rot_issue(const CUtensorMap* tz, const CUtensorMap* tx,
@@ -84,6 +86,7 @@ __device__ __forceinline__ void rot_issue(const CUtensorMap* tz, const CUtensorM
 __global__ void __launch_bounds__(RotCfg::THREADS, 1)
     rotate_kernel(const __grid_constant__ CUtensorMap tmap_z,
                   const __grid_constant__ CUtensorMap tmap_x, const RotArgs a) {
+  if (gate_closed(a.gate, a.gate_codes)) return;
   using C = RotCfg;
   constexpr int KO = C::BK / 8;
   extern __shared__ __align__(1024) double smem[];

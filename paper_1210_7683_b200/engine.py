@@ -161,10 +161,12 @@ class Engine:
         self._call(self._lib.gwg_set_kinship, k.ptr, k.where)
 
     def set_snp_coding(self, coding: str) -> None:
-        """"real" (default: any SNP values, DMMA rotation) or "genotypes"
-        (integer codes in [-127, 127]: exact int8 tcgen05 rotation, values
-        checked on the device) — gwg_set_snp_coding."""
-        code = {"real": nat.GWG_SNP_REAL, "genotypes": nat.GWG_SNP_GENOTYPES}.get(coding)
+        """"auto" (default: per slab, the exact int8 genotype path when every
+        value is an integer code in [-127, 127], else the FP64 path), "real"
+        (any SNP values, DMMA rotation and grid) or "genotypes" (integer codes
+        required, checked on the device) — gwg_set_snp_coding."""
+        code = {"real": nat.GWG_SNP_REAL, "genotypes": nat.GWG_SNP_GENOTYPES,
+                "auto": nat.GWG_SNP_AUTO}.get(coding)
         if code is None:
             raise DimensionError(f"unknown SNP coding {coding!r}")
         self._call(self._lib.gwg_set_snp_coding, code)
@@ -321,7 +323,7 @@ def device_working_set_bytes(n: int, p: int, t: int, mb: int, snp_coding: str = 
     traits = (2 * n * t + 2 * t) * 8 + (-(-t // 8) * 8) * np_ * (p + 1) * 8 + t * (2 * p + p * p // 2) * 8
     per_snp = (2 * n + 2 * np_) * 8 + 2 * t * p * 8
     total = fixed + traits + mb * per_snp
-    if snp_coding == "genotypes":
+    if snp_coding in ("genotypes", "auto"):
         p8 = 1 << max(0, (p - 1).bit_length()) if p <= 8 else -(-p // 8) * 8
         kt = max(1, 32 // p8)
         wrows = -(-t // kt) * kt * p8
@@ -355,7 +357,7 @@ def exp_sum_design(x_min: float, x_max: float, multiple: int = 64,
 def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", workers: int = 1,
                nb: int = 0, mb: int = 0, tb: int = 0, mbb: int = 0, tbb: int = 0,
                double_buffer: bool = True, memory_budget: int | None = None,
-               device: int = 0, device_eig: bool = False, snp_coding: str = "real") -> dict:
+               device: int = 0, device_eig: bool = False, snp_coding: str = "auto") -> dict:
     """Solve the whole m x t grid; returns {'b': (m, t, p), 'counters': dict}.
 
     Same signature and semantics as gwgrid.solve_grid (bindings.cpp:115-190,
@@ -365,8 +367,10 @@ def solve_grid(kinship, xl, snps, traits, h2, sigma2, scheduler: str = "ct", wor
     independent of tiling here as well.  ``mb`` is the streamed SNP slab
     width.  ``memory_budget`` bounds the device working set.  ``device_eig``
     moves the one-off eigendecomposition to the GPU (cuSOLVER); by default it
-    runs on the CPU like the reference.  ``snp_coding="genotypes"`` declares
-    integer-coded SNPs (exact int8 tensor-core rotation, see Engine).
+    runs on the CPU like the reference.  ``snp_coding``: "auto" (default)
+    picks, per slab, the exact int8 tensor-core path when every value is an
+    integer genotype code and the FP64 path otherwise; "genotypes" requires
+    codes, "real" always takes the FP64 path (see Engine.set_snp_coding).
     """
     kinship, xl, snps, traits, h2, sigma2, (n, p, m, t) = _dims_of(
         kinship, xl, snps, traits, h2, sigma2)

@@ -229,3 +229,29 @@ def test_int8_kernel_variants_bitwise_identical(n, p, m, t, monkeypatch):
         out[cl] = run(ds, basis, values, "genotypes")
     assert not np.isnan(out["2"]).any()
     assert np.array_equal(out["1"], out["2"])
+
+
+def test_auto_coding_picks_the_path_per_slab():
+    """GWG_SNP_AUTO (the engine default): a slab of integer codes takes the
+    genotype path, a slab with any other value the FP64 path — both queued,
+    gated on the device check, no error.  Slab by slab the results are those
+    of the explicit coding, bit for bit."""
+    n, p, m, t = 300, 4, 400, 23
+    ds = datagen.generate(n, p, m, t, seed=77)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    snps = ds["snps"].copy()
+    snps[7, 250] += 0.25  # SNP 250 lies in the third 100-column slab
+    ds2 = dict(ds, snps=snps)
+    auto = run(ds2, basis, values, "auto", mb=100)
+    geno = run(ds, basis, values, "genotypes", mb=100)
+    real = run(ds2, basis, values, "real", mb=100)
+    assert not np.isnan(auto).any()
+    assert np.array_equal(auto[:200], geno[:200])
+    assert np.array_equal(auto[300:], geno[300:])
+    assert np.array_equal(auto[200:300], real[200:300])
+    # the default engine coding is auto
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        assert np.array_equal(eng.run_grid(ds["snps"], mb=100), geno)
