@@ -331,6 +331,7 @@ bool rotated_x_unused(const gwg_engine* e) {
 
 void invalidate_derived(gwg_engine* e, bool spectrum) {
   e->split_valid = false;
+  e->expsum_valid = false;
   if (spectrum) {
     e->slices_valid = false;
     e->basis_t_valid = false;
@@ -448,6 +449,14 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
+// E and F for the current traits, once per trait set (both grid paths use them).
+int prepare_expsum(gwg_engine* e, gwg_status* st) {
+  if (e->expsum_valid) return GWG_OK;
+  if (int rc = build_expsum(e, st)) return rc;
+  e->expsum_valid = true;
+  return GWG_OK;
+}
+
 // Trait operands of the split grid: V = [D_j.X_L'_c, D_j.Y'_j] in the padded
 // linear-solve layout, W = Z V by the DMMA rotation kernel against Z^T, 8 int8
 // slices of W per column, and the D panels of gls_sbr_kernel.
@@ -507,26 +516,22 @@ int build_split(gwg_engine* e, gwg_status* st) {
                                                           e->wscale.d());
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
-  if (int rc = build_expsum(e, st)) return rc;
+  if (int rc = prepare_expsum(e, st)) return rc;
   e->split_valid = true;
   return GWG_OK;
 }
 
 // Split grid over one genotype slab: S_BR on DMMA (gls_sbr_kernel), then the
 // exact int8 linear terms + bordered Cholesky (linear_solve_kernel<P>).
-int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
-                 double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
-  if (int rc = build_split(e, st)) return rc;
-  using gwg::I8Cfg;
-  const int64_t t = e->t, p = e->p;
-  const int64_t kp = round_up(e->n, I8Cfg::BK);
-  const int64_t tiles_r = ceil_div(t, e->lops.kt);
-  const int64_t ncols = tiles_r * e->lops.rb;
-  const int64_t ld_s = round_up(rows, 2);
+// S_BR = (X'.X')^T D for one slab into e->sbr ([trait][SNP], ld ld_s):
+// directly against the D panels, or as ((X'.X')^T E) F — two DMMA GEMMs of
+// inner size n and r (expsum.cpp).  Needs the E/F panels (build_expsum) or,
+// when sbr_terms = 0, the D panels (build_split).  Gated like the launches
+// around it (gate_want).
+int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
+                     gwg_status* st) {
+  const int64_t t = e->t;
   GWG_CUDA_TRY(e->sbr.ensure(size_t(ld_s) * t * sizeof(double)));
-
-  // ---- S_BR = (X'.X')^T D: directly, or as ((X'.X')^T E) F (two DMMA GEMMs
-  // of inner size n and r, expsum.cpp) ----
   const gwg::SbrOps& so = e->sops;
   // dst = A^T P: A (kext x rows, ld lda) by TMA, P the D-panel operand with K
   // extent pk (a multiple of bk) over `cols` columns
@@ -552,7 +557,6 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     e->counters.kernel_launches += 1;
     return GWG_OK;
   };
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
   e->counters.sbr_terms = e->sbr_terms;
   e->counters.sbr_flops += uint64_t(rows) * 2ull *
                            (e->sbr_terms ? uint64_t(e->sbr_terms) * uint64_t(e->n + t)
@@ -561,13 +565,24 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     GWG_CUDA_TRY(e->gmat.ensure(size_t(rows) * r * sizeof(double)));
     if (int rc = sbr_gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true))
       return rc;
-    if (int rc = sbr_gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false))
-      return rc;
-  } else {
-    if (int rc =
-            sbr_gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false))
-      return rc;
+    return sbr_gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false);
   }
+  return sbr_gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false);
+}
+
+int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
+                 double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
+  if (int rc = build_split(e, st)) return rc;
+  using gwg::I8Cfg;
+  const int64_t t = e->t, p = e->p;
+  const int64_t kp = round_up(e->n, I8Cfg::BK);
+  const int64_t tiles_r = ceil_div(t, e->lops.kt);
+  const int64_t ncols = tiles_r * e->lops.rb;
+  const int64_t ld_s = round_up(rows, 2);
+
+  // ---- S_BR ----
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
+  if (int rc = launch_sbr_stage(e, rot_sq, rows, ld_s, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_s[1], e->comp));
 
   // ---- linear terms (int8 tcgen05) + solve ----
@@ -669,6 +684,25 @@ int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t
   a.gate_codes = e->gate_want;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_t;
   const int ctas = int(std::min<int64_t>(tiles, e->sms));
+  // S_BR through the factorised D (two DMMA GEMMs on X'.X'), then the grid
+  // kernel without the D column and the X'.X' operand (GridCfg::EXT): 2np
+  // instead of 2n(p+1) flop per cell (GWG_REAL_SPLIT=0 keeps the single
+  // fused kernel).  Measured per step (fused -> split): c1 36.0 -> 32.3 ms,
+  // c3 150 -> 127, c4 297 -> 287, p = 8 32.9 -> 30.7, p = 12 48.4 -> 46.3;
+  // few traits keep the fused kernel (c0, t = 100: 1.26 vs 1.39 ms) — the
+  // choice depends on t only, so results stay bitwise independent of slabs.
+  if (e->real_split && e->lowrank && e->t >= 256) {
+    if (int rc = prepare_expsum(e, st)) return rc;
+    if (e->sbr_terms > 0) {
+      const int64_t ld_s = round_up(rows, 2);
+      if (int rc = launch_sbr_stage(e, rot_sq, rows, ld_s, st)) return rc;
+      a.sbr = e->sbr.d();
+      a.ld_s = ld_s;
+      GWG_CUDA_TRY(e->ops.grid_ext(map, map_sq, a, ctas, e->comp));
+      e->counters.kernel_launches += 1;
+      return GWG_OK;
+    }
+  }
   GWG_CUDA_TRY(e->ops.grid(map, map_sq, a, ctas, e->comp));
   e->counters.kernel_launches += 1;
   return GWG_OK;
@@ -769,6 +803,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   }
   if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
   if (const char* sd = std::getenv("GWG_SBR_DIRECT")) e->lowrank = std::atoi(sd) == 0;
+  if (const char* rs = std::getenv("GWG_REAL_SPLIT")) e->real_split = std::atoi(rs) != 0;
   if (const char* cl = std::getenv("GWG_I8_CLUSTER")) {
     const int v = std::atoi(cl);
     e->i8_cluster = v == 1 || v == 2 ? v : 0;
@@ -927,7 +962,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   if (e->traits_host_valid) {
     e->h2_host.assign(h2, h2 + t);
     e->s2_host.assign(sigma2, sigma2 + t);
-  } else if (e->snp_coding != GWG_SNP_REAL && e->split && e->lowrank) {
+  } else if (e->lowrank && (e->snp_coding == GWG_SNP_REAL ? e->real_split : true)) {
     // queue the exponential sum's range now: by the time the split grid is
     // built the 48-byte answer is on the host and no round trip stalls it
     GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));

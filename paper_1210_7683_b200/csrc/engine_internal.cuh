@@ -109,6 +109,10 @@ struct gwg_engine {
   // GWG_SBR_DIRECT=1 in the environment: `lowrank` = false).
   bool lowrank = true;
   int32_t sbr_terms = 0;
+  bool expsum_valid = false;  // E, F (and sbr_terms) built for the current traits
+  // FP64 path: S_BR from the factorised GEMMs and the grid kernel without the
+  // D column (GWG_REAL_SPLIT=0 in the environment keeps the fused S_BR)
+  bool real_split = true;
   gwg_host::DevBuf epanel, fpanel, gmat, exps;
   // host copies of lambda / h2 / sigma2 when they were passed from the host:
   // the factorisation's range is then found without a device round trip
@@ -157,6 +161,9 @@ constexpr int64_t kMaxGenotypeN = 132000;
 inline const unsigned long long* gate_word(const gwg_engine* e) {
   return e->gate_want >= 0 ? static_cast<const unsigned long long*>(e->err.ptr) + 2 : nullptr;
 }
+int prepare_expsum(gwg_engine* e, gwg_status* st);
+int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
+                     gwg_status* st);
 int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                  int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
                  gwg_status* st);

@@ -71,10 +71,15 @@ struct CtxLayout {
 };
 
 template <int P_, int WM_OCT_, int WARPS_M_, int WARPS_T_, int BK_, int STAGES_,
-          bool PRODUCER_WARP_ = true, int GROUPS_ = 1>
+          bool PRODUCER_WARP_ = true, int GROUPS_ = 1, bool EXT_ = false>
 struct GridCfg {
   static constexpr int P = P_;
-  static constexpr int NC = P + 1;  // operand columns per trait
+  static constexpr int NC = P + 1;  // operand columns per trait in the panels (trait_prep)
+  // EXT: S_BR comes from HBM (the factorised ((X'.X')^T E) F of grid_split.cuh)
+  // instead of the D column against X'.X': the stages hold X' and the first P
+  // panel columns only, and the cell's last accumulator is not computed.
+  static constexpr bool EXT = EXT_;
+  static constexpr int NCS = EXT ? P : P + 1;  // panel columns staged and multiplied
   static constexpr int WM_OCT = WM_OCT_;
   static constexpr int WARPS_M = WARPS_M_;  // per consumer group
   static constexpr int WARPS_T = WARPS_T_;  // per consumer group
@@ -95,10 +100,11 @@ struct GridCfg {
   static constexpr int WARPS = GWARPS * GROUPS;
   static constexpr int THREADS = (WARPS + (PRODUCER_WARP ? GROUPS : 0)) * 32;
   static constexpr int A_STAGE = BK * BM;        // doubles (X' tile; X'.X' tile follows)
-  static constexpr int B_STAGE = BK * NC * BT;   // doubles
-  static constexpr uint32_t A_BYTES = 2 * A_STAGE * 8;
+  static constexpr int B_STAGE = BK * NCS * BT;  // doubles staged
+  static constexpr int B_GSTAGE = BK * NC * BT;  // panel doubles per k-chunk in HBM
+  static constexpr uint32_t A_BYTES = (EXT ? 1 : 2) * A_STAGE * 8;
   static constexpr uint32_t B_BYTES = B_STAGE * 8;
-  static constexpr int SA_STAGE = 2 * A_STAGE;   // smem doubles per stage for A and A.A
+  static constexpr int SA_STAGE = (EXT ? 1 : 2) * A_STAGE;  // smem doubles per stage: A (, A.A)
   static constexpr size_t SMEM_BYTES =
       size_t(GROUPS) * (size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t)) +
       sizeof(uint64_t);
@@ -124,6 +130,8 @@ struct GridArgs {
   int32_t kchunks;      // NP / BK
   int64_t np;           // padded n (multiple of BK)
   unsigned long long* err_key;  // min over failing cells of j*m_total + i
+  const double* sbr = nullptr;  // EXT: S_BR[j * ld_s + i]
+  int64_t ld_s = 0;
   const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
   int32_t gate_codes = 0;
 };
@@ -248,12 +256,21 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* tmap_a, const CUt
   for (int ko = 0; ko < KO; ++ko) {
     tma_load_2d(a_dst + ko * Cfg::BM * 8, tmap_a, (kc * KO + ko) * 8, tm * Cfg::BM, &full[s],
                 pol_a);
-    tma_load_2d(a_dst + Cfg::A_STAGE + ko * Cfg::BM * 8, tmap_q, (kc * KO + ko) * 8,
-                tm * Cfg::BM, &full[s], pol_a);
+    if (!Cfg::EXT)
+      tma_load_2d(a_dst + Cfg::A_STAGE + ko * Cfg::BM * 8, tmap_q, (kc * KO + ko) * 8,
+                  tm * Cfg::BM, &full[s], pol_a);
   }
   const double* bsrc = args.bops + size_t(tt) * size_t(args.np) * Cfg::NC * Cfg::BT +
-                       size_t(kc) * Cfg::B_STAGE;
-  bulk_load(sB + s * Cfg::B_STAGE, bsrc, Cfg::B_BYTES, &full[s], pol_b);
+                       size_t(kc) * Cfg::B_GSTAGE;
+  if (Cfg::EXT) {  // the first P column blocks of every k-octet
+#pragma unroll
+    for (int ko = 0; ko < KO; ++ko)
+      bulk_load(sB + s * Cfg::B_STAGE + ko * Cfg::NCS * Cfg::BT * 8,
+                bsrc + ko * Cfg::NC * Cfg::BT * 8, uint32_t(Cfg::NCS * Cfg::BT * 8 * 8), &full[s],
+                pol_b);
+  } else {
+    bulk_load(sB + s * Cfg::B_STAGE, bsrc, Cfg::B_BYTES, &full[s], pol_b);
+  }
 }
 
 template <class Cfg>
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                     const __grid_constant__ CUtensorMap tmap_q, const GridArgs args) {
   if (gate_closed(args.gate, args.gate_codes)) return;
   constexpr int P = Cfg::P;
-  constexpr int NC = Cfg::NC;
+  constexpr int NC = Cfg::NCS;      // accumulated columns per cell
   constexpr int KO = Cfg::BK / 8;  // k-octets per stage
   constexpr int WO = Cfg::WM_OCT;
   constexpr int G = Cfg::GROUPS;
@@ -361,7 +378,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
         for (int o = 0; o < WO; ++o) {
           af[o] = a2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
-          sq[o] = q2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
+          if (!Cfg::EXT) sq[o] = q2[(ko * (Cfg::BM / 8) + wm * WO + o) * 32 + lane];
         }
         // even-k pass over every accumulator, then the odd-k pass: dependent
         // DMMAs on one accumulator are WO*NC instructions apart.
@@ -369,13 +386,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int o = 0; o < WO; ++o) {
 #pragma unroll
           for (int c = 0; c < P; ++c) dmma(acc[o][c], af[o].x, bf[c].x);
-          dmma(acc[o][P], sq[o].x, bf[P].x);
+          if (!Cfg::EXT) dmma(acc[o][NC - 1], sq[o].x, bf[NC - 1].x);
         }
 #pragma unroll
         for (int o = 0; o < WO; ++o) {
 #pragma unroll
           for (int c = 0; c < P; ++c) dmma(acc[o][c], af[o].y, bf[c].y);
-          dmma(acc[o][P], sq[o].y, bf[P].y);
+          if (!Cfg::EXT) dmma(acc[o][NC - 1], sq[o].y, bf[NC - 1].y);
         }
       }
       __syncwarp();
@@ -394,9 +411,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int o = 0; o < WO; ++o) {
         const int64_t il = int64_t(tm) * Cfg::BM + (wm * WO + o) * 8 + (lane >> 2);
         if (il >= args.rows) continue;
-        double cell[NC];
+        double cell[P + 1];
 #pragma unroll
         for (int c = 0; c < NC; ++c) cell[c] = acc[o][c][e];
+        if (Cfg::EXT) cell[P] = __ldcs(args.sbr + int64_t(j) * args.ld_s + il);
         double beta[P];
 #if GWG_EXPERIMENT == 1
         bool ok = true;

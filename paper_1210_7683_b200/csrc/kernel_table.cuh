@@ -30,6 +30,9 @@ struct KernelOps {
   cudaError_t (*prep)(const PrepArgs&, cudaStream_t) = nullptr;
   cudaError_t (*grid)(const CUtensorMap&, const CUtensorMap&, const GridArgs&, int,
                       cudaStream_t) = nullptr;
+  // the same tiling with S_BR read from HBM (GridCfg::EXT; same panels)
+  cudaError_t (*grid_ext)(const CUtensorMap&, const CUtensorMap&, const GridArgs&, int,
+                          cudaStream_t) = nullptr;
 };
 
 template <class Cfg>
@@ -51,7 +54,7 @@ cudaError_t launch_grid(const CUtensorMap& map, const CUtensorMap& map_sq, const
 #define GWG_PINGPONG_MAXP 12
 #endif
 
-template <int P>
+template <int P, bool EXT = false>
 struct CfgFor {
   static constexpr int LIM = 227 * 1024 - 128;
   // Ping-pong (two 4-warp consumer groups, one producer warp each), p <= 12:
@@ -68,14 +71,19 @@ struct CfgFor {
   static constexpr int WARPS_M = 8 / GROUPS / WARPS_T;
   static constexpr int BM = 8 * WM_OCT * WARPS_M;
   static constexpr int BT = 8 * WARPS_T;
-  static constexpr int stage_bytes(int bk) { return GROUPS * bk * (2 * BM + (P + 1) * BT) * 8; }
+  static constexpr int stage_bytes(int bk, bool ext) {
+    return GROUPS * bk * ((ext ? 1 : 2) * BM + (ext ? P : P + 1) * BT) * 8;
+  }
   static constexpr int MIN_ST = PP ? 2 : 3;
-  // BK = 32 when MIN_ST stages fit, else 16 with as many stages as fit (<= 6)
-  static constexpr int BK = MIN_ST * stage_bytes(32) <= LIM ? 32 : 16;
-  static constexpr int FIT = LIM / stage_bytes(BK);
+  // BK = 32 when MIN_ST stages of the fused kernel fit, else 16, with as
+  // many stages as fit (<= 6); the EXT kernel keeps the fused kernel's BK
+  // (measured: letting its smaller stages pick BK = 32 with 2 stages made
+  // p = 12 78.7 ms instead of 46) and takes the extra stages instead
+  static constexpr int BK = MIN_ST * stage_bytes(32, false) <= LIM ? 32 : 16;
+  static constexpr int FIT = LIM / stage_bytes(BK, EXT);
   static constexpr int STAGES = FIT > 6 ? 6 : FIT;
   using type =
-      GridCfg<P, WM_OCT, WARPS_M, WARPS_T, BK, STAGES, GWG_PRODUCER_WARP, GROUPS>;
+      GridCfg<P, WM_OCT, WARPS_M, WARPS_T, BK, STAGES, GWG_PRODUCER_WARP, GROUPS, EXT>;
 };
 
 template <int P>
@@ -92,6 +100,9 @@ KernelOps make_ops() {
   k.ctx_stride = CtxLayout<P>::STRIDE;
   k.prep = &launch_trait_prep<P, Cfg::BT>;
   k.grid = &launch_grid<Cfg>;
+  using Ext = typename CfgFor<P, true>::type;
+  static_assert(Ext::BM == Cfg::BM && Ext::BT == Cfg::BT, "same tiles and panels");
+  k.grid_ext = &launch_grid<Ext>;
   return k;
 }
 

@@ -255,3 +255,24 @@ def test_auto_coding_picks_the_path_per_slab():
         eng.set_covariates(ds["xl"])
         eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
         assert np.array_equal(eng.run_grid(ds["snps"], mb=100), geno)
+
+
+@pytest.mark.parametrize("p", [1, 4, 12, 20])
+def test_fp64_path_factorised_sbr_matches_fused(p, monkeypatch):
+    """The all-FP64 path with t >= 256 takes S_BR from the factorised GEMMs and
+    runs the grid kernel without the D column (GridCfg::EXT); GWG_REAL_SPLIT=0
+    keeps the single fused kernel.  Same cells to rounding, both against the
+    oracle, and bitwise independent of the slab width."""
+    n, m, t = 200, 150, 300
+    ds = datagen.generate(n, p, m, t, seed=200 + p)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    split = run(ds, basis, values, "real")
+    assert np.array_equal(split, run(ds, basis, values, "real", mb=37))
+    monkeypatch.setenv("GWG_REAL_SPLIT", "0")
+    fused = run(ds, basis, values, "real")
+    rel = np.linalg.norm(split - fused, axis=2) / np.linalg.norm(fused, axis=2)
+    assert rel.max() < 1e-11, rel.max()
+    ii = np.arange(0, m, 7)
+    ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"][:, ii]),
+                           orc.rotate(basis, ds["traits"]), ds["h2"], ds["sigma2"], workers=8)
+    assert_parity(split[ii], ref)
