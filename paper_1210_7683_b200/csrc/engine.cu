@@ -600,10 +600,13 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     auto encode = get_encode();
     const cuuint64_t gdim[2] = {cuuint64_t(t * p), cuuint64_t(rows)};
     const cuuint64_t gstride[1] = {cuuint64_t(use_tma ? out_si * p * 8 : 16)};
-    const cuuint32_t box[2] = {gwg::I8Cfg::OUT_Q, 32};
+    // 16-double swizzled chunks, or one unswizzled {row, 32} box per warp tile
+    const bool tma_row = e->lops.tma_row;
+    const cuuint32_t box[2] = {tma_row ? cuuint32_t(e->lops.row) : gwg::I8Cfg::OUT_Q, 32};
     const cuuint32_t es[2] = {1, 1};
     CUresult r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box,
-                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        tma_row ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (use_tma && r != CUDA_SUCCESS)
       return set_status(st, GWG_CUDA, -1, -1, "tensor map (results) failed (%d)", int(r));

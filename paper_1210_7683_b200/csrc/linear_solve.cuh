@@ -54,15 +54,27 @@ struct LinCfg {
   // stages.  One 4 KB staging tile per epilogue warp.
   static constexpr bool WIDE = P <= LIN_WIDE_MAXP;  // measured: p=4 3.15 -> 2.83 ms, p=12 8.56 -> 7.95
   static constexpr int EPI = WIDE ? 16 : 8;
-  using Tile = I8Tile<RB, WIDE ? 3 : 4, 1, EPI, CL>;
-  static constexpr int ACC = Tile::ACC_BUFS;
+  static constexpr int ACC = 2;                           // TMEM accumulator buffers
   static constexpr int HMAX = EPI / 4 / ACC;              // warps per quarter and buffer
   static constexpr int HALVES = KT >= HMAX ? HMAX : 1;    // warps splitting one tile
   static constexpr int CELLS = KT / HALVES;               // cells per warp per tile
   static constexpr int CW = P8 < 8 ? P8 : 8;              // TMEM columns per load
   static constexpr int ROW = CELLS * P;                   // results per warp row per tile
-  static constexpr int CHUNK = Tile::OUT_Q;               // doubles per TMA store row (128 B)
+  static constexpr int CHUNK = 16;                        // doubles per swizzled TMA row (128 B)
   static constexpr bool TMA_OUT = ROW % CHUNK == 0;       // whole 128-byte chunks
+  // other even rows of <= 32 doubles leave through one unswizzled TMA box
+  // {ROW, 32} per warp and tile (direct stores cost p = 12 2.8 of 7.8 ms and
+  // c4 8.7 of 37.9 ms); rows above 16 doubles need an 8 KB staging tile
+  static constexpr bool TMA_ROW = !TMA_OUT && ROW % 2 == 0 && ROW <= 32;
+  static constexpr int OUT_BUFS = TMA_ROW && ROW * 8 * 32 > 4096 ? 2 : 1;
+  static constexpr int STAGES_0 = WIDE ? 3 : 4;
+  static constexpr uint32_t STAGE_B = 128 * 128 + 8 * RB * 128;
+  static constexpr int STAGES =
+      size_t(STAGES_0) * STAGE_B + size_t(EPI) * OUT_BUFS * 4096 + 1280 <= 227 * 1024
+          ? STAGES_0
+          : STAGES_0 - 1;
+  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL>;
+  static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
@@ -286,6 +298,24 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
                                tm * C::BM + qd * 32);
               }
             }
+        } else if (L::TMA_ROW && a.use_tma) {
+          // the warp's ROW results per SNP row, unswizzled [lane][ROW] in the
+          // staging tile, one TMA box {ROW, 32} after the tile's last group
+          if (g0 == 0) {
+            if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
+            __syncwarp();
+          }
+          double* row = reinterpret_cast<double*>(stg) + lane * L::ROW;
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) row[(g0 + u) * P + c] = beta[u][c];
+          if (g0 + L::GROUP >= L::CELLS) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0)
+              tma_store_2d(&tmap_out, stg, (j0 + cell0) * P, tm * C::BM + qd * 32);
+          }
         } else if (iv) {
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u) {
@@ -320,6 +350,8 @@ struct LinOps {
   cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                            const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
   int b_slices_box[2] = {8, 4};  // slice slots per TMA box
+  int row = 0;           // results per warp row per tile (LinCfg::ROW)
+  bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
 };
 
 template <int P>
@@ -330,6 +362,8 @@ LinOps make_lin_ops() {
   o.rb = LinCfg<P>::RB;
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
+  o.row = LinCfg<P>::ROW;
+  o.tma_row = LinCfg<P>::TMA_ROW;
   return o;
 }
 
