@@ -147,10 +147,11 @@ int64_t raw_ld(const gwg_engine* e) { return (e->n % 2 == 0) ? e->n : e->np; }
 // dst (n x cols, ld np) = Z^T src (n x cols, ld lds) with the deterministic
 // DMMA rotation kernel (rotate_kernel.cuh).
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds, double* dst_sq, const double* basis) {
+           int64_t lds, double* dst_sq, const double* basis, int64_t ldd) {
   if (cols <= 0) return GWG_OK;
   NvtxRange nvtx_("rotate");
   if (lds == 0) lds = e->np;
+  if (ldd == 0) ldd = e->np;
   CUtensorMap tz, tx;
   if (!basis) basis = e->basis.d();
   if (int rc = encode_kmajor(&tz, basis, e->n, e->n, e->np, gwg::RotCfg::BM, st)) return rc;
@@ -158,7 +159,7 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
   gwg::RotArgs a;
   a.dst = dst;
   a.dst_sq = dst_sq;
-  a.ldd = e->np;
+  a.ldd = ldd;
   a.n = int32_t(e->n);
   a.cols = int32_t(cols);
   a.tiles_m = int32_t(ceil_div(e->n, gwg::RotCfg::BM));
@@ -438,6 +439,7 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   a.s = dx + 8;
   a.w = dx + 8 + r;
   a.lam0 = rg[0];
+  e->ex_lam0 = rg[0];
   a.epanel = e->epanel.d();
   a.fpanel = e->fpanel.d();
   gwg::expsum_e_kernel<<<r, 256, 0, e->comp>>>(a);
@@ -506,8 +508,51 @@ int build_split(gwg_engine* e, gwg_status* st) {
   gwg::split_prep_kernel<<<int(t), 256, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
-  if (int rc = rotate(e, e->vmat.d(), ncols, e->wmat.d(), st, np, nullptr, e->basis_t.d()))
-    return rc;
+  if (int rc = prepare_expsum(e, st)) return rc;
+  if (e->sbr_terms > 0 && p > 1) {
+    // W through the factorisation D = E F: the covariate columns
+    // W_{j,c} = Z (D_j . X_L'_c) = (Z diag(X_L'_c) E) F_j — one GEMM of inner
+    // size n for all c (U = Z [diag(X_L'_c) E]_c, n x r (p-1)), then one of
+    // inner size r per c straight into W's padded rows j * p8 + c — instead of
+    // rotating t (p-1) columns (n^2 per column); non-negative E and F give the
+    // same error bound as Z (D_j . X_L'_c).  The trait column W_{j,p-1} =
+    // Z (D_j . Y'_j) is rotated as before.
+    const int64_t r = e->sbr_terms, rc_cols = r * (p - 1), p8 = e->lops.p8;
+    GWG_CUDA_TRY(cudaMemsetAsync(e->wmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
+    if (int rc = rotate(e, e->vmat.d() + (p - 1) * np, t, e->wmat.d() + (p - 1) * np, st,
+                        p8 * np, nullptr, e->basis_t.d(), p8 * np))
+      return rc;
+    GWG_CUDA_TRY(e->xepanel.ensure(size_t(np) * rc_cols * sizeof(double)));
+    GWG_CUDA_TRY(e->umat.ensure(size_t(n) * rc_cols * sizeof(double)));
+    gwg::ExpSumArgs x;
+    x.n = n;
+    x.np = np;
+    x.t = int32_t(t);
+    x.r = int32_t(r);
+    x.bt = int32_t(e->sops.bt);
+    x.lambda = e->lambda.d();
+    x.s = e->exps.d() + 8;
+    x.w = e->exps.d() + 8 + r;
+    x.lam0 = e->ex_lam0;
+    x.xmul = e->xl_rot.d();
+    x.ldx = np;
+    x.ncx = int32_t(p - 1);
+    x.panel_out = e->xepanel.d();
+    gwg::expsum_e_kernel<<<int(rc_cols), 256, 0, e->comp>>>(x);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    // U[k][(c, q)] = sum_l Z[k][l] x_c[l] E[l][q]  (A = Z^T's columns = Z's rows)
+    if (int rc = sbr_gemm(e, e->basis_t.d(), n, np, n, e->xepanel.d(), np, rc_cols,
+                          e->umat.d(), rc_cols, true, st))
+      return rc;
+    for (int64_t c = 0; c + 1 < p; ++c)  // W[(j p8 + c) np + k] = sum_q U[k][(c, q)] F[q][j]
+      if (int rc = sbr_gemm(e, e->umat.d() + c * r, r, rc_cols, n, e->fpanel.d(), r, t,
+                            e->wmat.d() + c * np, p8 * np, false, st))
+        return rc;
+  } else {
+    if (int rc = rotate(e, e->vmat.d(), ncols, e->wmat.d(), st, np, nullptr, e->basis_t.d()))
+      return rc;
+  }
   GWG_CUDA_TRY(e->wslices.ensure(size_t(I8Cfg::SLICES) * ncols * kp));
   GWG_CUDA_TRY(e->wscale.ensure(size_t(ncols) * sizeof(double)));
   gwg::slice_basis_kernel<<<int(ncols), 256, 0, e->comp>>>(e->wmat.d(), np, int32_t(n),
@@ -516,7 +561,6 @@ int build_split(gwg_engine* e, gwg_status* st) {
                                                           e->wscale.d());
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
-  if (int rc = prepare_expsum(e, st)) return rc;
   e->split_valid = true;
   return GWG_OK;
 }
@@ -528,34 +572,42 @@ int build_split(gwg_engine* e, gwg_status* st) {
 // inner size n and r (expsum.cpp).  Needs the E/F panels (build_expsum) or,
 // when sbr_terms = 0, the D panels (build_split).  Gated like the launches
 // around it (gate_want).
+// One gls_sbr_kernel GEMM: dst = A^T P with A (kext x rows, ld lda, read by
+// TMA) and P a D-panel operand of K extent pk (a multiple of bk) over `cols`
+// columns; dst[j * ldd + i], or dst[i * ldd + j] (rowmajor).  Gated like
+// the launches around it (gate_want).
+int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
+             const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
+             bool rowmajor, gwg_status* st) {
+  const gwg::SbrOps& so = e->sops;
+  CUtensorMap map;
+  if (int rc = encode_kmajor(&map, a_op, kext, rows, lda, so.bm, st)) return rc;
+  gwg::SbrArgs q;
+  q.dpanel = panel;
+  q.sbr = dst;
+  q.ld = ldd;
+  q.rows = rows;
+  q.t = int32_t(cols);
+  q.tiles_m = int32_t(ceil_div(rows, so.bm));
+  q.tiles_t = int32_t(ceil_div(cols, so.bt));
+  q.kchunks = int32_t(pk / so.bk);
+  q.np = pk;
+  q.rowmajor = rowmajor ? 1 : 0;
+  q.gate = gate_word(e);
+  q.gate_codes = e->gate_want;
+  const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
+  GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
+  e->counters.kernel_launches += 1;
+  return GWG_OK;
+}
+
 int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
                      gwg_status* st) {
   const int64_t t = e->t;
   GWG_CUDA_TRY(e->sbr.ensure(size_t(ld_s) * t * sizeof(double)));
-  const gwg::SbrOps& so = e->sops;
-  // dst = A^T P: A (kext x rows, ld lda) by TMA, P the D-panel operand with K
-  // extent pk (a multiple of bk) over `cols` columns
-  auto sbr_gemm = [&](const double* a_op, int64_t kext, int64_t lda, const double* panel,
-                      int64_t pk, int64_t cols, double* dst, int64_t ldd, bool rowmajor) -> int {
-    CUtensorMap map;
-    if (int rc = encode_kmajor(&map, a_op, kext, rows, lda, so.bm, st)) return rc;
-    gwg::SbrArgs q;
-    q.dpanel = panel;
-    q.sbr = dst;
-    q.ld = ldd;
-    q.rows = rows;
-    q.t = int32_t(cols);
-    q.tiles_m = int32_t(ceil_div(rows, so.bm));
-    q.tiles_t = int32_t(ceil_div(cols, so.bt));
-    q.kchunks = int32_t(pk / so.bk);
-    q.np = pk;
-    q.rowmajor = rowmajor ? 1 : 0;
-    q.gate = gate_word(e);
-    q.gate_codes = e->gate_want;
-    const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
-    GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
-    e->counters.kernel_launches += 1;
-    return GWG_OK;
+  auto gemm = [&](const double* a_op, int64_t kext, int64_t lda, const double* panel,
+                  int64_t pk, int64_t cols, double* dst, int64_t ldd, bool rowmajor) {
+    return sbr_gemm(e, a_op, kext, lda, rows, panel, pk, cols, dst, ldd, rowmajor, st);
   };
   e->counters.sbr_terms = e->sbr_terms;
   e->counters.sbr_flops += uint64_t(rows) * 2ull *
@@ -563,11 +615,11 @@ int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t 
                                          : uint64_t(e->n) * uint64_t(t));
   if (const int64_t r = e->sbr_terms) {
     GWG_CUDA_TRY(e->gmat.ensure(size_t(rows) * r * sizeof(double)));
-    if (int rc = sbr_gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true))
+    if (int rc = gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true))
       return rc;
-    return sbr_gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false);
+    return gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false);
   }
-  return sbr_gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false);
+  return gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false);
 }
 
 int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
@@ -864,7 +916,7 @@ void gwg_engine_destroy(gwg_engine* e) {
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
                     &e->wslices, &e->wscale, &e->dpanel, &e->sbr, &e->epanel, &e->fpanel,
-                    &e->gmat, &e->exps})
+                    &e->gmat, &e->exps, &e->xepanel, &e->umat})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   if (e->range_host) cudaFreeHost(e->range_host);

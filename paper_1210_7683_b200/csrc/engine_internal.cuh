@@ -114,6 +114,7 @@ struct gwg_engine {
   // D column (GWG_REAL_SPLIT=0 in the environment keeps the fused S_BR)
   bool real_split = true;
   gwg_host::DevBuf epanel, fpanel, gmat, exps;
+  gwg_host::DevBuf xepanel, umat;  // W build through the factorisation: diag(X_L'_c) E, Z diag(X_L'_c) E
   // host copies of lambda / h2 / sigma2 when they were passed from the host:
   // the factorisation's range is then found without a device round trip
   std::vector<double> h2_host, s2_host;
@@ -127,7 +128,7 @@ struct gwg_engine {
   double lam_lo = 0.0, lam_hi = 0.0;
   bool lam_bad = false;
   // the nodes on the device (exps + 8) were designed for this range
-  double ex_lo = 0.0, ex_hi = -1.0;
+  double ex_lo = 0.0, ex_hi = -1.0, ex_lam0 = 0.0;
   int32_t ex_mult = 0, ex_r = 0;
   unsigned long long* err_host = nullptr;
 
@@ -150,7 +151,8 @@ int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int6
                 int where, cudaStream_t s, gwg_status* st, int64_t ldd = 0);
 int64_t raw_ld(const gwg_engine* e);
 int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_status* st,
-           int64_t lds = 0, double* dst_sq = nullptr, const double* basis = nullptr);
+           int64_t lds = 0, double* dst_sq = nullptr, const double* basis = nullptr,
+           int64_t ldd = 0);
 // Split-grid trait operands (W slices, D panels) for the current traits.
 int build_split(gwg_engine* e, gwg_status* st);
 // Genotype split grid on raw slabs: X' is never materialised (only X'.X').
@@ -162,6 +164,9 @@ inline const unsigned long long* gate_word(const gwg_engine* e) {
   return e->gate_want >= 0 ? static_cast<const unsigned long long*>(e->err.ptr) + 2 : nullptr;
 }
 int prepare_expsum(gwg_engine* e, gwg_status* st);
+int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
+             const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
+             bool rowmajor, gwg_status* st);
 int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
                      gwg_status* st);
 int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,

@@ -137,6 +137,12 @@ struct ExpSumArgs {
   double lam0;          // min lambda
   double* epanel;       // E[k][r] = exp(-s_r (lambda_k - lam0)) as D panels over r
   double* fpanel;       // F[r][j] = w_r exp(-s_r (lam0 + gamma_j)) / (sigma2_j h_j)
+  // expsum_e_kernel with xmul: columns c * r + q of panel_out (ld ldx per c)
+  // hold x_c[k] E[k][q] for c < ncx (the W build's diag(X_L'_c) E)
+  const double* xmul = nullptr;
+  int64_t ldx = 0;
+  int32_t ncx = 0;
+  double* panel_out = nullptr;
 };
 
 // D-panel index ([tile][k/8][column octet][column%8][k%8]) of (k, column c).
@@ -156,12 +162,19 @@ __device__ __forceinline__ double exp_neg_prod(double s, double x) {
 }
 
 // One CTA per term r: column r of E, the K operand of GEMM 1 (K = eigen-rows).
+// With xmul: one CTA per (c, r), column c * r + q of panel_out = x_c . E_q.
 __global__ void __launch_bounds__(256) expsum_e_kernel(const ExpSumArgs a) {
-  const int r = blockIdx.x;
-  const double s = a.s[r];
-  for (int64_t k = threadIdx.x; k < a.np; k += blockDim.x)
-    a.epanel[panel_index(k, r, a.bt, a.np)] =
-        k < a.n ? exp_neg_prod(s, a.lambda[k] - a.lam0) : 0.0;
+  const int col = blockIdx.x;
+  const int q = a.xmul ? col % a.r : col;
+  const int c = a.xmul ? col / a.r : 0;
+  const double s = a.s[q];
+  double* out = a.xmul ? a.panel_out : a.epanel;
+  const double* x = a.xmul ? a.xmul + int64_t(c) * a.ldx : nullptr;
+  for (int64_t k = threadIdx.x; k < a.np; k += blockDim.x) {
+    double v = k < a.n ? exp_neg_prod(s, a.lambda[k] - a.lam0) : 0.0;
+    if (x) v = k < a.n ? v * x[k] : 0.0;
+    out[panel_index(k, col, a.bt, a.np)] = v;
+  }
 }
 
 // One CTA per trait j: column j of F, the K operand of GEMM 2 (K = terms).
