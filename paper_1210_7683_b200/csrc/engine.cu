@@ -477,15 +477,19 @@ int build_split(gwg_engine* e, gwg_status* st) {
     e->counters.kernel_launches += 1;
     e->basis_t_valid = true;
   }
+  if (int rc = prepare_expsum(e, st)) return rc;
+  // factorised D: only the trait columns of V are rotated, no D panels
+  const bool fact = e->sbr_terms > 0 && p > 1;
+  const bool padded = e->lops.p8 != p || t % e->lops.kt;  // W has padding rows
   const int64_t bt = e->sops.bt;
   const int64_t tiles_t = ceil_div(t, bt);
   GWG_CUDA_TRY(e->dpanel.ensure(size_t(tiles_t) * np * bt * sizeof(double)));
-  if (t % bt)  // padded traits of the last tile contribute zeros
+  if (t % bt && !fact)  // padded traits of the last tile contribute zeros
     GWG_CUDA_TRY(cudaMemsetAsync(e->dpanel.d() + size_t(tiles_t - 1) * np * bt, 0,
                                  size_t(np) * bt * sizeof(double), e->comp));
   GWG_CUDA_TRY(e->vmat.ensure(size_t(np) * ncols * sizeof(double)));
   GWG_CUDA_TRY(e->wmat.ensure(size_t(np) * ncols * sizeof(double)));
-  if (e->lops.p8 != p || t % e->lops.kt)
+  if (padded && !fact)
     GWG_CUDA_TRY(cudaMemsetAsync(e->vmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
   gwg::SplitPrepArgs a;
   a.n = n;
@@ -505,11 +509,11 @@ int build_split(gwg_engine* e, gwg_status* st) {
   a.sigma2 = e->sigma2.d();
   a.dpanel = e->dpanel.d();
   a.v = e->vmat.d();
+  a.y_only = fact ? 1 : 0;
   gwg::split_prep_kernel<<<int(t), 256, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
-  if (int rc = prepare_expsum(e, st)) return rc;
-  if (e->sbr_terms > 0 && p > 1) {
+  if (fact) {
     // W through the factorisation D = E F: the covariate columns
     // W_{j,c} = Z (D_j . X_L'_c) = (Z diag(X_L'_c) E) F_j — one GEMM of inner
     // size n for all c (U = Z [diag(X_L'_c) E]_c, n x r (p-1)), then one of
@@ -518,7 +522,8 @@ int build_split(gwg_engine* e, gwg_status* st) {
     // same error bound as Z (D_j . X_L'_c).  The trait column W_{j,p-1} =
     // Z (D_j . Y'_j) is rotated as before.
     const int64_t r = e->sbr_terms, rc_cols = r * (p - 1), p8 = e->lops.p8;
-    GWG_CUDA_TRY(cudaMemsetAsync(e->wmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
+    if (padded)  // padding rows (c >= p, traits past t) stay zero
+      GWG_CUDA_TRY(cudaMemsetAsync(e->wmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
     if (int rc = rotate(e, e->vmat.d() + (p - 1) * np, t, e->wmat.d() + (p - 1) * np, st,
                         p8 * np, nullptr, e->basis_t.d(), p8 * np))
       return rc;

@@ -28,6 +28,7 @@ struct SplitPrepArgs {
   double* dpanel;       // D panels for gls_sbr_kernel
   double* v;            // columns D.X_L'_c, D.Y'_j (ld np) at (j/kt)*rb + (j%kt)*p8 + c;
                         // padding columns are zeroed by the caller
+  int32_t y_only = 0;   // factorised W build: only the D.Y'_j columns, no D panels
 };
 
 // One CTA per trait: D_j = 1 / (sigma2 (h2 lambda + 1 - h2)) exactly as
@@ -43,8 +44,10 @@ __global__ void __launch_bounds__(256) split_prep_kernel(const SplitPrepArgs a) 
   for (int64_t k = threadIdx.x; k < a.np; k += blockDim.x) {
     const bool in = k < a.n;
     const double dinv = in ? 1.0 / (s2 * (h2 * a.lambda[k] + omh)) : 0.0;
-    panel[(k >> 3) * (int64_t(a.bt) * 8) + (k & 7)] = dinv;
-    for (int c = 0; c + 1 < a.p; ++c) v[c * a.np + k] = in ? dinv * a.xl[k + c * a.ldxl] : 0.0;
+    if (!a.y_only) {
+      panel[(k >> 3) * (int64_t(a.bt) * 8) + (k & 7)] = dinv;
+      for (int c = 0; c + 1 < a.p; ++c) v[c * a.np + k] = in ? dinv * a.xl[k + c * a.ldxl] : 0.0;
+    }
     v[(a.p - 1) * a.np + k] = in ? dinv * y[k] : 0.0;
   }
 }
