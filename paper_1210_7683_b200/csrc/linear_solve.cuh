@@ -65,8 +65,11 @@ struct LinCfg {
   // other even rows of <= 32 doubles leave through one unswizzled TMA box
   // {ROW, 32} per warp and tile (direct stores cost p = 12 2.8 of 7.8 ms and
   // c4 8.7 of 37.9 ms); rows above 16 doubles need an 8 KB staging tile
-  static constexpr bool TMA_ROW = !TMA_OUT && ROW % 2 == 0 && ROW <= 32;
-  static constexpr int OUT_BUFS = TMA_ROW && ROW * 8 * 32 > 4096 ? 2 : 1;
+  // (an odd row's last double is stored directly: a box row is a multiple of
+  // 16 bytes)
+  static constexpr bool TMA_ROW = !TMA_OUT && ROW >= 2 && ROW <= 33;
+  static constexpr int BW = ROW & ~1;                     // doubles per TMA box row
+  static constexpr int OUT_BUFS = TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
   static constexpr int STAGES_0 = WIDE ? 3 : 4;
   static constexpr uint32_t STAGE_B = 128 * 128 + 8 * RB * 128;
   static constexpr int STAGES =
@@ -305,16 +308,28 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
             __syncwarp();
           }
-          double* row = reinterpret_cast<double*>(stg) + lane * L::ROW;
+          // an odd row keeps one double out of the box: the last one when the
+          // row starts 16-byte aligned, else the first (the box start must be)
+          const int shift = (L::ROW & 1) ? (((j0 + cell0) * P) & 1) : 0;
+          double* row = reinterpret_cast<double*>(stg) + lane * L::BW;
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u)
 #pragma unroll
-            for (int c = 0; c < P; ++c) row[(g0 + u) * P + c] = beta[u][c];
+            for (int c = 0; c < P; ++c) {
+              const int f = (g0 + u) * P + c - shift;
+              if (f >= 0 && f < L::BW) {
+                row[f] = beta[u][c];
+              } else if (iv && j0 + cell0 + g0 + u < a.t) {  // odd row: the double left out
+                st_evict_first(
+                    a.out + (il * a.out_si + int64_t(j0 + cell0 + g0 + u) * a.out_sj) * P + c,
+                    beta[u][c], pol_out);
+              }
+            }
           if (g0 + L::GROUP >= L::CELLS) {
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0)
-              tma_store_2d(&tmap_out, stg, (j0 + cell0) * P, tm * C::BM + qd * 32);
+              tma_store_2d(&tmap_out, stg, (j0 + cell0) * P + shift, tm * C::BM + qd * 32);
           }
         } else if (iv) {
 #pragma unroll
@@ -350,7 +365,7 @@ struct LinOps {
   cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                            const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
   int b_slices_box[2] = {8, 4};  // slice slots per TMA box
-  int row = 0;           // results per warp row per tile (LinCfg::ROW)
+  int row = 0;           // doubles per TMA box row (LinCfg::BW)
   bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
 };
 
@@ -362,7 +377,7 @@ LinOps make_lin_ops() {
   o.rb = LinCfg<P>::RB;
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
-  o.row = LinCfg<P>::ROW;
+  o.row = LinCfg<P>::BW;
   o.tma_row = LinCfg<P>::TMA_ROW;
   return o;
 }

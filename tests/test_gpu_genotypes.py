@@ -276,3 +276,21 @@ def test_fp64_path_factorised_sbr_matches_fused(p, monkeypatch):
     ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"][:, ii]),
                            orc.rotate(basis, ds["traits"]), ds["h2"], ds["sigma2"], workers=8)
     assert_parity(split[ii], ref)
+
+
+@pytest.mark.parametrize("p", [3, 9, 12, 13, 21])
+def test_split_grid_tma_row_stores(p):
+    """Result rows that are not whole 128-byte chunks leave through one
+    unswizzled TMA box per warp tile (odd rows keep their first or last
+    double out of the box, whichever keeps the box start 16-byte aligned);
+    t even makes the numpy layout TMA-storable.  Against the FP64 path and
+    the stream layout's direct stores."""
+    n, m, t = 150, 300, 20
+    ds = datagen.generate(n, p, m, t, seed=300 + p)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    bg = run(ds, basis, values, "genotypes")
+    br = run(ds, basis, values, "real")
+    rel = np.linalg.norm(bg - br, axis=2) / np.linalg.norm(br, axis=2)
+    assert not np.isnan(bg).any() and rel.max() < 1e-10, rel.max()
+    bs = run(ds, basis, values, "genotypes", layout="stream", mb=64)
+    assert np.array_equal(bs.transpose(1, 0, 2), bg)

@@ -21,9 +21,10 @@ from paper_1210_7683_b200 import datagen  # noqa: E402
 
 PEAK = 37.15
 SLAB = {"c0": 10_000, "c1": 100_000, "c2": 100_000, "c3": 4_736, "c4": 50_000,
-        "p8": 50_000, "p12": 50_000}
+        "p8": 50_000, "p12": 50_000, "p13": 50_000}
 EXTRA = {"p8": datagen.GridConfig("p8", 1000, 8, 50_000, 1000, 2000),
-         "p12": datagen.GridConfig("p12", 1000, 12, 50_000, 1000, 2000)}
+         "p12": datagen.GridConfig("p12", 1000, 12, 50_000, 1000, 2000),
+         "p13": datagen.GridConfig("p13", 1000, 13, 50_000, 1000, 2000)}
 
 
 def run(name, steps):
