@@ -722,6 +722,13 @@ int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t 
 int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                  int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
                  gwg_status* st) {
+  if (!e->bops_valid) {  // the panels gwg_set_traits skipped (contexts are rebuilt alike)
+    gwg::PrepArgs pa = e->prep_args;
+    pa.panels = 1;
+    GWG_CUDA_TRY(e->ops.prep(pa, e->comp));
+    e->counters.kernel_launches += 1;
+    e->bops_valid = true;
+  }
   CUtensorMap map, map_sq;
   if (int rc = encode_kmajor(&map, rot, e->n, rows, e->np, e->ops.bm, st)) return rc;
   if (int rc = encode_kmajor(&map_sq, rot_sq, e->n, rows, e->np, e->ops.bm, st)) return rc;
@@ -1059,6 +1066,12 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   a.bops = e->bops.d();
   a.ctx = e->ctx.d();
   a.trait_err = static_cast<unsigned long long*>(e->err.ptr);
+  // explicit genotype coding with the split grid never reads the FP64 grid's
+  // operand panels unless a pre-rotated slab arrives: built on demand then
+  // (launch_fused)
+  a.panels = (e->snp_coding == GWG_SNP_GENOTYPES && e->split) ? 0 : 1;
+  e->bops_valid = a.panels != 0;
+  e->prep_args = a;
   GWG_CUDA_TRY(e->ops.prep(a, e->comp));
   e->counters.kernel_launches += 1;
   e->counters.context_builds += 1;

@@ -79,6 +79,8 @@ struct gwg_engine {
   int64_t t = 0;
   bool have_traits = false;
   gwg_host::DevBuf y_raw, y_rot, h2, sigma2, bops, ctx;
+  bool bops_valid = false;  // bops built for the current traits
+  gwg::PrepArgs prep_args{};  // the last trait prep (rerun with panels on demand)
 
   gwg_host::DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
   gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key, [2] genotype check

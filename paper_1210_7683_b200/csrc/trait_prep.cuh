@@ -32,6 +32,7 @@ struct PrepArgs {
   double* bops;
   double* ctx;
   unsigned long long* trait_err;  // min j whose weights fail the floor
+  int32_t panels = 1;             // write the FP64 grid's operand panels (bops)
 };
 
 template <int NV>
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(256) trait_prep_kernel(const PrepArgs a) {
       if (!(d > floor_)) bad_s = 1;
       dinv = 1.0 / d;
     }
+    if (!a.panels) continue;
     double* dst = panel + (k >> 3) * (NC * BT * 8) + (k & 7);
 #pragma unroll
     for (int c = 0; c < P1; ++c) dst[c * BT * 8] = k < a.n ? dinv * a.xl[k + c * a.ldxl] : 0.0;

@@ -294,3 +294,23 @@ def test_split_grid_tma_row_stores(p):
     assert not np.isnan(bg).any() and rel.max() < 1e-10, rel.max()
     bs = run(ds, basis, values, "genotypes", layout="stream", mb=64)
     assert np.array_equal(bs.transpose(1, 0, 2), bg)
+
+
+def test_genotype_coding_prerotated_slab_builds_panels_on_demand():
+    """Explicit genotype coding skips the FP64 grid's operand panels at
+    gwg_set_traits; a pre-rotated slab (always the FP64 path) builds them on
+    demand and gets the FP64 path's result."""
+    n, p, m, t = 160, 4, 90, 12
+    ds = datagen.generate(n, p, m, t, seed=91)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    xr = np.asfortranarray(basis.T @ ds["snps"])
+    out = {}
+    for coding in ("genotypes", "real"):
+        with gw.Engine(n, p) as eng:
+            eng.set_spectrum(basis, values)
+            eng.set_covariates(ds["xl"])
+            eng.set_snp_coding(coding)
+            eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+            out[coding] = eng.solve_snp_slab(xr, rotated=True)
+    assert not np.isnan(out["genotypes"]).any()
+    assert np.array_equal(out["genotypes"], out["real"])
