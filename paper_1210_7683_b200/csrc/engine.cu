@@ -478,8 +478,11 @@ int build_split(gwg_engine* e, gwg_status* st) {
     e->basis_t_valid = true;
   }
   if (int rc = prepare_expsum(e, st)) return rc;
-  // factorised D: only the trait columns of V are rotated, no D panels
-  const bool fact = e->sbr_terms > 0 && p > 1;
+  // factorised D: only the trait columns of V are rotated, no D panels (for
+  // t >= 256: with few traits the small GEMMs cost more than the rotation,
+  // c0 0.60 vs 0.71 ms; the choice depends on t only, results stay
+  // slab-invariant)
+  const bool fact = e->sbr_terms > 0 && p > 1 && t >= 256;
   const bool padded = e->lops.p8 != p || t % e->lops.kt;  // W has padding rows
   const int64_t bt = e->sops.bt;
   const int64_t tiles_t = ceil_div(t, bt);
