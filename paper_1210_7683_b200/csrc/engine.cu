@@ -193,14 +193,15 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
 // 2-D uint8 map over a K-major int8 operand (kp x cols) and 3-D map over
 // SLICES planes of (kp x ncols), both SWIZZLE_128B boxes for tcgen05.
 int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensorMap* tb,
-              const void* slices, int64_t ncols, int rb, int slices_box, gwg_status* st) {
+              const void* slices, int64_t ncols, int rb, int slices_box, gwg_status* st,
+              int a_rows) {
   using gwg::I8Cfg;
   auto encode = get_encode();
   if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
   {
     const cuuint64_t gdim[2] = {cuuint64_t(kp), cuuint64_t(cols)};
     const cuuint64_t gstride[1] = {cuuint64_t(kp)};
-    const cuuint32_t box[2] = {I8Cfg::BK, I8Cfg::BM};
+    const cuuint32_t box[2] = {I8Cfg::BK, cuuint32_t(a_rows)};
     const cuuint32_t es[2] = {1, 1};
     CUresult r = encode(tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(x), gdim, gstride,
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -261,10 +262,10 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   a.gate_codes = e->gate_want;
   // CTA pairs multicasting the B (Z-slice) tile when it streams from HBM
   // (measured at n = 10,000: 69.2 -> 49.0 ms; neutral at n = 1000)
-  const int cl = e->i8_cluster ? e->i8_cluster : (e->n >= 4096 ? 2 : 1);
+  const int cl = e->i8_cluster ? (e->i8_cluster == 3 ? 2 : e->i8_cluster) : (e->n >= 4096 ? 2 : 1);
   CUtensorMap tx, tb;
   if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB,
-                         I8Cfg::SLOTS / cl, st))
+                         I8Cfg::SLOTS / cl, st, I8Cfg::BM))
     return rc;
   const int64_t units = int64_t((a.tiles_m + cl - 1) / cl) * a.tiles_r;
   if (cl == 2)
@@ -647,11 +648,15 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
 
   // ---- linear terms (int8 tcgen05) + solve ----
   // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
-  // c2 22.5 -> 20.9, c4 43.1 -> 40.4; GWG_I8_CLUSTER=1 forces single CTAs)
+  // c2 22.5 -> 20.9, c4 43.1 -> 40.4).  GWG_I8_CLUSTER=1|2|3 forces single
+  // CTAs / these B pairs / pairs on two W tiles multicasting the SNP tile —
+  // the last measured slower even with one or two traits per tile (c4 33.2
+  // -> 35.6 ms, p = 12 5.25 -> 5.62), so the SNP tile's L2 traffic is not
+  // what bounds those configs.
   const int cl = e->i8_cluster ? e->i8_cluster : 2;
   CUtensorMap tx, tw, tout;
   if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb,
-                         e->lops.b_slices_box[cl - 1], st))
+                         e->lops.b_slices_box[cl - 1], st, e->lops.a_box_rows[cl - 1]))
     return rc;
   // numpy layout with a 16-byte pitch and base: results leave by TMA store
   const bool use_tma = out_sj == 1 && (out_si * p) % 2 == 0 &&
@@ -876,7 +881,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   if (const char* rs = std::getenv("GWG_REAL_SPLIT")) e->real_split = std::atoi(rs) != 0;
   if (const char* cl = std::getenv("GWG_I8_CLUSTER")) {
     const int v = std::atoi(cl);
-    e->i8_cluster = v == 1 || v == 2 ? v : 0;
+    e->i8_cluster = v >= 1 && v <= 3 ? v : 0;
   }
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));

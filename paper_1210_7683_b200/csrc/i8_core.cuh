@@ -23,13 +23,20 @@ namespace gwg {
 // Tile geometry shared by the int8 kernels: M = 128 SNPs, N = 7 slices x RB
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
-template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1>
+template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1,
+          int PAIR_AXIS_ = 0>
 struct I8Tile {
   // CLUSTER = 2: CTA pairs (a thread-block cluster) work on SNP tiles 2u and
   // 2u+1 against the same B rows; each CTA loads half of the B tile (4 of the
   // 8 slice slots) and multicasts it to both, halving the B operand's
   // L2->SMEM traffic (used where B dominates: large n, one trait per tile).
   static constexpr int CLUSTER = CLUSTER_;
+  // PAIR_AXIS = 1 (CLUSTER = 2): the pair takes B tiles 2u and 2u+1 of the
+  // same SNP tile instead, and each CTA loads half of the A tile (64 SNP
+  // rows) and multicasts it — for one or two traits per tile (p >= 9), where
+  // the SNP tile is re-read once per trait tile and dominates L2 traffic.
+  static constexpr int PAIR_AXIS = PAIR_AXIS_;
+  static_assert(PAIR_AXIS == 0 || CLUSTER == 2, "trait pairs need a CTA pair");
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
   // Seven signed 8-bit slices (base-256 digits of a 55-bit integer, see
@@ -44,8 +51,8 @@ struct I8Tile {
   static constexpr int OUT_BUFS = OUT_BUFS_;     // staging tiles per epilogue warp
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
   static constexpr uint32_t B_BYTES = SLOTS * RB * BK;  // <= 32 KB of smem (slots)
-  static constexpr int B_SLICES_PER_CTA = SLOTS / CLUSTER;
-  static constexpr uint32_t B_PART = B_BYTES / CLUSTER;  // loaded (and multicast) per CTA
+  static constexpr int B_SLICES_PER_CTA = PAIR_AXIS ? SLOTS : SLOTS / CLUSTER;
+  static constexpr uint32_t B_PART = PAIR_AXIS ? B_BYTES : B_BYTES / CLUSTER;  // loaded per CTA
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
@@ -154,6 +161,19 @@ __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map
       ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+      "h"(cta_mask), "l"(policy)
+      : "memory");
+}
+
+// 2-D TMA load multicast to the CTAs in cta_mask.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int32_t c0,
+                                               int32_t c1, uint64_t* bar, uint16_t cta_mask,
+                                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)),
       "h"(cta_mask), "l"(policy)
       : "memory");
 }
@@ -351,14 +371,18 @@ struct I8Sched {
     rank = C::CLUSTER > 1 ? int(blockIdx.x % C::CLUSTER) : 0;
     unit = int(blockIdx.x / C::CLUSTER);
     units = int(gridDim.x / C::CLUSTER);
-    tm_units = (tiles_m + C::CLUSTER - 1) / C::CLUSTER;
-    const int ntiles = tm_units * tiles_r;
+    // unit grid: (SNP-tile pairs x B tiles), or (SNP tiles x B-tile pairs)
+    tm_units = C::PAIR_AXIS ? tiles_m : (tiles_m + C::CLUSTER - 1) / C::CLUSTER;
+    tr_units = C::PAIR_AXIS ? (tiles_r + 1) / 2 : tiles_r;
+    const int ntiles = tm_units * tr_units;
     my_tiles = unit < ntiles ? (ntiles - 1 - unit) / units + 1 : 0;
   }
+  int tr_units;
   __device__ void coords(int lt, int& tm, int& tr) const {
-    int tu;
-    i8_tile_coords(unit + lt * units, tm_units, tiles_r, tu, tr);
-    tm = tu * C::CLUSTER + rank;
+    int tu, ru;
+    i8_tile_coords(unit + lt * units, tm_units, tr_units, tu, ru);
+    tm = C::PAIR_AXIS ? tu : tu * C::CLUSTER + rank;
+    tr = C::PAIR_AXIS ? ru * 2 + rank : ru;
   }
 };
 
@@ -395,6 +419,14 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
 #endif
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
       mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
+      if constexpr (C::PAIR_AXIS == 1) {
+        // half of the shared SNP tile each (box 128 k x 64 SNPs), multicast;
+        // this CTA's own B tile, all 8 slots
+        tma_load_2d_mc(st + sch.rank * (C::A_BYTES / 2), tmap_x, ks * C::BK,
+                       tm * C::BM + sch.rank * (C::BM / 2), &sm.full[s], 3, pol_x);
+        tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
+        continue;
+      }
       tma_load_2d(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
       if (C::CLUSTER > 1)
         tma_load_3d_mc(st + C::A_BYTES + sch.rank * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,

@@ -76,7 +76,8 @@ struct LinCfg {
       size_t(STAGES_0) * STAGE_B + size_t(EPI) * OUT_BUFS * 4096 + 1280 <= 227 * 1024
           ? STAGES_0
           : STAGES_0 - 1;
-  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL>;
+  // CL = 3: CTA pairs along the trait axis sharing (multicasting) the SNP tile
+  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 3 ? 2 : CL, CL == 3 ? 1 : 0>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
@@ -354,17 +355,20 @@ cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int sms,
                                 cudaStream_t s) {
   using C = typename LinCfg<P, CL>::Tile;
-  const int64_t units = int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
+  const int64_t units = C::PAIR_AXIS ? int64_t(a.tiles_m) * ((a.tiles_r + 1) / 2)
+                                     : int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
   return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a);
 }
 
 // Per-p entry of the split grid (kernels_lin_*.cu).
 struct LinOps {
   int kt = 0, p8 = 0, rb = 0;
-  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile
-  cudaError_t (*launch[2])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr};
-  int b_slices_box[2] = {8, 4};  // slice slots per TMA box
+  // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile;
+  // [2]: CTA pairs on two B tiles sharing (multicasting) the SNP tile
+  cudaError_t (*launch[3])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr, nullptr};
+  int b_slices_box[3] = {8, 4, 8};  // slice slots per TMA box
+  int a_box_rows[3] = {128, 128, 64};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
   bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
 };
@@ -377,6 +381,7 @@ LinOps make_lin_ops() {
   o.rb = LinCfg<P>::RB;
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
+  o.launch[2] = &launch_linear_solve<P, 3>;
   o.row = LinCfg<P>::BW;
   o.tma_row = LinCfg<P>::TMA_ROW;
   return o;

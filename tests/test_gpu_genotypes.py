@@ -216,19 +216,21 @@ def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
 
 
 @pytest.mark.parametrize("n,p,m,t", [(200, 4, 300, 20), (1000, 4, 1000, 64), (300, 12, 129, 17),
-                                     (257, 20, 333, 7)])
+                                     (257, 20, 333, 7), (300, 13, 200, 20)])
 def test_int8_kernel_variants_bitwise_identical(n, p, m, t, monkeypatch):
-    """Both int8 launch geometries (GWG_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
-    multicasting B) give the same bits: the int32 slice products are exact
-    and the recombination order fixed."""
+    """Every int8 launch geometry (GWG_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
+    on two SNP tiles multicasting B, 3 CTA pairs on two W tiles multicasting
+    the SNP tile) gives the same bits: the int32 slice products are exact and
+    the recombination order fixed."""
     ds = datagen.generate(n, p, m, t, seed=n + p)
     basis, values = gw.eigendecompose(ds["kinship"])
     out = {}
-    for cl in ("1", "2"):
+    for cl in ("1", "2", "3"):
         monkeypatch.setenv("GWG_I8_CLUSTER", cl)
         out[cl] = run(ds, basis, values, "genotypes")
     assert not np.isnan(out["2"]).any()
     assert np.array_equal(out["1"], out["2"])
+    assert np.array_equal(out["1"], out["3"])
 
 
 def test_auto_coding_picks_the_path_per_slab():
