@@ -37,6 +37,10 @@ namespace gwg {
 #define LIN_EXPERIMENT 0
 #endif
 
+#ifndef LIN_TRACE
+#define LIN_TRACE 0
+#endif
+
 #ifndef LIN_WIDE_MAXP
 #define LIN_WIDE_MAXP 16
 #endif
@@ -113,6 +117,14 @@ struct LinArgs {
   int32_t gate_codes = 0;
 };
 
+#if LIN_TRACE
+// Timing trace (never in a shipped build): CTA 0, the 8 epilogue warps of
+// TMEM lane quarter 0 and 1... (warps 4..11), first 48 of their tiles:
+// [0] before the acc_full wait, [1] after it, [2] TMEM released, [3] tile done.
+__device__ long long g_lin_trace[16][48][4];
+__device__ long long g_lin_t0;
+#endif
+
 template <int P, int CL>
 __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
@@ -178,7 +190,15 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       // to the recombination below: no per-column memory round trip
       const double sc_lane =
           lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) * 0x1p-55 : 0.0;  // sigma 2^-55, exact
+#if LIN_TRACE
+      const int tix = (lt - h) / L::ACC;
+      const bool tr_on = blockIdx.x == 0 && lane == 0 && tix < 48;
+      if (tr_on) g_lin_trace[ew][tix][0] = clock64();
+#endif
       mbar_wait(&sm.acc_full[buf], par);
+#if LIN_TRACE
+      if (tr_on) g_lin_trace[ew][tix][1] = clock64();
+#endif
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
       const bool tma = L::TMA_OUT && a.use_tma;
@@ -233,7 +253,12 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       for (int g0 = 0; g0 < L::CELLS; g0 += L::GROUP) {
         double lin[L::GROUP][P];
         recombine(cell0 + g0, L::GROUP, lin);
-        if (g0 + L::GROUP >= L::CELLS) release();
+        if (g0 + L::GROUP >= L::CELLS) {
+          release();
+#if LIN_TRACE
+          if (tr_on) g_lin_trace[ew][tix][2] = clock64();
+#endif
+        }
         double beta[L::GROUP][P];
         bool ok[L::GROUP];
 #pragma unroll
@@ -344,10 +369,21 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
         }
       }
       if (tma) nchunk += L::ROW / L::CHUNK;
+#if LIN_TRACE
+      if (tr_on) g_lin_trace[ew][tix][3] = clock64();
+#endif
     }
     if (lane == 0) bulk_wait0();
   }
   i8_teardown<C>(tmem_base, warp);
+#if LIN_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && P == 4) {
+    for (int w = 0; w < 16; ++w)
+      for (int i = 0; i < 48; ++i)
+        printf("LTR %d %d %lld %lld %lld %lld\n", w, i, g_lin_trace[w][i][0], g_lin_trace[w][i][1],
+               g_lin_trace[w][i][2], g_lin_trace[w][i][3]);
+  }
+#endif
 }
 
 template <int P, int CL>
