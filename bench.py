@@ -3,20 +3,23 @@
 c1: n=1000, p=4, m=100,000 SNPs per GPU, t=1,000 traits, FP64, synthetic
 inputs from BASELINE.json's generators (one seed).  A step is one pass of the
 hot path over one batch: rotate Y' = Z^T Y and X_R' = Z^T X_R on the device,
-build every trait context, and solve all m x t cells with the fused grid
-kernel (the eigendecomposition is the one-off CPU preloop, outside the step,
-as in the paper).
+build every trait context, and solve all m x t cells (the eigendecomposition
+is the one-off CPU preloop, outside the step, as in the paper).
 
-  value : inputs already resident in HBM (device pointers through the C ABI)
-  e2e   : the same step through gwg_run_grid / gwg_set_traits with pinned HOST
-          buffers: H2D of X_R and Y and D2H of every b_ij inside the timed region
-  --impl reference : the reference's CPU path (the oracle restatement of
-          gwgrid's compute_tile CT scheduler + OpenBLAS rotation, oracle/) on the
-          host cores, bounded sample of the same workload.
+  value  : inputs already resident in HBM (device pointers through the C ABI)
+  e2e    : the same step through gwg_set_traits + gwg_run_grid with pinned HOST
+           buffers (X_R as BASELINE's doubles): H2D of X_R and Y and D2H of
+           every b_ij inside the timed region; e2e_int8 the same with the
+           genotype codes as 1-byte int8 (GWG_FORMAT_I8)
+  parity : the timed grid against the CPU oracle's full c1 grid (every cell)
+  --impl reference : the reference's CPU path (oracle/: the restatement of
+           gwgrid's compute_tile CT scheduler + OpenBLAS rotation) on the host
+           cores over the same full c1 grid per step; it loads no engine code
+           (inputs from the oracle library's copy of the generator).
 
-Multi-GPU (torchrun): the SNP axis is sharded (weak scaling: m SNPs per rank);
-Z, lambda, X_L, Y, h2 are broadcast once from rank 0 over NCCL; no data-path
-collective; timing is max over ranks.
+Multi-GPU (torchrun): paper_1210_7683_b200.multi shards the SNP axis (weak
+scaling: m SNPs per rank); Z, lambda, X_L, Y, h2 are broadcast once from rank
+0 over NCCL; no data-path collective; timing is max over ranks.
 """
 from __future__ import annotations
 
@@ -24,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -46,6 +48,7 @@ PEAK_SOURCE = ("measured: DMMA.8x8x4 issue loop on this pool's B200 at 1965 MHz 
                "(profiles/r01_fp64_peak.txt; = 148 SM x 128 flop/clk x 1.965 GHz; "
                "MEASURED_PEAKS.json holds no FP64 figure)")
 SEED = 20261019
+PROFILE_TAG = "r02"
 
 
 def parse():
@@ -63,7 +66,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt-coding", dest="alt_coding", action="store_false",
                     help="skip timing the other SNP coding on the same data")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true",
+                    help="skip the CPU baseline (and with it the every-cell parity)")
     return ap.parse_args()
 
 
@@ -121,70 +125,52 @@ class Clocks:
                 "reasons": sorted(self.reasons), "samples": len(sm)}
 
 
-def dist_setup(n_gpus: int):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
 
 
 def make_inputs(args, rank: int, world: int, dev_index: int):
-    """Rank 0 builds the shared operands (kinship eig on the CPU); they are
-    broadcast over NCCL.  Each rank generates its own SNP shard."""
+    """Shared operands from rank 0 (kinship eig on the CPU), broadcast once by
+    multi.broadcast_shared; each rank generates only its own SNP shard
+    (weak scaling: global columns [rank m, (rank + 1) m))."""
     import torch
 
-    from paper_1210_7683_b200 import datagen, eigendecompose
+    from paper_1210_7683_b200 import datagen, eigendecompose, multi
 
     n, p, m, t = args.n, args.p, args.m, args.t
     dev = torch.device("cuda", dev_index)
-    shared = {}
+    shared_np, eig_s = None, None
     if rank == 0:
         phi = datagen.kinship(SEED, n, 2 * n)
         t0 = time.perf_counter()
         basis, values = eigendecompose(phi)
-        shared["eig_s"] = time.perf_counter() - t0
-        shared["basis"] = torch.from_numpy(np.ascontiguousarray(basis.T)).to(dev).t()
-        shared["values"] = torch.from_numpy(values).to(dev)
-        shared["xl"] = torch.from_numpy(np.ascontiguousarray(datagen.covariates(SEED, n, p).T)).to(dev).t()
-        shared["y"] = torch.from_numpy(np.ascontiguousarray(
-            datagen.normals(SEED, datagen.M_TRAITS, n, 0, t).T)).to(dev).t()
-        shared["h2"] = torch.from_numpy(datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95)).to(dev)
-    else:
-        shared["basis"] = torch.empty((n, n), dtype=torch.float64, device=dev).t()
-        shared["values"] = torch.empty(n, dtype=torch.float64, device=dev)
-        shared["xl"] = torch.empty((p - 1, n), dtype=torch.float64, device=dev).t()
-        shared["y"] = torch.empty((t, n), dtype=torch.float64, device=dev).t()
-        shared["h2"] = torch.empty(t, dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-
-        for key in ("basis", "values", "xl", "y", "h2"):
-            buf = shared[key]
-            base = buf.t() if buf.dim() == 2 else buf
-            dist.broadcast(base, src=0)
-        # the engine reads these on its own stream: finish the broadcasts first
-        torch.cuda.synchronize(dev)
-    shared["sigma2"] = torch.ones(t, dtype=torch.float64, device=dev)
-    # this rank's SNP shard: global columns [rank*m, (rank+1)*m), pinned host
+        eig_s = time.perf_counter() - t0
+        shared_np = {"basis": basis, "values": values, "xl": datagen.covariates(SEED, n, p),
+                     "y": datagen.normals(SEED, datagen.M_TRAITS, n, 0, t),
+                     "h2": datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95),
+                     "sigma2": np.ones(t)}
+    shared = multi.broadcast_shared(shared_np, n, p, t, device=dev)
+    torch.cuda.synchronize(dev)
+    shared["eig_s"] = eig_s
+    i0, i1 = multi.rank_range(m * world, world, rank)
     x_host = torch.empty((m, n), dtype=torch.float64).pin_memory()
     xh = x_host.numpy().T  # (n, m) column-major view
-    datagen.genotypes(SEED, datagen.M_SNPS, n, rank * m, m, out=xh)
-    return shared, x_host, xh
+    datagen.genotypes(SEED, datagen.M_SNPS, n, i0, i1 - i0, out=xh)
+    return shared, x_host, xh, i0
 
 
 def run_ours(args):
     import torch
 
     import paper_1210_7683_b200 as gw
+    from paper_1210_7683_b200 import multi
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = multi.dist_env()
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     n, p, m, t = args.n, args.p, args.m, args.t
-    shared, x_host_t, x_host = make_inputs(args, rank, world, local)
+    shared, x_host_t, x_host, i0 = make_inputs(args, rank, world, local)
     dev = torch.device("cuda", local)
 
     eng = gw.Engine(n, p, device=local)
@@ -197,7 +183,7 @@ def run_ours(args):
 
     def step():
         eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
-        eng.solve_snp_slab(x_dev, out=b_dev)
+        eng.solve_snp_slab(x_dev, out=b_dev, i0=i0)
 
     def barrier():
         if world > 1:
@@ -205,6 +191,15 @@ def run_ours(args):
 
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        import torch.distributed as dist
+
+        tm = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        return float(tm.item())
 
     for _ in range(args.warmup):
         step()
@@ -220,14 +215,7 @@ def run_ours(args):
         barrier()
     ms_total = ev0.elapsed_time(ev1)
     cnt = eng.counters()
-    ms_max = ms_total
-    if world > 1:
-        import torch.distributed as dist
-
-        tm = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        ms_max = float(tm.item())
-    ms_step = ms_max / args.steps
+    ms_step = max_over_ranks(ms_total) / args.steps
     cells = m * t * world
     value = cells / (ms_step * 1e-3)
     grid_flops_step = m * t * 2 * n * (p + 1)
@@ -290,7 +278,6 @@ def run_ours(args):
                 "algorithmic_flops_per_launch": issued,
                 "grid_fp64_equivalent_tflops": grid_flops_step / (kernel_ms * 1e-3) / 1e12}
 
-    # sanity: no NaN, finite results
     bad = int(torch.isnan(b_dev).sum().item())
 
     # ---- the other SNP coding on the same data, for transparency: the all-FP64
@@ -303,7 +290,7 @@ def run_ours(args):
 
         def alt_step():
             eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
-            eng.solve_snp_slab(x_dev, out=b_alt)
+            eng.solve_snp_slab(x_dev, out=b_alt, i0=i0)
 
         alt_step()
         barrier()
@@ -323,8 +310,8 @@ def run_ours(args):
         eng.set_snp_coding(args.snp_coding)
         del b_alt
 
-    # ---- e2e through gwg_run_grid with pinned host buffers ------------------
-    e2e = None
+    # ---- e2e through gwg_set_traits + gwg_run_grid with pinned host buffers --
+    e2e = e2e_i8 = None
     if not args.no_e2e:
         b_host_t = torch.empty((m, t, p), dtype=torch.float64).pin_memory()
         b_host = b_host_t.numpy()
@@ -333,36 +320,53 @@ def run_ours(args):
         y_host = y_host_t.numpy().T
         h2_host = shared["h2"].cpu().numpy()
         s2_host = np.ones(t)
+        codes_t = torch.empty((m, n), dtype=torch.int8).pin_memory()
+        codes_t.copy_(x_host_t.to(torch.int8))
+        codes = codes_t.numpy().T  # (n, m) int8, column-major, pinned
 
-        def e2e_step():
-            eng.set_traits(y_host, h2_host, s2_host)
-            eng.run_grid(x_host, out=b_host)
+        def timed_e2e(snps):
+            def e2e_step():
+                eng.set_traits(y_host, h2_host, s2_host)
+                eng.run_grid(snps, out=b_host, i0=i0)
 
-        for _ in range(max(1, args.warmup - 1)):
-            e2e_step()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        barrier()
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            import torch.distributed as dist
+            for _ in range(max(1, args.warmup - 1)):
+                e2e_step()
+            barrier()
+            eng.reset_counters()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                e2e_step()
+            barrier()
+            e2e_s = max_over_ranks(time.perf_counter() - t0)
+            same = bool(np.array_equal(b_host, b_dev.cpu().numpy()))
+            c = eng.counters()
+            return e2e_s, same, c
 
-            tm = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            e2e_s = float(tm.item())
-        # the e2e results must equal the device-resident ones bitwise
-        same = bool(np.array_equal(b_host, b_dev.cpu().numpy()))
+        e2e_s, same, c = timed_e2e(x_host)
         e2e = {"value": cells * args.steps / e2e_s, "unit": "GLS/s",
                "h2d_bytes_per_step": n * m * 8 + n * t * 8 + 2 * t * 8,
                "d2h_bytes_per_step": m * t * p * 8, "ms_per_step": 1e3 * e2e_s / args.steps,
+               "io_stall_ms_per_step": c["io_stall_ms"] / args.steps,
+               "api": "Engine.set_traits + Engine.run_grid (gwg_set_traits + gwg_run_grid), "
+                      "X_R as float64 (BASELINE's storage)",
                "bitwise_equal_to_device_path": same}
+        e2e_s, same, c = timed_e2e(codes)
+        e2e_i8 = {"value": cells * args.steps / e2e_s, "unit": "GLS/s",
+                  "h2d_bytes_per_step": n * m + n * t * 8 + 2 * t * 8,
+                  "d2h_bytes_per_step": m * t * p * 8, "ms_per_step": 1e3 * e2e_s / args.steps,
+                  "io_stall_ms_per_step": c["io_stall_ms"] / args.steps,
+                  "api": "the same with X_R as int8 genotype codes (GWG_FORMAT_I8)",
+                  "bitwise_equal_to_device_path": same}
+        del b_host_t, codes_t
 
-    # ---- CPU baseline: the oracle (reference restatement) on the host --------
-    cpu = None
+    # ---- CPU baseline (oracle) on the full grid, and every-cell parity -------
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args, shared, x_host)
+        from oracle.parity import parity_metrics
+
+        cpu, ref = cpu_baseline(args, shared, x_host)
+        parity = parity_metrics(b_dev.cpu().numpy(), ref)
+        del ref
 
     if rank == 0:
         line = {
@@ -386,7 +390,9 @@ def run_ours(args):
             "roofline": roof,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "e2e_int8": e2e_i8,
             "cpu_baseline": cpu,
+            "parity": parity,
             "nan_cells": bad,
             "other_coding": alt,
             "preloop_eig_s": shared.get("eig_s"),
@@ -400,17 +406,19 @@ def run_ours(args):
 
 
 def load_traffic(name: str):
-    path = os.path.join(ROOT, "profiles", "r01_%s_ncu.json" % name)
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        return None
+    for tag in (PROFILE_TAG, "r01"):
+        path = os.path.join(ROOT, "profiles", "%s_%s_ncu.json" % (tag, name))
+        try:
+            with open(path) as f:
+                return json.load(f).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            continue
+    return None
 
 
-def cpu_sample_run(args, basis, values, xl, y, h2, x_sample, workers):
-    """The reference CPU step on a sample: OpenBLAS rotations + contexts +
-    compute_tile (CT, 160x160 blocks, `workers` threads)."""
+def cpu_sample_run(basis, values, xl, y, h2, x_sample, workers):
+    """The reference CPU step: OpenBLAS rotations + contexts + compute_tile
+    (CT, 160x160 blocks, `workers` threads) — oracle/ (test infrastructure)."""
     from oracle import oracle as orc
 
     orc.set_blas_threads(workers)
@@ -420,62 +428,76 @@ def cpu_sample_run(args, basis, values, xl, y, h2, x_sample, workers):
     return orc.compute_grid(values, xlr, xr, yr, h2, np.ones(len(h2)), workers=workers)
 
 
-def cpu_baseline(args, shared, x_host, sample_m: int | None = None):
+def cpu_baseline(args, shared, x_host):
+    """The oracle's reference CPU step over the SAME full grid the device just
+    timed (rank 0, N = 1): its time is the cpu_baseline, its grid the parity
+    reference."""
     basis = shared["basis"].cpu().numpy()
     values = shared["values"].cpu().numpy()
     xl = shared["xl"].cpu().numpy()
     y = shared["y"].cpu().numpy()
     h2 = shared["h2"].cpu().numpy()
     workers = os.cpu_count() or 1
-    ms = sample_m or int(os.environ.get("GWG_CPU_SAMPLE_M", "100000"))
-    xs = np.asfortranarray(x_host[:, :ms])
-    cpu_sample_run(args, basis, values, xl, y, h2, xs[:, :160], workers)  # warm
+    xs = np.asfortranarray(x_host)
+    cpu_sample_run(basis, values, xl, y, h2, xs[:, :160], workers)  # warm
     t0 = time.perf_counter()
-    cpu_sample_run(args, basis, values, xl, y, h2, xs, workers)
+    ref = cpu_sample_run(basis, values, xl, y, h2, xs, workers)
     dt = time.perf_counter() - t0
-    return {"value": ms * args.t / dt, "unit": "GLS/s", "cores": workers, "kind": "port",
-            "sample": f"{ms} SNPs x {args.t} traits of c1 (rotation + contexts + compute_tile CT, "
-                      f"{workers} worker threads, OpenBLAS {workers} threads), {dt:.1f} s"}
+    ms = xs.shape[1]
+    return ({"value": ms * args.t / dt, "unit": "GLS/s", "cores": workers, "kind": "port",
+             "sample": f"the full c1 grid: {ms} SNPs x {args.t} traits (rotation + contexts + "
+                       f"compute_tile CT, {workers} worker threads, OpenBLAS {workers} threads), "
+                       f"{dt:.1f} s"}, ref)
 
 
 def run_reference(args):
-    world, rank, _ = dist_setup(args.gpus)
+    """bench.py --impl reference: the reference's CPU path (oracle/, the
+    restated gwgrid compute_tile CT scheduler + OpenBLAS rotation) over the
+    same full c1 grid per step.  Inputs come from the oracle library's own
+    copy of the seeded generator; no engine library is loaded."""
+    from paper_1210_7683_b200 import multi
+
+    world, rank, _ = multi.dist_env()
     if rank != 0:
         return
-    from paper_1210_7683_b200 import datagen, eigendecompose
+    from oracle import oracle as orc
+    from paper_1210_7683_b200 import datagen  # pure Python; generator calls go to `lib`
 
-    n, p, t = args.n, args.p, args.t
-    phi = datagen.kinship(SEED, n, 2 * n)
-    basis, values = eigendecompose(phi)
-    xl = datagen.covariates(SEED, n, p)
-    y = datagen.normals(SEED, datagen.M_TRAITS, n, 0, t)
-    h2 = datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95)
-    ms = int(os.environ.get("GWG_CPU_SAMPLE_M", "8000"))
-    xs = datagen.genotypes(SEED, datagen.M_SNPS, n, 0, ms)
+    lib = orc.load()
+    n, p, m, t = args.n, args.p, args.m, args.t
+    phi = datagen.kinship(SEED, n, 2 * n, lib=lib)
+    basis, values = orc.eigendecompose(phi)
+    xl = datagen.covariates(SEED, n, p, lib=lib)
+    y = datagen.normals(SEED, datagen.M_TRAITS, n, 0, t, lib=lib)
+    h2 = datagen.uniform(SEED, datagen.M_H2, t, 0.05, 0.95, lib=lib)
+    xs = datagen.genotypes(SEED, datagen.M_SNPS, n, 0, m, lib=lib)
     workers = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_sample_run(args, basis, values, xl, y, h2, xs[:, :160], workers)
+    warm = min(m, 2000)
+    for _ in range(args.warmup):  # BLAS threads and caches: a 2,000-SNP slice
+        cpu_sample_run(basis, values, xl, y, h2, xs[:, :warm], workers)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cpu_sample_run(args, basis, values, xl, y, h2, xs, workers)
+        cpu_sample_run(basis, values, xl, y, h2, xs, workers)
     dt = (time.perf_counter() - t0) / args.steps
-    value = ms * t / dt
+    value = m * t / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GLS/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json generators, seed %d)" % SEED,
-        "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": args.m, "t": t,
-                   "cells_per_step": ms * t, "m_sample_per_step": ms,
-                   "parallelism": "host threads x%d (rank 0)" % (os.cpu_count() or 1),
-                   "snp_coding": "real (the reference's double-precision CPU path)"},
+        "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": m, "t": t,
+                   "cells_per_step": m * t,
+                   "parallelism": "host threads x%d (rank 0)" % workers,
+                   "snp_coding": "real (the reference's double-precision CPU path)",
+                   "warmup_sample": f"{warm} SNPs x {t} traits"},
         "cpu_baseline": {"value": value, "unit": "GLS/s", "cores": workers, "kind": "port",
-                         "sample": f"{ms} SNPs x {t} traits of c1 per step (oracle/ restatement "
-                                   "of gwgrid compute_tile CT + OpenBLAS rotation)"},
+                         "sample": f"the full c1 grid per step: {m} SNPs x {t} traits (oracle/ "
+                                   "restatement of gwgrid compute_tile CT + OpenBLAS rotation)"},
         "e2e": {"value": value, "unit": "GLS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference (gwgrid) cannot be built here: Eigen3/CLI11/doctest absent; "
-                "this is the oracle/ C++ restatement of its CPU path",
+                "this is the oracle/ C++ restatement of its CPU path; inputs from the "
+                "oracle library's copy of the generator (no engine code loaded)",
     }
     print(json.dumps(line), flush=True)
 

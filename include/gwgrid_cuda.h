@@ -76,12 +76,51 @@ typedef struct gwg_counters {
    * SNP factorised; sbr_terms = r of the last slab (0 = direct contraction) */
   uint64_t sbr_flops;
   int64_t sbr_terms;
+  /* run_grid: compute-side waits on slab I/O (pipeline_run's stall,
+   * pipeline.hpp:106-136): gaps of the compute stream between slabs (first
+   * H2D included) plus the tail of result stores after the last slab */
+  double io_stall_ms;
+  /* order-independent checksum of every b_ij solved with
+   * gwg_run_options.checksum = 1 since the last reset: the wrapping sum over
+   * cells and components of gwg_cell_hash(i, j, c, bits(b_ijc)) — identical
+   * for any slab width, layout, shard split or GPU count */
+  uint64_t checksum;
+  uint64_t checksum_cells;
 } gwg_counters;
+
+/* Input formats of SNP slabs given to gwg_run_grid. */
+enum gwg_snp_format {
+  GWG_FORMAT_F64 = 0,  /* x_r is double (any real values; raw or rotated)          */
+  GWG_FORMAT_I8 = 1    /* x_r is int8_t genotype codes in [-127, 127], 1 byte each:
+                          8x less host memory and PCIe traffic; the genotype path
+                          runs on them directly (GWG_SNP_REAL converts to FP64 on
+                          the device); -128 is a GWG_DIMENSION error */
+};
+
+/* Result sink: receives each slab's cells from a pinned host buffer that is
+ * valid only during the call: rows SNPs starting at global SNP index i0
+ * against all t traits, in the run's layout, slab-local
+ * (NUMPY: (il*t + j)*p; STREAM: (j*rows + il)*p).  Called from one writer
+ * thread per engine, in slab order; gwg_group_run_grid calls it from several
+ * threads at once (one per device).  A non-zero return aborts the run with
+ * GWG_IO. */
+typedef int32_t (*gwg_result_sink)(void* user, int64_t i0, int64_t rows, const double* cells);
 
 typedef struct gwg_run_options {
   int64_t mb;          /* SNP columns per streamed slab; 0 = engine default       */
   int32_t layout;      /* gwg_layout of the host result buffer                    */
   int32_t double_buffer; /* 1 = overlap H2D / compute / D2H (default)            */
+  int32_t snp_format;  /* gwg_snp_format of x_r (default GWG_FORMAT_F64)         */
+  int32_t checksum;    /* 1 = accumulate the device checksum into counters        */
+  int64_t i0;          /* global SNP index of x_r's first column (a shard of a
+                          larger grid): error coordinates and checksum keys are
+                          global; results still start at b[0]                    */
+  int64_t ldb;         /* STREAM layout: cells per trait row of b (>= m; 0 = m)  */
+  gwg_result_sink sink; /* non-NULL: results leave through the sink (rotating
+                          pinned buffers; b_host unused and may be NULL)        */
+  void* sink_user;
+  int32_t ring;        /* pinned result buffers rotated through the sink (0 = 2) */
+  int32_t reserved;
 } gwg_run_options;
 
 typedef struct gwg_engine gwg_engine;
@@ -125,9 +164,12 @@ int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_s
  * h2[t], sigma2[t]; rotates Y on the device and builds every trait context
  * (weights d, D = 1/d, D.Y', D.X_L', S_TL, chol(S_TL), z_T) in one kernel.
  * Replaces transform_trait_slab + build_trait_contexts (grid.cpp:135-175) and
- * the per-pass load_pass (grid.cpp:501-517).  A trait whose rotated weights
- * fail the relative floor (gls.cpp:59-75) fails with
- * GWG_NOT_POSITIVE_DEFINITE, snp_index = -1, trait_index = the first such j. */
+ * the per-pass load_pass (grid.cpp:501-517).  Asynchronous: the call queues
+ * its work and returns without a host round trip.  A trait whose rotated
+ * weights fail the relative floor (gls.cpp:59-75) is reported as
+ * GWG_NOT_POSITIVE_DEFINITE, snp_index = -1, trait_index = the first such j,
+ * by the next call that synchronises (gwg_solve_snp_slab, gwg_run_grid*,
+ * gwg_synchronize), ahead of any cell error. */
 int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* h2,
                        const double* sigma2, int32_t where, int32_t is_rotated,
                        gwg_status* st);
@@ -147,14 +189,65 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
                            int32_t out_where, int32_t layout, int64_t ldo,
                            gwg_status* st);
 
-/* Stream the whole m x t grid from host memory: X_R (n x m, raw, col-major)
- * in mb-column slabs through double-buffered H2D / rotate+grid / D2H on three
- * CUDA streams, into the host result buffer b (m*t*p doubles, `layout`).
- * Replaces preloop_stream_transform + run_grid (grid.cpp:378-641) for
- * in-memory operands (the GWG1 file legs are out of scope). */
-int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
+/* Stream the whole m x t grid from host memory: X_R (n x m, raw unless
+ * rotated, col-major; double or int8 codes per opts->snp_format) in
+ * mb-column slabs through double-buffered H2D / rotate+grid / D2H on three
+ * CUDA streams, into the host result buffer b (m*t*p doubles, `layout`) or
+ * through opts->sink.  Replaces preloop_stream_transform + run_grid
+ * (grid.cpp:378-641) with its double-buffered pipeline_run
+ * (pipeline.hpp:78-137) for in-memory operands; counters->io_stall_ms is
+ * pipeline_run's stall. */
+int32_t gwg_run_grid(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host,
                      const gwg_run_options* opts, gwg_counters* counters,
                      gwg_status* st);
+
+/* The per-(cell, component) term of the order-independent result checksum
+ * (host copy of the device formula, for checking a downloaded grid):
+ * a splitmix64 mix of the global SNP index i, trait index j, component c and
+ * the IEEE-754 bits of b_ijc.  The checksum is the wrapping uint64 sum of
+ * these terms over every component of every cell. */
+uint64_t gwg_cell_hash(int64_t i, int64_t j, int64_t c, uint64_t bits);
+
+/* Order the engine's compute stream after all work already queued on
+ * `stream` (a cudaStream_t as void*, e.g. torch's current stream), without a
+ * host round trip: device operands produced there are then safe to read. */
+int32_t gwg_wait_stream(gwg_engine* e, void* stream, gwg_status* st);
+
+/* ---- One process, several GPUs --------------------------------
+ * A group holds one engine per listed device (a device may repeat).  The
+ * shared operands go host -> the first device once and are then broadcast
+ * device-to-device (peer copies over NVLink / NVSwitch): the spectrum, the
+ * rotated covariates X_L' and the rotated traits Y' (plus h2, sigma2); each
+ * device builds its own trait contexts.  gwg_group_run_grid shards m into
+ * contiguous, balanced column ranges, one per device, and runs gwg_run_grid
+ * on each from its own host thread with its own pinned buffers; there is no
+ * other collective.  Results land in the caller's buffer (or sink) at global
+ * positions; counters are summed (checksum included: it does not depend on
+ * the split); the first failing cell in trait-major order over the whole grid
+ * is reported, like the one-device run.  Replaces run_grid's worker
+ * parallelism (grid.cpp:519-639) at device granularity. */
+typedef struct gwg_group gwg_group;
+gwg_group* gwg_group_create(const int32_t* devices, int32_t count, int64_t n, int64_t p,
+                            gwg_status* st);
+void gwg_group_destroy(gwg_group* g);
+int32_t gwg_group_size(const gwg_group* g);
+/* The k-th device's engine (options, counters, single-device calls). */
+gwg_engine* gwg_group_engine(gwg_group* g, int32_t k);
+int32_t gwg_group_set_spectrum(gwg_group* g, const double* basis, const double* lambda,
+                               int32_t where, gwg_status* st);
+int32_t gwg_group_set_covariates(gwg_group* g, const double* xl, int32_t where,
+                                 gwg_status* st);
+int32_t gwg_group_set_traits(gwg_group* g, int64_t t, const double* y, const double* h2,
+                             const double* sigma2, int32_t where, int32_t is_rotated,
+                             gwg_status* st);
+int32_t gwg_group_set_snp_coding(gwg_group* g, int32_t coding, gwg_status* st);
+int32_t gwg_group_set_option(gwg_group* g, int32_t option, int64_t value, gwg_status* st);
+/* Shard k covers SNP columns [bounds[k], bounds[k+1]) of an m-column run
+ * (bounds has size() + 1 entries). */
+int32_t gwg_group_shards(const gwg_group* g, int64_t m, int64_t* bounds);
+int32_t gwg_group_run_grid(gwg_group* g, int64_t m, const void* x_r_host, double* b_host,
+                           const gwg_run_options* opts, gwg_counters* counters,
+                           gwg_status* st);
 
 /* Independent verification route (CholeskyOracle, gls.cpp:188-244, as used by
  * gwgrid.verify_grid, bindings.cpp:192-222): for every trait j, factor
@@ -207,8 +300,8 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
  * run exactly on the int8 tensor cores (tcgen05.mma kind::i8, seven 8-bit
  * slices, exact int64 recombination, one rounding) and only S_BR = (X'.X')^T D
  * stays on DMMA, factorised as ((X'.X')^T E) F through a positive exponential
- * sum of D (gwg_exp_sum_design; GWG_SNP_GENOTYPES with GWG_SBR_DIRECT=1 in the
- * environment forces the direct contraction) — the same cells to rounding
+ * sum of D (gwg_exp_sum_design; GWG_OPT_SBR_DIRECT = 1 forces the direct
+ * contraction) — the same cells to rounding
  * (~1e-14 norm-wise), ~6.5x faster than the all-FP64 path at BASELINE config
  * 1; results stay bitwise independent of slab geometry.  GWG_SNP_AUTO (the
  * default): per slab, the device check decides — a slab of codes takes the
@@ -216,6 +309,33 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
  * of the path not taken return at once, no host round trip), never an error.
  * Pre-rotated slabs (is_rotated = 1) always take the FP64 path. */
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
+
+/* Engine options (no reference counterpart: they select among this library's
+ * own kernel schedules).  Every choice gives the reference's cells to
+ * rounding, and the result is a pure function of the inputs and the options
+ * (never of the caller's environment or the slab geometry).
+ *   GWG_OPT_SPLIT       1 (default): genotype slabs take the split grid
+ *                       (S_BR on DMMA, exact int8 linear terms + solve);
+ *                       0: the all-FP64 fused grid kernel for them too.
+ *   GWG_OPT_SBR_DIRECT  0 (default): S_BR through the positive exponential-sum
+ *                       factorisation of D where it applies; 1: always the
+ *                       direct contraction (X'.X')^T D.
+ *   GWG_OPT_REAL_SPLIT  1 (default): the FP64 path with t >= 256 takes the
+ *                       factorised S_BR and the grid kernel without the D
+ *                       column; 0: the single fused kernel.
+ *   GWG_OPT_I8_CLUSTER  0 (default, auto), 1 single CTAs, 2 CTA pairs
+ *                       multicasting the W/Z-slice tile, 3 CTA pairs
+ *                       multicasting the SNP tile (bitwise identical).
+ *   GWG_OPT_SBR_CFG     gls_sbr_kernel tile configuration index (default 0). */
+enum gwg_option {
+  GWG_OPT_SPLIT = 1,
+  GWG_OPT_SBR_DIRECT = 2,
+  GWG_OPT_REAL_SPLIT = 3,
+  GWG_OPT_I8_CLUSTER = 4,
+  GWG_OPT_SBR_CFG = 5
+};
+int32_t gwg_set_option(gwg_engine* e, int32_t option, int64_t value, gwg_status* st);
+int32_t gwg_get_option(gwg_engine* e, int32_t option, int64_t* value, gwg_status* st);
 
 /* Counters accumulated since the last reset. */
 int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out);

@@ -63,6 +63,13 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = ctypes.c_int32
             fn.argtypes = args
+        U64, PD = ctypes.c_uint64, ctypes.c_void_p
+        lib.gwg_gen_genotypes.argtypes = [U64, I32, I64, I64, I64, I32, PD, I64]
+        lib.gwg_gen_genotypes.restype = None
+        lib.gwg_gen_normals.argtypes = [U64, I32, I64, I64, I64, PD, I64]
+        lib.gwg_gen_normals.restype = None
+        lib.gwg_gen_uniform.argtypes = [U64, I32, I64, D, D, PD]
+        lib.gwg_gen_uniform.restype = None
         lib.orc_set_blas_threads.argtypes = [ctypes.c_int]
         lib.orc_set_blas_threads.restype = None
         lib.orc_cell_flops.restype = ctypes.c_uint64

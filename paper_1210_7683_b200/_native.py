@@ -28,6 +28,11 @@ GWG_LAYOUT_STREAM = 1
 GWG_SNP_REAL = 0
 GWG_SNP_GENOTYPES = 1
 GWG_SNP_AUTO = 2
+GWG_FORMAT_F64 = 0
+GWG_FORMAT_I8 = 1
+
+# gwg_option
+OPTIONS = {"split": 1, "sbr_direct": 2, "real_split": 3, "i8_cluster": 4, "sbr_cfg": 5}
 
 # Every symbol include/gwgrid_cuda.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -54,6 +59,21 @@ EXPORTED_SYMBOLS = (
     "gwg_gen_genotypes",
     "gwg_gen_normals",
     "gwg_gen_uniform",
+    "gwg_set_option",
+    "gwg_get_option",
+    "gwg_cell_hash",
+    "gwg_wait_stream",
+    "gwg_group_create",
+    "gwg_group_destroy",
+    "gwg_group_size",
+    "gwg_group_engine",
+    "gwg_group_set_spectrum",
+    "gwg_group_set_covariates",
+    "gwg_group_set_traits",
+    "gwg_group_set_snp_coding",
+    "gwg_group_set_option",
+    "gwg_group_shards",
+    "gwg_group_run_grid",
 )
 
 
@@ -82,10 +102,18 @@ class Counters(ctypes.Structure):
         ("quad_ms", ctypes.c_double),
         ("sbr_flops", ctypes.c_uint64),
         ("sbr_terms", ctypes.c_int64),
+        ("io_stall_ms", ctypes.c_double),
+        ("checksum", ctypes.c_uint64),
+        ("checksum_cells", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# int32_t (*gwg_result_sink)(void* user, int64_t i0, int64_t rows, const double* cells)
+RESULT_SINK = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                               ctypes.c_void_p)
 
 
 class RunOptions(ctypes.Structure):
@@ -93,6 +121,14 @@ class RunOptions(ctypes.Structure):
         ("mb", ctypes.c_int64),
         ("layout", ctypes.c_int32),
         ("double_buffer", ctypes.c_int32),
+        ("snp_format", ctypes.c_int32),
+        ("checksum", ctypes.c_int32),
+        ("i0", ctypes.c_int64),
+        ("ldb", ctypes.c_int64),
+        ("sink", RESULT_SINK),
+        ("sink_user", ctypes.c_void_p),
+        ("ring", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -140,6 +176,22 @@ def load() -> ctypes.CDLL:
         "gwg_gen_normals": (None, [U64, I32, I64, I64, I64, P, I64]),
         "gwg_gen_uniform": (None, [U64, I32, I64, D, D, P]),
         "gwg_exp_sum_design": (I32, [D, D, I32, I32, P, P, P]),
+        "gwg_set_option": (I32, [P, I32, I64, S]),
+        "gwg_get_option": (I32, [P, I32, ctypes.POINTER(I64), S]),
+        "gwg_cell_hash": (U64, [I64, I64, I64, U64]),
+        "gwg_wait_stream": (I32, [P, P, S]),
+        "gwg_group_create": (P, [ctypes.POINTER(I32), I32, I64, I64, S]),
+        "gwg_group_destroy": (None, [P]),
+        "gwg_group_size": (I32, [P]),
+        "gwg_group_engine": (P, [P, I32]),
+        "gwg_group_set_spectrum": (I32, [P, P, P, I32, S]),
+        "gwg_group_set_covariates": (I32, [P, P, I32, S]),
+        "gwg_group_set_traits": (I32, [P, I64, P, P, P, I32, I32, S]),
+        "gwg_group_set_snp_coding": (I32, [P, I32, S]),
+        "gwg_group_set_option": (I32, [P, I32, I64, S]),
+        "gwg_group_shards": (I32, [P, I64, ctypes.POINTER(I64)]),
+        "gwg_group_run_grid": (I32, [P, I64, P, P, ctypes.POINTER(RunOptions),
+                                     ctypes.POINTER(Counters), S]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -6,8 +6,12 @@
 //   transform_snp_slab + compute_tile        -> gwg_solve_snp_slab
 //   preloop_stream_transform + run_grid (CT, double-buffered pipeline_run,
 //   pipeline.hpp:78-137)                     -> gwg_run_grid
-// Rotations are cuBLAS DGEMMs (plain library GEMMs); the per-trait context
-// and the fused grid kernel are this library's own sm_100a kernels.
+// Every kernel on the path is this library's own sm_100a code: the
+// deterministic FP64-DMMA rotation (rotate_kernel.cuh) and its exact int8
+// tcgen05 counterpart for genotype slabs (rotate_i8.cuh), the per-trait
+// context kernel (trait_prep.cuh), the fused FP64 grid kernel
+// (grid_kernel.cuh) and the genotype split grid (grid_split.cuh: S_BR on DMMA;
+// linear_solve.cuh: exact int8 linear terms fused with the Cholesky solve).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -30,6 +34,7 @@
 #include "engine_internal.cuh"
 #include "rotate_i8.cuh"
 #include "rotate_kernel.cuh"
+#include "slab_kernels.cuh"
 
 namespace gwg_host {
 
@@ -96,9 +101,10 @@ int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int wher
            gwg_status* st) {
   GWG_CUDA_TRY(dst.ensure(std::max<size_t>(count, 1) * sizeof(double)));
   if (count == 0) return GWG_OK;
+  // device operands may live on another GPU (the group's peer broadcast):
+  // cudaMemcpyDefault lets UVA pick the route
   GWG_CUDA_TRY(cudaMemcpyAsync(dst.ptr, src, count * sizeof(double),
-                               where == GWG_DEVICE ? cudaMemcpyDeviceToDevice
-                                                   : cudaMemcpyHostToDevice,
+                               where == GWG_DEVICE ? cudaMemcpyDefault : cudaMemcpyHostToDevice,
                                e->comp));
   if (where != GWG_DEVICE) e->counters.bytes_loaded += count * sizeof(double);
   return GWG_OK;
@@ -111,8 +117,7 @@ int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int6
   if (ldd == 0) ldd = e->np;
   GWG_CUDA_TRY(dst.ensure(size_t(ldd) * std::max<int64_t>(cols, 1) * sizeof(double)));
   if (cols == 0) return GWG_OK;
-  const cudaMemcpyKind kind =
-      where == GWG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind kind = where == GWG_DEVICE ? cudaMemcpyDefault : cudaMemcpyHostToDevice;
   if (lds == e->n && ldd == e->n) {
     GWG_CUDA_TRY(cudaMemcpyAsync(dst.ptr, src, size_t(e->n) * cols * sizeof(double), kind, s));
   } else {
@@ -174,11 +179,21 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
   return GWG_OK;
 }
 
-int read_errors(gwg_engine* e, gwg_status* st, bool trait_only) {
+int read_errors(gwg_engine* e, gwg_status* st) {
   GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 3 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
-  if (!trait_only && e->snp_coding == GWG_SNP_GENOTYPES && e->err_host[2] != ~0ull)
+  if (e->err_host[0] != ~0ull) {  // queued by gwg_set_traits, reported here
+    const int64_t j = int64_t(e->err_host[0]);
+    return set_status(st, GWG_NOT_POSITIVE_DEFINITE, -1, j,
+                      "trait covariance is not positive definite in the rotated basis: a "
+                      "weight entry is below the relative floor (trait %lld)",
+                      (long long)j);
+  }
+  if (e->i8_input && e->err_host[2] != ~0ull)
+    return set_status(st, GWG_DIMENSION, -1, -1,
+                      "int8 SNP slabs must hold genotype codes in [-127, 127] (found -128)");
+  if (e->snp_coding == GWG_SNP_GENOTYPES && e->err_host[2] != ~0ull)
     return set_status(st, GWG_DIMENSION, -1, -1,
                       "SNP values are not integer genotype codes in [-127, 127] "
                       "(gwg_set_snp_coding(GENOTYPES)); use real-valued coding");
@@ -186,7 +201,8 @@ int read_errors(gwg_engine* e, gwg_status* st, bool trait_only) {
 }
 
 int reset_errors(gwg_engine* e, gwg_status* st) {
-  GWG_CUDA_TRY(cudaMemsetAsync(e->err.ptr, 0xff, 3 * sizeof(unsigned long long), e->comp));
+  GWG_CUDA_TRY(cudaMemsetAsync(static_cast<unsigned long long*>(e->err.ptr) + 1, 0xff,
+                               2 * sizeof(unsigned long long), e->comp));
   return GWG_OK;
 }
 
@@ -327,8 +343,72 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   return GWG_OK;
 }
 
+// int8 genotype slab (GWG_FORMAT_I8: n x cols codes, ld n) -> X'.X' (the
+// genotype path) or, for GWG_SNP_REAL / n beyond the exact-int8 bound, FP64
+// codes -> the DMMA rotation.  Codes are codes: no per-slab verdict gates
+// the launches; a -128 is an error (read_errors).
+int rotate_snps_i8(gwg_engine* e, const int8_t* src, int64_t cols, gwg_status* st) {
+  e->slab_i8 = false;
+  e->slab_auto = false;
+  if (cols <= 0) return GWG_OK;
+  using gwg::I8Cfg;
+  const int64_t n = e->n, kp = round_up(n, I8Cfg::BK);
+  const int blocks = int(std::min<int64_t>(cols, int64_t(e->sms) * 16));
+  if (e->snp_coding == GWG_SNP_REAL || n >= kMaxGenotypeN) {
+    GWG_CUDA_TRY(e->stage.ensure(size_t(raw_ld(e)) * cols * sizeof(double)));
+    gwg::i8_unpack_kernel<<<blocks, 256, 0, e->comp>>>(src, int32_t(n), int32_t(cols),
+                                                       e->stage.d(), raw_ld(e));
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    const int saved = e->snp_coding;
+    e->snp_coding = GWG_SNP_REAL;
+    const int rc = rotate_snps(e, e->stage.d(), raw_ld(e), cols, st);
+    e->snp_coding = saved;
+    return rc;
+  }
+  NvtxRange nvtx_("rotate_i8");
+  if (!e->slices_valid) {
+    GWG_CUDA_TRY(e->zslices.ensure(size_t(I8Cfg::SLICES) * n * kp));
+    GWG_CUDA_TRY(e->zscale.ensure(size_t(n) * sizeof(double)));
+    gwg::slice_basis_kernel<<<int(n), 256, 0, e->comp>>>(
+        e->basis.d(), e->np, int32_t(n), int32_t(n), int32_t(kp),
+        static_cast<int8_t*>(e->zslices.ptr), e->zscale.d());
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    e->slices_valid = true;
+  }
+  GWG_CUDA_TRY(e->xi8.ensure(size_t(cols) * kp));
+  gwg::i8_pack_kernel<<<blocks, 256, 0, e->comp>>>(
+      src, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
+      static_cast<unsigned long long*>(e->err.ptr) + 2);
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  if (int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
+                         e->split ? nullptr : e->rot.d(), e->rot_sq.d(), e->np, st))
+    return rc;
+  e->counters.preloop_flops += 2ull * uint64_t(n) * uint64_t(n) * uint64_t(cols);
+  e->slab_i8 = true;
+  return GWG_OK;
+}
+
+int launch_checksum(gwg_engine* e, const double* out, int64_t rows, int layout, int64_t i0,
+                    gwg_status* st) {
+  const bool numpy = layout == GWG_LAYOUT_NUMPY;
+  const int64_t outer = numpy ? rows : e->t, inner = numpy ? e->t : rows;
+  const int blocks = int(std::min<int64_t>(outer, int64_t(e->sms) * 8));
+  gwg::checksum_kernel<<<blocks, 256, 0, e->comp>>>(out, outer, inner, int32_t(e->p),
+                                                    numpy ? 1 : 0, i0,
+                                                    static_cast<unsigned long long*>(e->csum.ptr));
+  GWG_CUDA_TRY(cudaGetLastError());
+  e->counters.kernel_launches += 1;
+  e->csum_cells += uint64_t(rows) * uint64_t(e->t);
+  return GWG_OK;
+}
+
 bool rotated_x_unused(const gwg_engine* e) {
-  return e->snp_coding == GWG_SNP_GENOTYPES && e->split;
+  if (!e->split) return false;
+  if (e->i8_input) return e->snp_coding != GWG_SNP_REAL && e->n < kMaxGenotypeN;
+  return e->snp_coding == GWG_SNP_GENOTYPES;
 }
 
 void invalidate_derived(gwg_engine* e, bool spectrum) {
@@ -633,7 +713,16 @@ int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t 
 
 int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
                  double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
-  if (int rc = build_split(e, st)) return rc;
+  {
+    // The trait-derived operands (W, its slices, E/F) belong to the traits,
+    // not to this slab: they are built ungated, so a first slab that takes the
+    // FP64 path under GWG_SNP_AUTO cannot leave a stale W marked valid.
+    const int saved_gate = e->gate_want;
+    e->gate_want = -1;
+    const int rc = build_split(e, st);
+    e->gate_want = saved_gate;
+    if (rc) return rc;
+  }
   using gwg::I8Cfg;
   const int64_t t = e->t, p = e->p;
   const int64_t kp = round_up(e->n, I8Cfg::BK);
@@ -648,7 +737,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
 
   // ---- linear terms (int8 tcgen05) + solve ----
   // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
-  // c2 22.5 -> 20.9, c4 43.1 -> 40.4).  GWG_I8_CLUSTER=1|2|3 forces single
+  // c2 22.5 -> 20.9, c4 43.1 -> 40.4).  GWG_OPT_I8_CLUSTER = 1|2|3 forces single
   // CTAs / these B pairs / pairs on two W tiles multicasting the SNP tile —
   // the last measured slower even with one or two traits per tile (c4 33.2
   // -> 35.6 ms, p = 12 5.25 -> 5.62), so the SNP tile's L2 traffic is not
@@ -761,13 +850,19 @@ int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t
   const int ctas = int(std::min<int64_t>(tiles, e->sms));
   // S_BR through the factorised D (two DMMA GEMMs on X'.X'), then the grid
   // kernel without the D column and the X'.X' operand (GridCfg::EXT): 2np
-  // instead of 2n(p+1) flop per cell (GWG_REAL_SPLIT=0 keeps the single
+  // instead of 2n(p+1) flop per cell (GWG_OPT_REAL_SPLIT = 0 keeps the single
   // fused kernel).  Measured per step (fused -> split): c1 36.0 -> 32.3 ms,
   // c3 150 -> 127, c4 297 -> 287, p = 8 32.9 -> 30.7, p = 12 48.4 -> 46.3;
   // few traits keep the fused kernel (c0, t = 100: 1.26 vs 1.39 ms) — the
   // choice depends on t only, so results stay bitwise independent of slabs.
   if (e->real_split && e->lowrank && e->t >= 256) {
-    if (int rc = prepare_expsum(e, st)) return rc;
+    {
+      const int saved_gate = e->gate_want;  // trait operands: ungated (see launch_split)
+      e->gate_want = -1;
+      const int rc = prepare_expsum(e, st);
+      e->gate_want = saved_gate;
+      if (rc) return rc;
+    }
     if (e->sbr_terms > 0) {
       const int64_t ld_s = round_up(rows, 2);
       if (int rc = launch_sbr_stage(e, rot_sq, rows, ld_s, st)) return rc;
@@ -791,14 +886,18 @@ int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st) {
   return GWG_OK;
 }
 
-// Default streamed slab: whole waves of the persistent grid kernel
-// (tiles_m * tiles_t a multiple of the SM count) and ~64-128 MB of results.
+// Default streamed slab: ~96 MB of results per slab, in whole waves of the
+// persistent FP64 grid kernel (tiles_m * tiles_t a multiple of the SM count)
+// when a wave is that small; with many traits (a wave's results would be
+// tens of GB, c3: 3.2 MB per SNP) a multiple of 128 SNPs — the int8 kernels'
+// SNP tile — with at least 128.
 int64_t default_slab(const gwg_engine* e, int64_t m) {
   const int64_t tiles_t = ceil_div(e->t, int64_t(e->ops.bt) * e->ops.groups);
   const int64_t unit_tiles = e->sms / std::gcd<int64_t>(tiles_t, e->sms);
   const int64_t unit = unit_tiles * e->ops.bm;  // SNPs per whole-wave slab
   const int64_t target = std::max<int64_t>(1, (96ll << 20) / (e->t * e->p * 8));
-  return std::min(m, std::max<int64_t>(1, target / unit) * unit);
+  if (target >= unit) return std::min(m, target / unit * unit);
+  return std::min(m, std::max<int64_t>(128, target / 128 * 128));
 }
 
 // memcpy split over a few threads for large slabs (pageable user memory <->
@@ -833,13 +932,144 @@ int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
                     (long long)i, (long long)j);
 }
 
+
+// ---- shared-operand installs ------------------------------------------------
+
+int set_spectrum_impl(gwg_engine* e, const double* basis, int64_t ldb, const double* lambda,
+                      int where, gwg_status* st) {
+  if (!basis || !lambda) return set_status(st, GWG_DIMENSION, -1, -1, "null spectrum operand");
+  if (int rc = upload_cols(e, e->basis, basis, ldb, e->n, where, e->comp, st)) return rc;
+  if (int rc = upload(e, e->lambda, lambda, size_t(e->n), where, st)) return rc;
+  if (int rc = spectrum_range(e, st)) return rc;
+  e->have_spectrum = true;
+  e->have_covariates = false;
+  e->have_traits = false;
+  invalidate_derived(e, true);
+  return GWG_OK;
+}
+
+int set_covariates_impl(gwg_engine* e, const double* xl, int64_t ldx, int where, bool rotated,
+                        gwg_status* st) {
+  if (!e->have_spectrum)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_spectrum must come first");
+  const int64_t pm1 = e->p - 1;
+  GWG_CUDA_TRY(e->xl_rot.ensure(size_t(e->np) * std::max<int64_t>(pm1, 1) * sizeof(double)));
+  if (pm1 > 0) {
+    if (!xl) return set_status(st, GWG_DIMENSION, -1, -1, "null covariate block");
+    if (rotated) {
+      if (int rc = upload_cols(e, e->xl_rot, xl, ldx, pm1, where, e->comp, st)) return rc;
+    } else {
+      if (int rc = upload_cols(e, e->xl_raw, xl, ldx, pm1, where, e->comp, st)) return rc;
+      if (int rc = rotate(e, e->xl_raw.d(), pm1, e->xl_rot.d(), st)) return rc;
+    }
+  }
+  if (where != GWG_DEVICE)  // the caller may free or reuse its host block on return
+    GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  e->have_covariates = true;
+  e->have_traits = false;
+  invalidate_derived(e, false);
+  return GWG_OK;
+}
+
+// Traits: Y (raw or rotated, leading dimension ldy, on y_where) and h2/sigma2
+// (on s_where).  Nothing here waits for the device: the weight-floor verdict
+// stays in error word 0 until the next synchronising call reads it.
+int set_traits_impl(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int y_where,
+                    const double* h2, const double* sigma2, int s_where, bool rotated,
+                    gwg_status* st) {
+  if (!e->have_covariates)
+    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_covariates must come first");
+  if (t < 1 || t > (int64_t(1) << 30))
+    return set_status(st, GWG_DIMENSION, -1, -1, "trait count out of range (got %lld)",
+                      (long long)t);
+  if (!y || !h2 || !sigma2) return set_status(st, GWG_DIMENSION, -1, -1, "null trait operand");
+  e->have_traits = false;
+  invalidate_derived(e, false);
+  const int64_t n = e->n;
+  if (int rc = upload(e, e->h2, h2, size_t(t), s_where, st)) return rc;
+  if (int rc = upload(e, e->sigma2, sigma2, size_t(t), s_where, st)) return rc;
+  e->traits_host_valid = s_where == GWG_HOST;
+  e->range_pending = false;
+  if (e->traits_host_valid) {
+    e->h2_host.assign(h2, h2 + t);
+    e->s2_host.assign(sigma2, sigma2 + t);
+  } else if (e->lowrank && (e->snp_coding == GWG_SNP_REAL ? e->real_split : true)) {
+    // queue the exponential sum's range first (it needs only lambda, h2 and
+    // sigma2): the Y rotation and the context build queued behind it keep the
+    // device busy while the 48-byte answer travels, so the split grid's
+    // build finds it on the host without stalling the device
+    GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
+    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
+                                                      e->sigma2.d(), int32_t(t), e->exps.d());
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+    GWG_CUDA_TRY(cudaMemcpyAsync(e->range_host, e->exps.d(), 6 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, e->comp));
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_range, e->comp));
+    e->range_pending = true;
+  }
+  if (rotated) {
+    if (int rc = upload_cols(e, e->y_rot, y, ldy, t, y_where, e->comp, st)) return rc;
+  } else {
+    if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st)) return rc;
+    GWG_CUDA_TRY(e->y_rot.ensure(size_t(e->np) * t * sizeof(double)));
+    if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
+  }
+  const int64_t tiles_t = ceil_div(t, e->ops.bt);
+  const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
+  GWG_CUDA_TRY(e->bops.ensure(bops_doubles * sizeof(double)));
+  GWG_CUDA_TRY(e->ctx.ensure(size_t(t) * e->ops.ctx_stride * sizeof(double)));
+  if (t % e->ops.bt)  // padded traits of the last tile contribute zeros
+    GWG_CUDA_TRY(cudaMemsetAsync(e->bops.d() + size_t(tiles_t - 1) * e->np * (e->p + 1) *
+                                                   e->ops.bt,
+                                 0, size_t(e->np) * (e->p + 1) * e->ops.bt * sizeof(double),
+                                 e->comp));
+  GWG_CUDA_TRY(cudaMemsetAsync(e->err.ptr, 0xff, sizeof(unsigned long long), e->comp));
+  gwg::PrepArgs a;
+  a.n = n;
+  a.np = e->np;
+  a.t = int32_t(t);
+  a.lambda = e->lambda.d();
+  a.y = e->y_rot.d();
+  a.ldy = e->np;
+  a.xl = e->xl_rot.d();
+  a.ldxl = e->np;
+  a.h2 = e->h2.d();
+  a.sigma2 = e->sigma2.d();
+  a.bops = e->bops.d();
+  a.ctx = e->ctx.d();
+  a.trait_err = static_cast<unsigned long long*>(e->err.ptr);
+  // explicit genotype coding with the split grid never reads the FP64 grid's
+  // operand panels unless a pre-rotated slab arrives: built on demand then
+  // (launch_fused)
+  a.panels = (e->snp_coding == GWG_SNP_GENOTYPES && e->split) ? 0 : 1;
+  e->bops_valid = a.panels != 0;
+  e->prep_args = a;
+  GWG_CUDA_TRY(e->ops.prep(a, e->comp));
+  e->counters.kernel_launches += 1;
+  e->counters.context_builds += 1;
+  const uint64_t pm1 = uint64_t(e->p - 1);
+  e->counters.loop_flops += uint64_t(t) * uint64_t(n) * (5 + 3 * pm1 + pm1 * pm1);
+  // host operands are consumed before the call returns (the caller owns and
+  // may reuse them, like the reference's synchronous load_pass); device
+  // operands stay asynchronous
+  if (y_where == GWG_HOST || s_where == GWG_HOST) GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  e->t = t;
+  e->have_traits = true;
+  return GWG_OK;
+}
+
 }  // namespace gwg_host
 
 using namespace gwg_host;
 
 extern "C" {
 
-const char* gwg_version(void) { return "gwgrid_cuda 0.1.0 sm_100a"; }
+const char* gwg_version(void) { return "gwgrid_cuda 0.2.0 sm_100a"; }
+
+uint64_t gwg_cell_hash(int64_t i, int64_t j, int64_t c, uint64_t bits) {
+  return gwg::cell_term(gwg::cell_key(uint64_t(i), uint64_t(j)), uint64_t(c), bits);
+}
 
 gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* st) {
   clear_status(st);
@@ -872,17 +1102,9 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   e->np = round_up(n, kBK);
   e->ops = ops;
   e->lops = lops;
-  {
-    const char* v = std::getenv("GWG_SBR_CFG");
-    e->sops = gwg::sbr_ops(v ? std::atoi(v) : 0);
-  }
-  if (const char* sp = std::getenv("GWG_SPLIT")) e->split = std::atoi(sp) != 0;
-  if (const char* sd = std::getenv("GWG_SBR_DIRECT")) e->lowrank = std::atoi(sd) == 0;
-  if (const char* rs = std::getenv("GWG_REAL_SPLIT")) e->real_split = std::atoi(rs) != 0;
-  if (const char* cl = std::getenv("GWG_I8_CLUSTER")) {
-    const int v = std::atoi(cl);
-    e->i8_cluster = v >= 1 && v <= 3 ? v : 0;
-  }
+  // The numerics are fixed by the engine's options alone (gwg_set_option),
+  // never by the caller's environment.
+  e->sops = gwg::sbr_ops(0);
   auto bail = [&](const char* what, cudaError_t err) {
     set_status(st, GWG_CUDA, -1, -1, "%s: %s", what, cudaGetErrorString(err));
     gwg_engine_destroy(e);
@@ -936,7 +1158,7 @@ void gwg_engine_destroy(gwg_engine* e) {
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
                     &e->wslices, &e->wscale, &e->dpanel, &e->sbr, &e->epanel, &e->fpanel,
-                    &e->gmat, &e->exps, &e->xepanel, &e->umat})
+                    &e->gmat, &e->exps, &e->xepanel, &e->umat, &e->raw8[0], &e->raw8[1], &e->csum})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   if (e->range_host) cudaFreeHost(e->range_host);
@@ -947,9 +1169,13 @@ void gwg_engine_destroy(gwg_engine* e) {
     if (e->ev_comp[b]) cudaEventDestroy(e->ev_comp[b]);
     if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
   }
-  for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2]})
+  for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2],
+                         e->ev_wait})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->pipe_events) cudaEventDestroy(ev);
+  for (PinBuf& b : e->pin_x) b.release();
+  for (PinBuf& b : e->pin_res) b.release();
   if (e->comp) cudaStreamDestroy(e->comp);
   if (e->h2d) cudaStreamDestroy(e->h2d);
   if (e->d2h) cudaStreamDestroy(e->d2h);
@@ -960,15 +1186,7 @@ int32_t gwg_set_spectrum(gwg_engine* e, const double* basis, const double* lambd
                          gwg_status* st) {
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
-  if (!basis || !lambda) return set_status(st, GWG_DIMENSION, -1, -1, "null spectrum operand");
-  if (int rc = upload_cols(e, e->basis, basis, e->n, e->n, where, e->comp, st)) return rc;
-  if (int rc = upload(e, e->lambda, lambda, size_t(e->n), where, st)) return rc;
-  if (int rc = spectrum_range(e, st)) return rc;
-  e->have_spectrum = true;
-  e->have_covariates = false;
-  e->have_traits = false;
-  invalidate_derived(e, true);
-  return GWG_OK;
+  return set_spectrum_impl(e, basis, e ? e->n : 0, lambda, where, st);
 }
 
 extern "C" int32_t gwg_internal_device_eig(double* a, int64_t n, int64_t lda, double* w,
@@ -993,20 +1211,7 @@ int32_t gwg_set_kinship(gwg_engine* e, const double* phi, int32_t where, gwg_sta
 int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_status* st) {
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
-  if (!e->have_spectrum)
-    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_spectrum must come first");
-  const int64_t pm1 = e->p - 1;
-  GWG_CUDA_TRY(e->xl_rot.ensure(size_t(e->np) * std::max<int64_t>(pm1, 1) * sizeof(double)));
-  if (pm1 > 0) {
-    if (!xl) return set_status(st, GWG_DIMENSION, -1, -1, "null covariate block");
-    if (int rc = upload_cols(e, e->xl_raw, xl, e->n, pm1, where, e->comp, st)) return rc;
-    if (int rc = rotate(e, e->xl_raw.d(), pm1, e->xl_rot.d(), st)) return rc;
-  }
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
-  e->have_covariates = true;
-  e->have_traits = false;
-  invalidate_derived(e, false);
-  return GWG_OK;
+  return set_covariates_impl(e, xl, e->n, where, false, st);
 }
 
 int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* h2,
@@ -1014,88 +1219,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
   NvtxRange nvtx_("gwg_set_traits");
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
-  if (!e->have_covariates)
-    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_covariates must come first");
-  if (t < 1 || t > (int64_t(1) << 30))
-    return set_status(st, GWG_DIMENSION, -1, -1, "trait count out of range (got %lld)",
-                      (long long)t);
-  if (!y || !h2 || !sigma2) return set_status(st, GWG_DIMENSION, -1, -1, "null trait operand");
-  e->have_traits = false;
-  invalidate_derived(e, false);
-  const int64_t n = e->n;
-  if (is_rotated) {
-    if (int rc = upload_cols(e, e->y_rot, y, n, t, where, e->comp, st)) return rc;
-  } else {
-    if (int rc = upload_cols(e, e->y_raw, y, n, t, where, e->comp, st)) return rc;
-    GWG_CUDA_TRY(e->y_rot.ensure(size_t(e->np) * t * sizeof(double)));
-    if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
-  }
-  if (int rc = upload(e, e->h2, h2, size_t(t), where, st)) return rc;
-  if (int rc = upload(e, e->sigma2, sigma2, size_t(t), where, st)) return rc;
-  e->traits_host_valid = where == GWG_HOST;
-  e->range_pending = false;
-  if (e->traits_host_valid) {
-    e->h2_host.assign(h2, h2 + t);
-    e->s2_host.assign(sigma2, sigma2 + t);
-  } else if (e->lowrank && (e->snp_coding == GWG_SNP_REAL ? e->real_split : true)) {
-    // queue the exponential sum's range now: by the time the split grid is
-    // built the 48-byte answer is on the host and no round trip stalls it
-    GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
-    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
-                                                      e->sigma2.d(), int32_t(t), e->exps.d());
-    GWG_CUDA_TRY(cudaGetLastError());
-    e->counters.kernel_launches += 1;
-    GWG_CUDA_TRY(cudaMemcpyAsync(e->range_host, e->exps.d(), 6 * sizeof(double),
-                                 cudaMemcpyDeviceToHost, e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_range, e->comp));
-    e->range_pending = true;
-  }
-  const int64_t tiles_t = ceil_div(t, e->ops.bt);
-  const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
-  GWG_CUDA_TRY(e->bops.ensure(bops_doubles * sizeof(double)));
-  GWG_CUDA_TRY(e->ctx.ensure(size_t(t) * e->ops.ctx_stride * sizeof(double)));
-  if (t % e->ops.bt)  // padded traits of the last tile contribute zeros
-    GWG_CUDA_TRY(cudaMemsetAsync(e->bops.d() + size_t(tiles_t - 1) * e->np * (e->p + 1) *
-                                                   e->ops.bt,
-                                 0, size_t(e->np) * (e->p + 1) * e->ops.bt * sizeof(double),
-                                 e->comp));
-  if (int rc = reset_errors(e, st)) return rc;
-  gwg::PrepArgs a;
-  a.n = n;
-  a.np = e->np;
-  a.t = int32_t(t);
-  a.lambda = e->lambda.d();
-  a.y = e->y_rot.d();
-  a.ldy = e->np;
-  a.xl = e->xl_rot.d();
-  a.ldxl = e->np;
-  a.h2 = e->h2.d();
-  a.sigma2 = e->sigma2.d();
-  a.bops = e->bops.d();
-  a.ctx = e->ctx.d();
-  a.trait_err = static_cast<unsigned long long*>(e->err.ptr);
-  // explicit genotype coding with the split grid never reads the FP64 grid's
-  // operand panels unless a pre-rotated slab arrives: built on demand then
-  // (launch_fused)
-  a.panels = (e->snp_coding == GWG_SNP_GENOTYPES && e->split) ? 0 : 1;
-  e->bops_valid = a.panels != 0;
-  e->prep_args = a;
-  GWG_CUDA_TRY(e->ops.prep(a, e->comp));
-  e->counters.kernel_launches += 1;
-  e->counters.context_builds += 1;
-  const uint64_t pm1 = uint64_t(e->p - 1);
-  e->counters.loop_flops += uint64_t(t) * uint64_t(n) * (5 + 3 * pm1 + pm1 * pm1);
-  if (int rc = read_errors(e, st, true)) return rc;
-  if (e->err_host[0] != ~0ull) {
-    const int64_t j = int64_t(e->err_host[0]);
-    return set_status(st, GWG_NOT_POSITIVE_DEFINITE, -1, j,
-                      "trait covariance is not positive definite in the rotated basis: a "
-                      "weight entry is below the relative floor (trait %lld)",
-                      (long long)j);
-  }
-  e->t = t;
-  e->have_traits = true;
-  return GWG_OK;
+  return set_traits_impl(e, t, y, e->n, where, h2, sigma2, where, is_rotated != 0, st);
 }
 
 int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* x_r,
@@ -1122,6 +1246,9 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   if (is_rotated || !rotated_x_unused(e))
     GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
+  // before the rotation: it writes this slab's genotype verdict (word 2)
+  if (int rc = reset_errors(e, st)) return rc;
+  e->i8_input = false;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
   if (is_rotated) {
     if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;
@@ -1146,7 +1273,6 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
   const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : (out_where == GWG_DEVICE ? ldo : mb);
   const int64_t m_total = i0 + mb;
-  if (int rc = reset_errors(e, st)) return rc;
   e->split_timed = false;
   GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
   if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), mb, i0, m_total, dev_out, si, sj, st))
@@ -1163,7 +1289,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     }
     e->counters.bytes_stored += uint64_t(mb) * t * p * 8;
   }
-  if (int rc = read_errors(e, st, false)) return rc;
+  if (int rc = read_errors(e, st)) return rc;
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
   if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
@@ -1174,137 +1300,6 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   }
   // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
   return raise_cell_error(e, m_total, st);
-}
-
-int32_t gwg_run_grid(gwg_engine* e, int64_t m, const double* x_r_host, double* b_host,
-                     const gwg_run_options* opts, gwg_counters* counters, gwg_status* st) {
-  NvtxRange nvtx_("gwg_run_grid");
-  clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
-  if (!e->have_traits)
-    return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_traits must come first");
-  if (m < 1 || !x_r_host || !b_host)
-    return set_status(st, GWG_DIMENSION, -1, -1, "bad run_grid arguments (m=%lld)",
-                      (long long)m);
-  const auto wall0 = std::chrono::steady_clock::now();
-  const int64_t n = e->n, t = e->t, p = e->p;
-  const int layout = opts ? opts->layout : GWG_LAYOUT_NUMPY;
-  if (layout != GWG_LAYOUT_NUMPY && layout != GWG_LAYOUT_STREAM)
-    return set_status(st, GWG_DIMENSION, -1, -1, "unknown layout %d", layout);
-  const bool dbuf = opts ? opts->double_buffer != 0 : true;
-  // Default slab: whole waves of the persistent grid (tiles_m * tiles_t a
-  // multiple of the SM count) and ~64-128 MB of results per slab.
-  const int64_t mb = opts && opts->mb > 0 ? std::min(opts->mb, m) : default_slab(e, m);
-  const int nbuf = dbuf ? 2 : 1;
-
-  const size_t x_bytes = size_t(n) * m * sizeof(double);
-  const size_t b_bytes = size_t(m) * t * p * sizeof(double);
-  // Fully pinned buffers (both ends inside page-locked memory) take the direct
-  // async path.  Anything else goes through the staged pipeline's own pinned
-  // bounce buffers: registering arbitrary user memory in place is unsafe when
-  // a neighbouring allocation already registered part of its pages.
-  const bool direct =
-      is_pinned_host(x_r_host) &&
-      is_pinned_host(reinterpret_cast<const char*>(x_r_host) + x_bytes - 1) &&
-      is_pinned_host(b_host) && is_pinned_host(reinterpret_cast<const char*>(b_host) + b_bytes - 1);
-  if (!direct) {
-    SlabRead rd = [&](int64_t i0, int64_t rows, double* dst) {
-      parallel_copy(dst, x_r_host + size_t(i0) * n, size_t(n) * rows * 8);
-      return true;
-    };
-    SlabWrite wr = [&](int64_t i0, int64_t rows, const double* src) {
-      if (layout == GWG_LAYOUT_NUMPY) {
-        parallel_copy(b_host + size_t(i0) * t * p, src, size_t(rows) * t * p * 8);
-      } else {
-        for (int64_t j = 0; j < t; ++j)
-          std::memcpy(b_host + (size_t(j) * m + i0) * p, src + size_t(j) * rows * p,
-                      size_t(rows) * p * 8);
-      }
-      return true;
-    };
-    uint64_t loaded = 0, stored = 0;
-    const int rc = staged_pipeline(e, m, mb, false, layout, rd, wr, &loaded, &stored, nullptr, st);
-    if (rc != GWG_OK) return rc;
-    e->counters.bytes_loaded += loaded;
-    e->counters.bytes_stored += stored;
-    e->counters.wall_ms =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0)
-            .count();
-    if (counters) *counters = e->counters;
-    return raise_cell_error(e, m, st);
-  }
-
-  for (int b = 0; b < nbuf; ++b) {
-    GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));
-    GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
-  }
-  if (!rotated_x_unused(e)) GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
-  GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
-  const int64_t slabs = ceil_div(m, mb);
-  while (int64_t(e->slab_events.size()) < 2 * slabs) {
-    cudaEvent_t ev;
-    GWG_CUDA_TRY(cudaEventCreate(&ev));
-    e->slab_events.push_back(ev);
-  }
-  if (int rc = reset_errors(e, st)) return rc;
-  // Fresh pipeline: make the side streams wait for everything already queued.
-  for (int b = 0; b < 2; ++b) {
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], e->comp));
-  }
-  for (int64_t s = 0; s < slabs; ++s) {
-    const int b = int(s % nbuf);
-    const int64_t i0 = s * mb;
-    const int64_t rows = std::min(mb, m - i0);
-    cudaStream_t up = dbuf ? e->h2d : e->comp;
-    cudaStream_t down = dbuf ? e->d2h : e->comp;
-    // H2D of the raw slab (one flat copy for even n) once the rotation of
-    // slab s - nbuf released raw[b].
-    GWG_CUDA_TRY(cudaStreamWaitEvent(up, e->ev_rot_done[b], 0));
-    if (int rc = upload_cols(e, e->raw[b], x_r_host + size_t(i0) * n, n, rows, GWG_HOST, up, st,
-                             raw_ld(e)))
-      return rc;
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_h2d[b], up));
-    // Compute: rotate + fused grid once the slab landed and out[b] drained.
-    GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
-    GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
-    if (int rc = rotate_snps(e, e->raw[b].d(), raw_ld(e), rows, st)) return rc;
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
-    const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
-    const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : rows;
-    if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), rows, i0, m, e->out[b].d(), si, sj, st))
-      return rc;
-    GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s + 1], e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_comp[b], e->comp));
-    // D2H of the slab's results.
-    GWG_CUDA_TRY(cudaStreamWaitEvent(down, e->ev_comp[b], 0));
-    if (layout == GWG_LAYOUT_NUMPY) {
-      GWG_CUDA_TRY(cudaMemcpyAsync(b_host + size_t(i0) * t * p, e->out[b].ptr,
-                                   size_t(rows) * t * p * sizeof(double),
-                                   cudaMemcpyDeviceToHost, down));
-    } else {
-      GWG_CUDA_TRY(cudaMemcpy2DAsync(b_host + size_t(i0) * p, size_t(m) * p * sizeof(double),
-                                     e->out[b].ptr, size_t(rows) * p * sizeof(double),
-                                     size_t(rows) * p * sizeof(double), t,
-                                     cudaMemcpyDeviceToHost, down));
-    }
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], down));
-    e->counters.bytes_stored += uint64_t(rows) * t * p * 8;
-  }
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
-  if (int rc = read_errors(e, st, false)) return rc;
-  for (int64_t s = 0; s < slabs; ++s) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, e->slab_events[2 * s], e->slab_events[2 * s + 1]) ==
-        cudaSuccess)
-      e->counters.grid_kernel_ms += ms;
-  }
-  e->counters.wall_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
-  if (counters) *counters = e->counters;
-  return raise_cell_error(e, m, st);
 }
 
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
@@ -1319,6 +1314,60 @@ int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
   return GWG_OK;
 }
 
+int32_t gwg_set_option(gwg_engine* e, int32_t option, int64_t value, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  auto flag = [&](bool& dst) -> int {
+    if (value != 0 && value != 1)
+      return set_status(st, GWG_DIMENSION, -1, -1, "option %d takes 0 or 1 (got %lld)",
+                        int(option), (long long)value);
+    dst = value != 0;
+    return GWG_OK;
+  };
+  switch (option) {
+    case GWG_OPT_SPLIT:
+      return flag(e->split);
+    case GWG_OPT_SBR_DIRECT: {
+      bool direct = !e->lowrank;
+      if (int rc = flag(direct)) return rc;
+      if (direct == e->lowrank) invalidate_derived(e, false);  // E/F, W and D panels
+      e->lowrank = !direct;
+      return GWG_OK;
+    }
+    case GWG_OPT_REAL_SPLIT:
+      return flag(e->real_split);
+    case GWG_OPT_I8_CLUSTER:
+      if (value < 0 || value > 3)
+        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_I8_CLUSTER takes 0..3 (got %lld)",
+                          (long long)value);
+      e->i8_cluster = int(value);
+      return GWG_OK;
+    case GWG_OPT_SBR_CFG:
+      if (value < 0 || value >= gwg::kSbrConfigs)
+        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_SBR_CFG takes 0..%d (got %lld)",
+                          gwg::kSbrConfigs - 1, (long long)value);
+      if (int(value) != e->sbr_cfg) invalidate_derived(e, false);  // panel tiling changes
+      e->sbr_cfg = int(value);
+      e->sops = gwg::sbr_ops(e->sbr_cfg);
+      return GWG_OK;
+  }
+  return set_status(st, GWG_DIMENSION, -1, -1, "unknown option %d", int(option));
+}
+
+int32_t gwg_get_option(gwg_engine* e, int32_t option, int64_t* value, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!value) return set_status(st, GWG_DIMENSION, -1, -1, "null option value");
+  switch (option) {
+    case GWG_OPT_SPLIT: *value = e->split; return GWG_OK;
+    case GWG_OPT_SBR_DIRECT: *value = !e->lowrank; return GWG_OK;
+    case GWG_OPT_REAL_SPLIT: *value = e->real_split; return GWG_OK;
+    case GWG_OPT_I8_CLUSTER: *value = e->i8_cluster; return GWG_OK;
+    case GWG_OPT_SBR_CFG: *value = e->sbr_cfg; return GWG_OK;
+  }
+  return set_status(st, GWG_DIMENSION, -1, -1, "unknown option %d", int(option));
+}
+
 int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out) {
   if (!e || !out) return GWG_DIMENSION;
   *out = e->counters;
@@ -1326,15 +1375,23 @@ int32_t gwg_get_counters(gwg_engine* e, gwg_counters* out) {
 }
 
 void gwg_reset_counters(gwg_engine* e) {
-  if (e) e->counters = gwg_counters{};
+  if (!e) return;
+  e->counters = gwg_counters{};
+  e->csum_cells = 0;
+  if (e->csum.ptr) {
+    cudaSetDevice(e->device);
+    cudaMemsetAsync(e->csum.ptr, 0, sizeof(unsigned long long), e->comp);
+  }
 }
 
 int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
   clear_status(st);
   if (int rc = check_engine(e, st)) return rc;
-  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
+  // a trait failure queued by gwg_set_traits surfaces here at the latest
+  if (e->have_traits) return read_errors(e, st);
+  GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   return GWG_OK;
 }
 

@@ -55,6 +55,27 @@ struct DevBuf {
   double* d() const { return static_cast<double*>(ptr); }
 };
 
+// Page-locked host buffer kept by the engine across runs (cudaMallocHost is
+// slow: the pipeline's staging buffers are allocated once and reused).
+struct PinBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
 
 int set_status(gwg_status* st, int code, int64_t snp, int64_t trait, const char* fmt, ...);
 void clear_status(gwg_status* st);
@@ -83,7 +104,18 @@ struct gwg_engine {
   gwg::PrepArgs prep_args{};  // the last trait prep (rerun with panels on demand)
 
   gwg_host::DevBuf raw[2], rot, rot_sq, out[2], stage;  // rot / rot_sq: X' and X'.X', ld np
+  gwg_host::DevBuf raw8[2];  // int8 genotype slabs (GWG_FORMAT_I8), n x rows, ld n
   gwg_host::DevBuf err;  // [0] trait error key, [1] cell error key, [2] genotype check
+  // the run's SNP slabs came as int8 codes: a code outside [-127, 127] is an
+  // error whatever the coding (err word 2)
+  bool i8_input = false;
+  // order-independent result checksum (gwg_run_options.checksum): [0] sum
+  gwg_host::DevBuf csum;
+  uint64_t csum_cells = 0;
+  // pinned staging of the slab pipeline (pipeline.cu), reused across runs
+  gwg_host::PinBuf pin_x[2];
+  std::vector<gwg_host::PinBuf> pin_res;
+  std::vector<cudaEvent_t> pipe_events;  // host-buffer hand-off events
   // SNP coding: 0 = real-valued (DMMA rotation), 1 = integer genotype codes
   // (exact int8 tcgen05 rotation); slices of Z are rebuilt after a new spectrum.
   int snp_coding = GWG_SNP_AUTO;
@@ -91,8 +123,7 @@ struct gwg_engine {
   gwg_host::DevBuf zslices, zscale, xi8;
   // Split grid for genotype slabs (grid_split.cuh): linear terms x_i^T W on
   // the int8 tensor cores fused with the solve, quadratic term S_BR on DMMA.
-  // `split` = use it
-  // (GWG_SPLIT=0 in the environment turns it off for A/B timing);
+  // `split` = use it (GWG_OPT_SPLIT);
   // `slab_i8` = the current slab was rotated from integer codes (xi8 valid).
   bool split = true, slab_i8 = false;
   // GWG_SNP_AUTO: the current slab queued both paths, each gated on its
@@ -100,20 +131,21 @@ struct gwg_engine {
   // (1 genotype, 0 FP64, -1 ungated)
   bool slab_auto = false;
   int gate_want = -1;
-  // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs multicasting B
-  // (GWG_I8_CLUSTER)
+  // int8 kernels: 0 auto, 1 single CTAs, 2 CTA pairs multicasting B, 3 CTA
+  // pairs multicasting the SNP tile (GWG_OPT_I8_CLUSTER)
   int i8_cluster = 0;
+  int sbr_cfg = 0;  // GWG_OPT_SBR_CFG
   bool basis_t_valid = false, split_valid = false;
   gwg_host::DevBuf basis_t, vmat, wmat, wslices, wscale, dpanel, sbr;
   // S_BR = ((X'.X')^T E) F, the positive exponential-sum factorisation of D
   // (expsum.cpp): `sbr_terms` = r for the current traits, 0 = direct DMMA
   // contraction against D (inputs outside the factorisation's range, or
-  // GWG_SBR_DIRECT=1 in the environment: `lowrank` = false).
+  // GWG_OPT_SBR_DIRECT = 1: `lowrank` = false).
   bool lowrank = true;
   int32_t sbr_terms = 0;
   bool expsum_valid = false;  // E, F (and sbr_terms) built for the current traits
   // FP64 path: S_BR from the factorised GEMMs and the grid kernel without the
-  // D column (GWG_REAL_SPLIT=0 in the environment keeps the fused S_BR)
+  // D column (GWG_OPT_REAL_SPLIT = 0 keeps the fused S_BR)
   bool real_split = true;
   gwg_host::DevBuf epanel, fpanel, gmat, exps;
   gwg_host::DevBuf xepanel, umat;  // W build through the factorisation: diag(X_L'_c) E, Z diag(X_L'_c) E
@@ -136,6 +168,7 @@ struct gwg_engine {
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
   cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
+  cudaEvent_t ev_wait = nullptr;  // gwg_wait_stream
   cudaEvent_t ev_s[3];     // split grid: before gls_sbr, before linear_solve, after it
   bool split_timed = false;
   std::vector<cudaEvent_t> slab_events;
@@ -178,7 +211,13 @@ int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t
 void invalidate_derived(gwg_engine* e, bool spectrum);
 // SNP slab -> e->rot / e->rot_sq with the engine's SNP coding (DMMA or int8).
 int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg_status* st);
-int read_errors(gwg_engine* e, gwg_status* st, bool trait_only);
+// Copy the error words to the host (one sync) and report, in this order: a
+// pending trait weight-floor failure (-1, j), an int8 code outside
+// [-127, 127] (or, for GWG_SNP_GENOTYPES, a non-code value); cell errors are
+// left to raise_cell_error.
+int read_errors(gwg_engine* e, gwg_status* st);
+// Reset the per-slab words (cell key, genotype verdict); the trait word is
+// reset by set_traits only.
 int reset_errors(gwg_engine* e, gwg_status* st);
 int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
@@ -188,13 +227,57 @@ int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st);
 int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st);
 int64_t default_slab(const gwg_engine* e, int64_t m);
 
-// Staged slab pipeline (stream_io.cu): read_fn fills a pinned n x rows slab
-// (ld n); write_fn drains a pinned result slab in out_layout order
-// (NUMPY: (il*t + j)*p; STREAM: (j*rows + il)*p).
-using SlabRead = std::function<bool(int64_t i0, int64_t rows, double* dst)>;
+// The slab pipeline (pipeline.cu), run_grid's traversal on the device.
+// Input: slab s arrives either straight from a pinned host array (x_direct,
+// column-major, ld n, element size by format) or through read_fn, which
+// fills a pinned n x rows staging slab (ld n) on a reader thread.  Output:
+// either straight into a pinned host array (b_direct; NUMPY rows at
+// il * t * p, STREAM at (j * ldb + il) * p) or through write_fn, which drains
+// a pinned slab-local result buffer (NUMPY (il*t + j)*p, STREAM
+// (j*rows + il)*p) on a writer thread.  i0 arguments of the callbacks are
+// local to the run (0 = x's first column).
+using SlabRead = std::function<bool(int64_t i0, int64_t rows, void* dst)>;
 using SlabWrite = std::function<bool(int64_t i0, int64_t rows, const double* src)>;
-int staged_pipeline(gwg_engine* e, int64_t m, int64_t mb, bool rotated, int out_layout,
-                    const SlabRead& read_fn, const SlabWrite& write_fn, uint64_t* loaded,
-                    uint64_t* stored, int* io_error, gwg_status* st);
+struct PipeSpec {
+  int64_t m = 0;         // SNP columns of this run
+  int64_t i0 = 0;        // global SNP index of its first column
+  int64_t mb = 0;        // slab width
+  int fmt = GWG_FORMAT_F64;
+  bool rotated = false;  // f64 slabs already rotated (the FP64 path)
+  int layout = GWG_LAYOUT_NUMPY;
+  bool dbuf = true;
+  int ring = 2;          // pinned result buffers behind write_fn
+  bool checksum = false;
+  const void* x_direct = nullptr;
+  SlabRead read_fn;
+  double* b_direct = nullptr;
+  int64_t ldb = 0;       // STREAM layout row length of b_direct (cells)
+  SlabWrite write_fn;
+};
+struct PipeStats {
+  uint64_t loaded = 0, stored = 0;
+  double stall_ms = 0.0;
+  int io_error = 0;      // 1 = read_fn failed, 2 = write_fn failed
+};
+int run_pipeline(gwg_engine* e, const PipeSpec& spec, PipeStats* stats, gwg_status* st);
+// gwg_run_grid's argument checks and spec (shared with the device group)
+int run_grid_impl(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host,
+                  const gwg_run_options* opts, gwg_counters* counters, gwg_status* st);
+// memcpy over a few threads (pageable user memory <-> pinned staging)
+void parallel_copy(void* dst, const void* src, size_t bytes);
+// Shared-operand installs with explicit leading dimensions and locations (the
+// device group broadcasts device-resident, already rotated operands).
+int set_spectrum_impl(gwg_engine* e, const double* basis, int64_t ldb, const double* lambda,
+                      int where, gwg_status* st);
+int set_covariates_impl(gwg_engine* e, const double* xl, int64_t ldx, int where, bool rotated,
+                        gwg_status* st);
+int set_traits_impl(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int y_where,
+                    const double* h2, const double* sigma2, int s_where, bool rotated,
+                    gwg_status* st);
+// int8 genotype slab (n x cols, ld n) -> e->rot_sq (and xi8) with the engine's coding
+int rotate_snps_i8(gwg_engine* e, const int8_t* src, int64_t cols, gwg_status* st);
+// accumulate the result checksum of one slab-local result buffer
+int launch_checksum(gwg_engine* e, const double* out, int64_t rows, int layout, int64_t i0,
+                    gwg_status* st);
 
 }  // namespace gwg_host

@@ -13,7 +13,7 @@
 //       G = (X'.X')^T E stored [SNP][r] (rowmajor), then S_BR = G F, 2r(n+t)
 //       flop per SNP; S_BR is stored [trait][SNP].
 //   linear_solve_kernel<P> (linear_solve.cuh): x_i^T W exactly on the int8
-//       tensor cores against eight 7-bit slices of W (tcgen05.mma kind::i8,
+//       tensor cores against seven signed 8-bit slices of W (tcgen05.mma kind::i8,
 //       TMEM accumulators, exact int64 recombination), and in the same
 //       epilogue the bordered Cholesky solve against S_BR and the per-trait
 //       context (solve_cell), b_ij out by TMA store.  The FP64 pipe is idle
@@ -253,6 +253,7 @@ SbrOps make_sbr_ops() {
   return o;
 }
 // variant 0 = SbrDefault (64 SNPs x 64 traits); 1 = 128 x 40; 2 = 64 x 40
+constexpr int kSbrConfigs = 3;
 SbrOps sbr_ops(int variant);
 
 }  // namespace gwg

@@ -19,6 +19,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cerrno>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -88,10 +89,13 @@ struct Fd {
   }
 };
 
+// Positional I/O that retries interrupted calls and short transfers, like
+// the reference's read_exact / write_exact (proj/src/stream.cpp:47-81).
 bool pread_all(int fd, void* dst, size_t bytes, uint64_t off) {
   char* p = static_cast<char*>(dst);
   while (bytes) {
     const ssize_t r = ::pread(fd, p, bytes, off_t(off));
+    if (r < 0 && errno == EINTR) continue;
     if (r <= 0) return false;
     p += r;
     bytes -= size_t(r);
@@ -104,6 +108,7 @@ bool pwrite_all(int fd, const void* src, size_t bytes, uint64_t off) {
   const char* p = static_cast<const char*>(src);
   while (bytes) {
     const ssize_t r = ::pwrite(fd, p, bytes, off_t(off));
+    if (r < 0 && errno == EINTR) continue;
     if (r <= 0) return false;
     p += r;
     bytes -= size_t(r);
@@ -161,28 +166,6 @@ int open_stream(const char* path, int expected_kind, Fd& f, Header& h, gwg_statu
   return GWG_OK;
 }
 
-// A binary semaphore per buffer, for the reader/writer hand-offs.
-struct Slot {
-  std::mutex mu;
-  std::condition_variable cv;
-  int64_t ready = -1;  // slab index whose data is ready for the consumer
-  int64_t freed = -1;  // last slab index the consumer released
-  void publish(int64_t s) {
-    { std::lock_guard<std::mutex> l(mu); ready = s; }
-    cv.notify_all();
-  }
-  void release(int64_t s) {
-    { std::lock_guard<std::mutex> l(mu); freed = s; }
-    cv.notify_all();
-  }
-  template <class Pred>
-  bool wait(Pred pred, const std::atomic<bool>& abort) {
-    std::unique_lock<std::mutex> l(mu);
-    cv.wait(l, [&] { return pred() || abort.load(); });
-    return !abort.load();
-  }
-};
-
 }  // namespace
 
 extern "C" {
@@ -228,161 +211,6 @@ int32_t gwg_set_traits_file(gwg_engine* e, const char* traits_path, gwg_status* 
 
 }  // extern "C"
 
-namespace gwg_host {
-
-// The staged slab pipeline shared by the file legs and by gwg_run_grid on
-// pageable host memory: a reader thread fills pinned hx[s%2] (read_fn), the
-// coordinator runs H2D -> rotate (or square, for rotated input) -> fused grid
-// -> D2H into pinned hres[s%2], a writer thread drains it (write_fn).  CUDA
-// events hand buffer ownership between the three agents, exactly the
-// two-workspace discipline of pipeline_run (pipeline.hpp:62-137).
-int staged_pipeline(gwg_engine* e, int64_t m, int64_t mb, bool rotated, int out_layout,
-                    const SlabRead& read_fn, const SlabWrite& write_fn, uint64_t* loaded_out,
-                    uint64_t* stored_out, int* io_error_out, gwg_status* st) {
-  const int64_t n = e->n, t = e->t, p = e->p;
-  double* hx[2] = {nullptr, nullptr};
-  double* hres[2] = {nullptr, nullptr};
-  struct Pinned {
-    double** a;
-    double** b;
-    ~Pinned() {
-      for (int i = 0; i < 2; ++i) {
-        if (a[i]) cudaFreeHost(a[i]);
-        if (b[i]) cudaFreeHost(b[i]);
-      }
-    }
-  } pinned{hx, hres};
-  for (int b = 0; b < 2; ++b) {
-    GWG_CUDA_TRY(cudaMallocHost(&hx[b], size_t(n) * mb * sizeof(double)));
-    GWG_CUDA_TRY(cudaMallocHost(&hres[b], size_t(mb) * t * p * sizeof(double)));
-    GWG_CUDA_TRY(e->raw[b].ensure(size_t(raw_ld(e)) * mb * sizeof(double)));
-    GWG_CUDA_TRY(e->out[b].ensure(size_t(mb) * t * p * sizeof(double)));
-  }
-  if (rotated || !rotated_x_unused(e))
-    GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
-  GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
-  if (int rc = reset_errors(e, st)) return rc;
-  for (int b = 0; b < 2; ++b) {
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], e->comp));
-    GWG_CUDA_TRY(cudaEventRecord(e->ev_h2d[b], e->comp));
-  }
-  const int64_t slabs = ceil_div(m, mb);
-  while (int64_t(e->slab_events.size()) < 2 * slabs) {
-    cudaEvent_t ev;
-    GWG_CUDA_TRY(cudaEventCreate(&ev));
-    e->slab_events.push_back(ev);
-  }
-  Slot xs[2], rs[2];
-  std::atomic<bool> abort{false};
-  std::atomic<int> io_error{0};  // 1 = read, 2 = write
-  std::atomic<uint64_t> loaded{0}, stored{0};
-  auto wake_all = [&] {
-    for (auto& q : xs) q.cv.notify_all();
-    for (auto& q : rs) q.cv.notify_all();
-  };
-
-  std::thread reader([&] {
-    for (int64_t s = 0; s < slabs && !abort.load(); ++s) {
-      const int b = int(s & 1);
-      // the H2D of slab s-2 out of hx[b] must have completed
-      if (!xs[b].wait([&] { return xs[b].freed >= s - 2; }, abort)) return;
-      if (s >= 2) cudaEventSynchronize(e->ev_h2d[b]);
-      const int64_t i0 = s * mb, rows = std::min(mb, m - i0);
-      if (!read_fn(i0, rows, hx[b])) {
-        io_error = 1;
-        abort = true;
-        wake_all();
-        return;
-      }
-      loaded += uint64_t(n) * rows * 8;
-      xs[b].publish(s);
-    }
-  });
-  std::thread writer([&] {
-    for (int64_t s = 0; s < slabs && !abort.load(); ++s) {
-      const int b = int(s & 1);
-      if (!rs[b].wait([&] { return rs[b].ready >= s; }, abort)) return;
-      cudaEventSynchronize(e->ev_d2h_done[b]);
-      const int64_t i0 = s * mb, rows = std::min(mb, m - i0);
-      if (!write_fn(i0, rows, hres[b])) {
-        io_error = 2;
-        abort = true;
-        wake_all();
-        return;
-      }
-      stored += uint64_t(rows) * t * p * 8;
-      rs[b].release(s);
-    }
-  });
-
-  int rc = GWG_OK;
-  for (int64_t s = 0; s < slabs && rc == GWG_OK; ++s) {
-    const int b = int(s & 1);
-    const int64_t i0 = s * mb, rows = std::min(mb, m - i0);
-    if (!xs[b].wait([&] { return xs[b].ready >= s; }, abort)) break;
-    auto enqueue = [&]() -> int {
-      GWG_CUDA_TRY(cudaStreamWaitEvent(e->h2d, e->ev_rot_done[b], 0));
-      GWG_CUDA_TRY(cudaMemcpy2DAsync(e->raw[b].ptr, raw_ld(e) * 8, hx[b], n * 8, n * 8, rows,
-                                     cudaMemcpyHostToDevice, e->h2d));
-      GWG_CUDA_TRY(cudaEventRecord(e->ev_h2d[b], e->h2d));
-      GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_h2d[b], 0));
-      GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_d2h_done[b], 0));
-      if (rotated) {
-        GWG_CUDA_TRY(cudaMemcpy2DAsync(e->rot.ptr, e->np * 8, e->raw[b].ptr, raw_ld(e) * 8,
-                                       n * 8, rows, cudaMemcpyDeviceToDevice, e->comp));
-        if (int r = square_rotated(e, rows, st)) return r;
-      } else if (int r = rotate_snps(e, e->raw[b].d(), raw_ld(e), rows, st)) {
-        return r;
-      }
-      GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
-      GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s], e->comp));
-      const int64_t si = out_layout == GWG_LAYOUT_NUMPY ? t : 1;
-      const int64_t sj = out_layout == GWG_LAYOUT_NUMPY ? 1 : rows;
-      if (int r = launch_slab(e, e->rot.d(), e->rot_sq.d(), rows, i0, m, e->out[b].d(), si, sj,
-                              st))
-        return r;
-      GWG_CUDA_TRY(cudaEventRecord(e->slab_events[2 * s + 1], e->comp));
-      GWG_CUDA_TRY(cudaEventRecord(e->ev_comp[b], e->comp));
-      return GWG_OK;
-    };
-    if ((rc = enqueue()) != GWG_OK) break;
-    xs[b].release(s);
-    // D2H into hres[b] once the writer released slab s-2
-    if (!rs[b].wait([&] { return rs[b].freed >= s - 2; }, abort)) break;
-    auto d2h = [&]() -> int {
-      GWG_CUDA_TRY(cudaStreamWaitEvent(e->d2h, e->ev_comp[b], 0));
-      GWG_CUDA_TRY(cudaMemcpyAsync(hres[b], e->out[b].ptr, size_t(rows) * t * p * 8,
-                                   cudaMemcpyDeviceToHost, e->d2h));
-      GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], e->d2h));
-      return GWG_OK;
-    };
-    if ((rc = d2h()) != GWG_OK) break;
-    rs[b].publish(s);
-  }
-  if (rc != GWG_OK) abort = true;
-  wake_all();
-  reader.join();
-  writer.join();
-  cudaStreamSynchronize(e->h2d);
-  cudaStreamSynchronize(e->comp);
-  cudaStreamSynchronize(e->d2h);
-  if (rc != GWG_OK) return rc;
-  if (io_error_out) *io_error_out = io_error.load();
-  if (io_error) return GWG_IO;
-  GWG_CUDA_TRY(cudaGetLastError());
-  for (int64_t s = 0; s < slabs; ++s) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, e->slab_events[2 * s], e->slab_events[2 * s + 1]) ==
-        cudaSuccess)
-      e->counters.grid_kernel_ms += ms;
-  }
-  if (loaded_out) *loaded_out = loaded.load();
-  if (stored_out) *stored_out = stored.load();
-  return read_errors(e, st, false);
-}
-
-}  // namespace gwg_host
 
 extern "C" {
 
@@ -425,11 +253,16 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
     return set_status(st, GWG_IO, -1, -1, "cannot size %s", out_path);
 
   const int fd_in = in.fd, fd_out = out.fd;
-  SlabRead rd = [&](int64_t i0, int64_t rows, double* dst) {
+  PipeSpec sp;
+  sp.m = m;
+  sp.mb = mb;
+  sp.rotated = snps_rotated != 0;
+  sp.layout = GWG_LAYOUT_STREAM;
+  sp.read_fn = [&](int64_t i0, int64_t rows, void* dst) {
     return pread_all(fd_in, dst, size_t(n) * rows * 8, kHeader + uint64_t(i0) * n * 8);
   };
   // write_result_cells (stream.cpp:414-438): t contiguous runs per slab
-  SlabWrite wr = [&](int64_t i0, int64_t rows, const double* src) {
+  sp.write_fn = [&](int64_t i0, int64_t rows, const double* src) {
     const size_t run = size_t(rows) * p * 8;
     for (int64_t j = 0; j < t; ++j)
       if (!pwrite_all(fd_out, src + size_t(j) * rows * p, run,
@@ -437,14 +270,16 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
         return false;
     return true;
   };
-  uint64_t loaded = 0, stored = 0;
-  int io_error = 0;
-  const int rc = staged_pipeline(e, m, mb, snps_rotated != 0, GWG_LAYOUT_STREAM, rd, wr,
-                                 &loaded, &stored, &io_error, st);
-  if (io_error)
-    return set_status(st, GWG_IO, -1, -1, io_error == 1 ? "short read in %s" : "short write to %s",
-                      io_error == 1 ? snps_path : out_path);
+  e->i8_input = false;
+  PipeStats ps;
+  const int rc = run_pipeline(e, sp, &ps, st);
+  const uint64_t loaded = ps.loaded, stored = ps.stored;
+  e->counters.io_stall_ms += ps.stall_ms;
+  if (ps.io_error)
+    return set_status(st, GWG_IO, -1, -1, ps.io_error == 1 ? "short read in %s" : "short write to %s",
+                      ps.io_error == 1 ? snps_path : out_path);
   if (rc != GWG_OK) return rc;
+  if (int r = read_errors(e, st)) return r;
   e->counters.bytes_loaded += loaded;
   e->counters.bytes_stored += stored;
   e->counters.wall_ms =

@@ -2,7 +2,11 @@
 
 BASELINE.json names no public dataset; every input is drawn from one seed
 (counter-based splitmix64 in csrc/datagen.cpp, so any SNP column range can be
-regenerated on its own — by a rank owning a shard, or by a spot check):
+regenerated on its own — by a rank owning a shard, or by a spot check).  The
+generator is compiled into the engine library AND into the oracle library
+(oracle/Makefile builds the same datagen.cpp), so the CPU reference arm of
+bench.py produces bit-identical inputs without loading the engine: every
+function takes ``lib=`` (default: the engine library).
 
 * Phi = G G^T / s + 1e-3 I, G n x s standardized Binomial(2, maf) genotypes,
   maf ~ U[0.05, 0.5] per column
@@ -42,9 +46,13 @@ CONFIGS = {
 }
 
 
+def _lib(lib):
+    return lib if lib is not None else nat.load()
+
+
 def genotypes(seed: int, matrix: int, rows: int, col0: int, ncols: int,
-              standardize: bool = False, out: np.ndarray | None = None) -> np.ndarray:
-    lib = nat.load()
+              standardize: bool = False, out: np.ndarray | None = None, lib=None) -> np.ndarray:
+    lib = _lib(lib)
     if out is None:
         out = np.empty((rows, ncols), dtype=np.float64, order="F")
     assert out.flags.f_contiguous and out.shape == (rows, ncols)
@@ -54,8 +62,8 @@ def genotypes(seed: int, matrix: int, rows: int, col0: int, ncols: int,
 
 
 def normals(seed: int, matrix: int, rows: int, col0: int, ncols: int,
-            out: np.ndarray | None = None) -> np.ndarray:
-    lib = nat.load()
+            out: np.ndarray | None = None, lib=None) -> np.ndarray:
+    lib = _lib(lib)
     if out is None:
         out = np.empty((rows, ncols), dtype=np.float64, order="F")
     assert out.flags.f_contiguous and out.shape == (rows, ncols)
@@ -63,41 +71,52 @@ def normals(seed: int, matrix: int, rows: int, col0: int, ncols: int,
     return out
 
 
-def uniform(seed: int, matrix: int, count: int, lo: float, hi: float) -> np.ndarray:
-    lib = nat.load()
+def uniform(seed: int, matrix: int, count: int, lo: float, hi: float, lib=None) -> np.ndarray:
+    lib = _lib(lib)
     out = np.empty(count, dtype=np.float64)
     lib.gwg_gen_uniform(seed, matrix, count, ctypes.c_double(lo), ctypes.c_double(hi),
                         out.ctypes.data)
     return out
 
 
-def kinship(seed: int, n: int, s: int) -> np.ndarray:
-    g = genotypes(seed, M_KINSHIP, n, 0, s, standardize=True)
+def kinship(seed: int, n: int, s: int, lib=None) -> np.ndarray:
+    g = genotypes(seed, M_KINSHIP, n, 0, s, standardize=True, lib=lib)
     phi = (g @ g.T) / float(s)
     phi = 0.5 * (phi + phi.T)
     phi[np.diag_indices(n)] += 1e-3
     return np.asfortranarray(phi)
 
 
-def covariates(seed: int, n: int, p: int) -> np.ndarray:
+def covariates(seed: int, n: int, p: int, lib=None) -> np.ndarray:
     xl = np.empty((n, max(p - 1, 0)), dtype=np.float64, order="F")
     if p >= 2:
         xl[:, 0] = 1.0
     if p >= 3:
-        normals(seed, M_COVARIATES, n, 0, p - 2, out=xl[:, 1:])
+        normals(seed, M_COVARIATES, n, 0, p - 2, out=xl[:, 1:], lib=lib)
     return xl
 
 
+def genotype_codes(seed: int, matrix: int, rows: int, col0: int, ncols: int,
+                   lib=None) -> np.ndarray:
+    """The same genotypes as int8 codes (GWG_FORMAT_I8: 1 byte per code)."""
+    out = np.empty((rows, ncols), dtype=np.int8, order="F")
+    step = 8192
+    for a in range(0, ncols, step):
+        k = min(step, ncols - a)
+        out[:, a:a + k] = genotypes(seed, matrix, rows, col0 + a, k, lib=lib)
+    return out
+
+
 def generate(n: int, p: int, m: int, t: int, seed: int = 1, s: int | None = None,
-             snps_out: np.ndarray | None = None) -> dict:
+             snps_out: np.ndarray | None = None, lib=None) -> dict:
     """A whole dataset as a dict of arrays (the gwgrid.generate shape, with
     BASELINE.json's generators)."""
     s = s if s is not None else 2 * n
     return {
-        "kinship": kinship(seed, n, s),
-        "xl": covariates(seed, n, p),
-        "snps": genotypes(seed, M_SNPS, n, 0, m, out=snps_out),
-        "traits": normals(seed, M_TRAITS, n, 0, t),
-        "h2": uniform(seed, M_H2, t, 0.05, 0.95),
+        "kinship": kinship(seed, n, s, lib=lib),
+        "xl": covariates(seed, n, p, lib=lib),
+        "snps": genotypes(seed, M_SNPS, n, 0, m, out=snps_out, lib=lib),
+        "traits": normals(seed, M_TRAITS, n, 0, t, lib=lib),
+        "h2": uniform(seed, M_H2, t, 0.05, 0.95, lib=lib),
         "sigma2": np.ones(t, dtype=np.float64),
     }

@@ -17,9 +17,11 @@ from paper_1210_7683_b200 import datagen  # noqa: E402
 from tests.test_gpu_parity import assert_parity  # noqa: E402
 
 
-def run(ds, basis, values, coding, **kw):
+def run(ds, basis, values, coding, options=None, **kw):
     n, p = ds["kinship"].shape[0], ds["xl"].shape[1] + 1
     with gw.Engine(n, p) as eng:
+        for name, value in (options or {}).items():
+            eng.set_option(name, value)
         eng.set_spectrum(basis, values)
         eng.set_covariates(ds["xl"])
         eng.set_snp_coding(coding)
@@ -154,9 +156,9 @@ def test_device_snp_operand_alignment_and_odd_n(n, offset):
 
 
 @pytest.mark.parametrize("case", ["config", "edge_h", "wide_spectrum"])
-def test_low_rank_sbr_matches_direct_contraction(case, monkeypatch):
+def test_low_rank_sbr_matches_direct_contraction(case):
     """S_BR = ((X'.X')^T E) F (positive exponential sum, csrc/expsum.cpp)
-    against the direct DMMA contraction (X'.X')^T D (GWG_SBR_DIRECT=1) and
+    against the direct DMMA contraction (X'.X')^T D (GWG_OPT_SBR_DIRECT) and
     the oracle, including h2 = 0 (D constant), h2 = 1 and a spectrum spanning
     nine decades."""
     n, p, m, t = 400, 4, 500, 40
@@ -169,8 +171,7 @@ def test_low_rank_sbr_matches_direct_contraction(case, monkeypatch):
         values = np.geomspace(1e-7, 1e2, n)
     ds = dict(ds, h2=h2)
     b_low = run(ds, basis, values, "genotypes")
-    monkeypatch.setenv("GWG_SBR_DIRECT", "1")
-    b_dir = run(ds, basis, values, "genotypes")
+    b_dir = run(ds, basis, values, "genotypes", options={"sbr_direct": 1})
     assert not np.isnan(b_low).any()
     rel = np.linalg.norm(b_low - b_dir, axis=2) / np.linalg.norm(b_dir, axis=2)
     assert rel.max() < 1e-11, rel.max()
@@ -179,7 +180,7 @@ def test_low_rank_sbr_matches_direct_contraction(case, monkeypatch):
     assert_parity(b_low, ref)
 
 
-def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
+def test_low_rank_sbr_is_used_and_falls_back():
     """The engine takes the factorised S_BR on BASELINE-like inputs (two
     gls_sbr launches per slab instead of one) and the direct contraction
     when D is outside the factorisation's range: h2 = 3, sigma2 = -1 and a
@@ -189,8 +190,9 @@ def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
     basis, values = gw.eigendecompose(ds["kinship"])
     n, p, t = 200, 3, 8
 
-    def launches(values, h2, sigma2):
+    def launches(values, h2, sigma2, direct=0):
         with gw.Engine(n, p) as eng:
+            eng.set_option("sbr_direct", direct)
             eng.set_spectrum(basis, values)
             eng.set_covariates(ds["xl"])
             eng.set_snp_coding("genotypes")
@@ -203,9 +205,8 @@ def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
     odd = (np.linspace(0.1, 0.6, n), np.full(t, 3.0), np.full(t, -1.0))
     k_low, b_low = launches(values, ds["h2"], ds["sigma2"])
     k_odd, b_odd = launches(*odd)
-    monkeypatch.setenv("GWG_SBR_DIRECT", "1")
-    k_dir, b_dir = launches(values, ds["h2"], ds["sigma2"])
-    k_odd_dir, b_odd_dir = launches(*odd)
+    k_dir, b_dir = launches(values, ds["h2"], ds["sigma2"], direct=1)
+    k_odd_dir, b_odd_dir = launches(*odd, direct=1)
     assert k_low == k_dir + 1 and k_odd == k_odd_dir == k_dir
     rel = np.linalg.norm(b_low - b_dir, axis=2) / np.linalg.norm(b_dir, axis=2)
     assert rel.max() < 1e-11, rel.max()
@@ -217,8 +218,8 @@ def test_low_rank_sbr_is_used_and_falls_back(monkeypatch):
 
 @pytest.mark.parametrize("n,p,m,t", [(200, 4, 300, 20), (1000, 4, 1000, 64), (300, 12, 129, 17),
                                      (257, 20, 333, 7), (300, 13, 200, 20)])
-def test_int8_kernel_variants_bitwise_identical(n, p, m, t, monkeypatch):
-    """Every int8 launch geometry (GWG_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
+def test_int8_kernel_variants_bitwise_identical(n, p, m, t):
+    """Every int8 launch geometry (GWG_OPT_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
     on two SNP tiles multicasting B, 3 CTA pairs on two W tiles multicasting
     the SNP tile) gives the same bits: the int32 slice products are exact and
     the recombination order fixed."""
@@ -226,8 +227,7 @@ def test_int8_kernel_variants_bitwise_identical(n, p, m, t, monkeypatch):
     basis, values = gw.eigendecompose(ds["kinship"])
     out = {}
     for cl in ("1", "2", "3"):
-        monkeypatch.setenv("GWG_I8_CLUSTER", cl)
-        out[cl] = run(ds, basis, values, "genotypes")
+        out[cl] = run(ds, basis, values, "genotypes", options={"i8_cluster": int(cl)})
     assert not np.isnan(out["2"]).any()
     assert np.array_equal(out["1"], out["2"])
     assert np.array_equal(out["1"], out["3"])
@@ -259,10 +259,40 @@ def test_auto_coding_picks_the_path_per_slab():
         assert np.array_equal(eng.run_grid(ds["snps"], mb=100), geno)
 
 
+@pytest.mark.parametrize("t", [23, 300])
+def test_auto_coding_first_slab_non_code(t):
+    """GWG_SNP_AUTO when the FIRST slab after set_traits holds a non-code
+    value and every later slab codes: the trait operands of the genotype path
+    (W, its slices, E/F) are built ungated on the first slab, so the later
+    slabs get the explicit genotype coding's bits (advisor finding: they used
+    to be built under the first slab's FP64 verdict and left stale)."""
+    n, p, m = 300, 4, 400
+    ds = datagen.generate(n, p, m, t, seed=78)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    snps = ds["snps"].copy()
+    snps[3, 10] += 0.5  # first 100-column slab is real-valued
+    ds2 = dict(ds, snps=snps)
+    auto = run(ds2, basis, values, "auto", mb=100)
+    geno = run(ds, basis, values, "genotypes", mb=100)
+    real = run(ds2, basis, values, "real", mb=100)
+    assert not np.isnan(auto).any()
+    assert np.array_equal(auto[:100], real[:100])
+    assert np.array_equal(auto[100:], geno[100:])
+    # the same through solve_snp_slab, slab by slab (the verdict word is reset
+    # before each slab's rotation)
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        parts = [eng.solve_snp_slab(np.asfortranarray(snps[:, a:a + 100]), i0=a)
+                 for a in range(0, m, 100)]
+    assert np.array_equal(np.concatenate(parts), auto)
+
+
 @pytest.mark.parametrize("p", [1, 4, 12, 20])
-def test_fp64_path_factorised_sbr_matches_fused(p, monkeypatch):
+def test_fp64_path_factorised_sbr_matches_fused(p):
     """The all-FP64 path with t >= 256 takes S_BR from the factorised GEMMs and
-    runs the grid kernel without the D column (GridCfg::EXT); GWG_REAL_SPLIT=0
+    runs the grid kernel without the D column (GridCfg::EXT); GWG_OPT_REAL_SPLIT = 0
     keeps the single fused kernel.  Same cells to rounding, both against the
     oracle, and bitwise independent of the slab width."""
     n, m, t = 200, 150, 300
@@ -270,8 +300,7 @@ def test_fp64_path_factorised_sbr_matches_fused(p, monkeypatch):
     basis, values = gw.eigendecompose(ds["kinship"])
     split = run(ds, basis, values, "real")
     assert np.array_equal(split, run(ds, basis, values, "real", mb=37))
-    monkeypatch.setenv("GWG_REAL_SPLIT", "0")
-    fused = run(ds, basis, values, "real")
+    fused = run(ds, basis, values, "real", options={"real_split": 0})
     rel = np.linalg.norm(split - fused, axis=2) / np.linalg.norm(fused, axis=2)
     assert rel.max() < 1e-11, rel.max()
     ii = np.arange(0, m, 7)

@@ -77,6 +77,14 @@ def test_file_legs_match_in_memory_engine(tmp_path, coding):
             got = gwg1.read_result(out_path)
             assert np.array_equal(got, mem)
         assert c["bytes_stored"] >= 1111 * 45 * 4 * 8
+        # the file leg against the oracle (restated compute_tile), not only
+        # against the in-memory engine
+        from oracle import oracle as orc
+        from tests.test_gpu_parity import assert_parity
+
+        ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"]),
+                               orc.rotate(basis, ds["traits"]), ds["h2"], ds["sigma2"], workers=8)
+        assert_parity(gwg1.read_result(out_path), ref)
         # a rotated SNP stream (the reference's preloop output) gives the same cells
         rot_path = str(tmp_path / "rot.gwg")
         gwg1.write_snp_stream(rot_path, basis.T @ ds["snps"])

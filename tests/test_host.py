@@ -133,41 +133,56 @@ def test_generator_columns_are_independent_of_range():
     assert np.array_equal(nf[:, 3:5], datagen.normals(11, datagen.M_TRAITS, 50, 3, 2))
 
 
+def _oracle_compute(shared, x, i0):
+    """The per-rank solve injected into multi.solve_sharded: the oracle
+    (test infrastructure) in place of the device engine."""
+    from paper_1210_7683_b200.checksum import grid_checksum
+
+    z, lam = shared["basis"].numpy(), shared["values"].numpy()
+    xl, y = shared["xl"].numpy(), shared["y"].numpy()
+    b = orc.compute_grid(lam, z.T @ xl, z.T @ x, z.T @ y, shared["h2"].numpy(),
+                         shared["sigma2"].numpy())
+    return b, grid_checksum(b, i0=i0)
+
+
 def _shard_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
 
+    from paper_1210_7683_b200 import multi
+
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n, p, m, t = 24, 3, 10, 4
-    # rank 0 builds the shared operands and broadcasts them (bench.py's plan)
-    if rank == 0:
-        ds = datagen.generate(n, p, m * world, t, seed=4)
+    n, p, m, t = 24, 3, 21, 4
+
+    def make_shared():  # rank 0 only: the one-off preloop
+        ds = datagen.generate(n, p, 1, t, seed=4)
         z, lam = gw.eigendecompose(ds["kinship"])
-        shared = [torch.from_numpy(np.ascontiguousarray(a)) for a in
-                  (z, lam, ds["xl"], ds["traits"], ds["h2"])]
-    else:
-        shared = [torch.empty(s, dtype=torch.float64) for s in
-                  ((n, n), (n,), (n, p - 1), (n, t), (t,))]
-    for buf in shared:
-        dist.broadcast(buf, src=0)
-    z, lam, xl, y, h2 = (s.numpy() for s in shared)
-    # each rank generates its own SNP shard [rank*m, (rank+1)*m) and solves it
-    snps = datagen.genotypes(4, datagen.M_SNPS, n, rank * m, m)
-    b = orc.compute_grid(lam, z.T @ xl, z.T @ snps, z.T @ y, h2, np.ones(t))
-    gathered = [torch.empty((m, t, p), dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(gathered, torch.from_numpy(b))
+        return {"basis": z, "values": lam, "xl": ds["xl"], "y": ds["traits"], "h2": ds["h2"],
+                "sigma2": ds["sigma2"]}
+
+    def load_shard(i0, i1):  # each rank generates only its own columns
+        return datagen.genotypes(4, datagen.M_SNPS, n, i0, i1 - i0)
+
+    res = multi.solve_sharded(n, p, m, t, make_shared, load_shard, _oracle_compute)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (res["i0"], res["i1"], res["b"]))
     if rank == 0:
-        q.put(np.concatenate([g.numpy() for g in gathered], axis=0))
+        q.put((gathered, res["checksum"]))
     dist.destroy_process_group()
 
 
 def test_snp_sharding_over_two_ranks_matches_single_rank():
-    """The multi-GPU plan (bench.py): shard m over ranks, broadcast the shared
-    operands, no data-path collective.  Checked with gloo on CPU, the per-rank
-    solve done by the oracle (the GPU path is covered by the gpu tests)."""
+    """The multi-GPU plan (paper_1210_7683_b200.multi, which bench.py uses):
+    shard m over ranks, broadcast the shared operands once, no data-path
+    collective.  Run with gloo on CPU, world size 2, through solve_sharded
+    with the per-rank solve injected (the oracle here; engine_compute on the
+    GPU): the shards tile [0, m) and reassemble the single-rank grid bit for
+    bit, and the gathered checksum is the whole grid's."""
     import multiprocessing as mp
     import socket
+
+    from paper_1210_7683_b200.checksum import grid_checksum
 
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -177,15 +192,34 @@ def test_snp_sharding_over_two_ranks_matches_single_rank():
     procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
     for pr in procs:
         pr.start()
-    sharded = q.get(timeout=120)
+    gathered, checksum = q.get(timeout=180)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    ds = datagen.generate(24, 3, 20, 4, seed=4)
+    assert [(a, b) for a, b, _ in gathered] == [(0, 10), (10, 21)]
+    sharded = np.concatenate([b for _, _, b in gathered], axis=0)
+    ds = datagen.generate(24, 3, 21, 4, seed=4)
     z, lam = gw.eigendecompose(ds["kinship"])
     whole = orc.compute_grid(lam, z.T @ ds["xl"], z.T @ ds["snps"], z.T @ ds["traits"],
                              ds["h2"], np.ones(4))
     assert np.array_equal(sharded, whole)
+    assert checksum == grid_checksum(whole)
+
+
+def test_shard_plan_matches_device_group_formula():
+    """multi.shard_bounds (torchrun ranks) and gwg_group_shards (one process,
+    several GPUs) split m identically: contiguous, balanced, covering."""
+    from paper_1210_7683_b200 import multi
+
+    for m in (1, 7, 100, 100_001):
+        for world in (1, 2, 3, 4, 8):
+            b = multi.shard_bounds(m, world)
+            assert b[0] == 0 and b[-1] == m
+            sizes = np.diff(b)
+            assert sizes.min() >= 0 and sizes.max() - sizes.min() <= 1
+            assert multi.rank_range(m, world, world - 1) == (b[-2], b[-1])
+    # weak scaling (bench.py): m per rank fixed -> rank r owns [r m, (r+1) m)
+    assert multi.shard_bounds(8 * 1000, 8) == [r * 1000 for r in range(9)]
 
 
 def test_empty_grids_are_dimension_errors():
