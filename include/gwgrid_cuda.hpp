@@ -131,10 +131,15 @@ class DeviceGrid {
 
   // transform_trait_slab + build_trait_contexts for a raw trait slab n x t
   // (trait0 only tags errors in the reference; traits are 0-based here).
+  // Like the reference (grid.cpp:146-175) this throws a trait's weight-floor
+  // failure here: the asynchronous gwg_set_traits is followed by one
+  // gwg_synchronize, which reports it.
   void build_trait_contexts(const double* traits, std::int64_t t, const double* h2,
                             const double* sigma2, bool rotated = false) {
     gwg_status st{};
     gwg_set_traits(e_, t, traits, h2, sigma2, GWG_HOST, rotated ? 1 : 0, &st);
+    throw_if(st);
+    gwg_synchronize(e_, &st);
     throw_if(st);
     t_ = t;
   }

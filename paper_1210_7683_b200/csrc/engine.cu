@@ -179,7 +179,7 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
   return GWG_OK;
 }
 
-int read_errors(gwg_engine* e, gwg_status* st) {
+int read_errors(gwg_engine* e, gwg_status* st, bool slab_checks) {
   GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 3 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
@@ -190,6 +190,7 @@ int read_errors(gwg_engine* e, gwg_status* st) {
                       "weight entry is below the relative floor (trait %lld)",
                       (long long)j);
   }
+  if (!slab_checks) return GWG_OK;
   if (e->i8_input && e->err_host[2] != ~0ull)
     return set_status(st, GWG_DIMENSION, -1, -1,
                       "int8 SNP slabs must hold genotype codes in [-127, 127] (found -128)");
@@ -1140,6 +1141,9 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   for (cudaEvent_t& ev : e->ev_s) cudaEventCreate(&ev);
   if ((err = e->err.ensure(3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMalloc", err);
+  if ((err = cudaMemsetAsync(e->err.ptr, 0xff, 3 * sizeof(unsigned long long), e->comp)) !=
+      cudaSuccess)
+    return bail("cudaMemset", err);
   if ((err = cudaMallocHost(&e->err_host, 3 * sizeof(unsigned long long))) != cudaSuccess)
     return bail("cudaMallocHost", err);
   if ((err = cudaMallocHost(&e->range_host, 8 * sizeof(double))) != cudaSuccess)
@@ -1289,7 +1293,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     }
     e->counters.bytes_stored += uint64_t(mb) * t * p * 8;
   }
-  if (int rc = read_errors(e, st)) return rc;
+  if (int rc = read_errors(e, st, true)) return rc;
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
   if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
@@ -1390,7 +1394,7 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
   GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
   // a trait failure queued by gwg_set_traits surfaces here at the latest
-  if (e->have_traits) return read_errors(e, st);
+  if (e->have_traits) return read_errors(e, st, false);
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   return GWG_OK;
 }

@@ -214,8 +214,9 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
 // Copy the error words to the host (one sync) and report, in this order: a
 // pending trait weight-floor failure (-1, j), an int8 code outside
 // [-127, 127] (or, for GWG_SNP_GENOTYPES, a non-code value); cell errors are
-// left to raise_cell_error.
-int read_errors(gwg_engine* e, gwg_status* st);
+// left to raise_cell_error.  slab_checks = false reports the trait word only
+// (gwg_synchronize: the slab words belong to the call that queued the slab).
+int read_errors(gwg_engine* e, gwg_status* st, bool slab_checks);
 // Reset the per-slab words (cell key, genotype verdict); the trait word is
 // reset by set_traits only.
 int reset_errors(gwg_engine* e, gwg_status* st);

@@ -368,7 +368,7 @@ int run_grid_impl(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host
   if (ps.io_error == 2 && sink)
     return set_status(st, GWG_IO, -1, -1, "result sink aborted the run");
   if (rc != GWG_OK) return rc;
-  if (int r = read_errors(e, st)) return r;
+  if (int r = read_errors(e, st, true)) return r;
   if (sp.checksum) {
     unsigned long long sum = 0;
     GWG_CUDA_TRY(cudaMemcpy(&sum, e->csum.ptr, sizeof(sum), cudaMemcpyDeviceToHost));

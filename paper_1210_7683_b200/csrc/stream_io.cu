@@ -279,7 +279,7 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
     return set_status(st, GWG_IO, -1, -1, ps.io_error == 1 ? "short read in %s" : "short write to %s",
                       ps.io_error == 1 ? snps_path : out_path);
   if (rc != GWG_OK) return rc;
-  if (int r = read_errors(e, st)) return r;
+  if (int r = read_errors(e, st, true)) return r;
   e->counters.bytes_loaded += loaded;
   e->counters.bytes_stored += stored;
   e->counters.wall_ms =

