@@ -211,6 +211,7 @@ def run_ours(args):
         ev0.record(stream)
         for _ in range(args.steps):
             step()
+        eng.synchronize()  # the steps' error words (device outputs are asynchronous)
         ev1.record(stream)
         barrier()
     ms_total = ev0.elapsed_time(ev1)
@@ -299,6 +300,7 @@ def run_ours(args):
         a0.record(stream)
         for _ in range(args.steps):
             alt_step()
+        eng.synchronize()
         a1.record(stream)
         barrier()
         alt_ms = a0.elapsed_time(a1) / args.steps

@@ -174,7 +174,11 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
                        const double* sigma2, int32_t where, int32_t is_rotated,
                        gwg_status* st);
 
-/* Solve the cells of one SNP slab against every installed trait:
+/* Solve the cells of one SNP slab against every installed trait (with a
+ * device b_out the call is asynchronous: it returns once the work is queued
+ * on the engine's compute stream, and errors — a failing cell with its
+ * coordinates, a trait failure, non-code genotypes — are reported by the next
+ * synchronising call: gwg_synchronize, a host-output solve or gwg_run_grid):
  * rows = mb SNP columns starting at global SNP index i0, x_r = n x mb
  * col-major (raw unless is_rotated; rotated on the device when raw).
  * Results for cell (il, j) go to b_out at
@@ -212,6 +216,11 @@ uint64_t gwg_cell_hash(int64_t i, int64_t j, int64_t c, uint64_t bits);
  * `stream` (a cudaStream_t as void*, e.g. torch's current stream), without a
  * host round trip: device operands produced there are then safe to read. */
 int32_t gwg_wait_stream(gwg_engine* e, void* stream, gwg_status* st);
+
+/* The converse: order `stream` after all work queued on the engine so far
+ * (device event, no host round trip) — e.g. torch's current stream before it
+ * reads a device output of an asynchronous gwg_solve_snp_slab. */
+int32_t gwg_signal_stream(gwg_engine* e, void* stream, gwg_status* st);
 
 /* ---- One process, several GPUs --------------------------------
  * A group holds one engine per listed device (a device may repeat).  The

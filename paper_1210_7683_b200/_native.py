@@ -63,6 +63,7 @@ EXPORTED_SYMBOLS = (
     "gwg_get_option",
     "gwg_cell_hash",
     "gwg_wait_stream",
+    "gwg_signal_stream",
     "gwg_group_create",
     "gwg_group_destroy",
     "gwg_group_size",
@@ -180,6 +181,7 @@ def load() -> ctypes.CDLL:
         "gwg_get_option": (I32, [P, I32, ctypes.POINTER(I64), S]),
         "gwg_cell_hash": (U64, [I64, I64, I64, U64]),
         "gwg_wait_stream": (I32, [P, P, S]),
+        "gwg_signal_stream": (I32, [P, P, S]),
         "gwg_group_create": (P, [ctypes.POINTER(I32), I32, I64, I64, S]),
         "gwg_group_destroy": (None, [P]),
         "gwg_group_size": (I32, [P]),

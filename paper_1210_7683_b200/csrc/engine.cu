@@ -207,6 +207,32 @@ int reset_errors(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
+int begin_epoch(gwg_engine* e, gwg_status* st) {
+  if (e->epoch_open) return GWG_OK;
+  if (int rc = reset_errors(e, st)) return rc;
+  e->epoch_open = true;
+  return GWG_OK;
+}
+
+int end_epoch(gwg_engine* e, gwg_status* st) {
+  const int rc = read_errors(e, st, true);  // synchronises the compute stream
+  for (size_t k = 0; k < e->timings_used; ++k) {
+    const auto& tm = e->timings[k];
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, tm.ev[0], tm.ev[1]) == cudaSuccess) e->counters.rotate_ms += ms;
+    if (cudaEventElapsedTime(&ms, tm.ev[2], tm.ev[3]) == cudaSuccess) e->counters.grid_kernel_ms += ms;
+    if (tm.split) {
+      if (cudaEventElapsedTime(&ms, tm.ev[4], tm.ev[5]) == cudaSuccess) e->counters.quad_ms += ms;
+      if (cudaEventElapsedTime(&ms, tm.ev[5], tm.ev[6]) == cudaSuccess) e->counters.linear_ms += ms;
+    }
+  }
+  cudaGetLastError();  // an event of a failed launch never recorded
+  e->timings_used = 0;
+  e->epoch_open = false;
+  if (rc) return rc;
+  return raise_cell_error(e, st);
+}
+
 // 2-D uint8 map over a K-major int8 operand (kp x cols) and 3-D map over
 // SLICES planes of (kp x ncols), both SWIZZLE_128B boxes for tcgen05.
 int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensorMap* tb,
@@ -732,9 +758,10 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   const int64_t ld_s = round_up(rows, 2);
 
   // ---- S_BR ----
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[0], e->comp));
+  cudaEvent_t* sev = e->split_ev ? e->split_ev : e->ev_s;
+  GWG_CUDA_TRY(cudaEventRecord(sev[0], e->comp));
   if (int rc = launch_sbr_stage(e, rot_sq, rows, ld_s, st)) return rc;
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[1], e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(sev[1], e->comp));
 
   // ---- linear terms (int8 tcgen05) + solve ----
   // CTA pairs multicasting the W-slice tile (measured: c1 2.90 -> 2.86 ms,
@@ -789,7 +816,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   (void)tiles;
   GWG_CUDA_TRY(e->lops.launch[cl - 1](tx, tw, tout, a, e->sms, e->comp));
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_s[2], e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(sev[2], e->comp));
   e->split_timed = true;
   e->counters.kernel_launches += 1;
   return GWG_OK;
@@ -922,11 +949,11 @@ void parallel_copy(void* dst, const void* src, size_t bytes) {
   for (auto& th : pool) th.join();
 }
 
-int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st) {
+int raise_cell_error(gwg_engine* e, gwg_status* st) {
   const unsigned long long key = e->err_host[1];
   if (key == ~0ull) return GWG_OK;
-  const int64_t j = int64_t(key / uint64_t(m_total));
-  const int64_t i = int64_t(key % uint64_t(m_total));
+  const int64_t j = int64_t(key / uint64_t(kKeyStride));
+  const int64_t i = int64_t(key % uint64_t(kKeyStride));
   return set_status(st, GWG_NOT_POSITIVE_DEFINITE, i, j,
                     "normal equations are not positive definite at cell (variant %lld, trait "
                     "%lld)",
@@ -1174,10 +1201,13 @@ void gwg_engine_destroy(gwg_engine* e) {
     if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
   }
   for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2],
-                         e->ev_wait})
+                         e->ev_wait, e->ev_signal})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->pipe_events) cudaEventDestroy(ev);
+  for (auto& tm : e->timings)
+    for (cudaEvent_t ev : tm.ev)
+      if (ev) cudaEventDestroy(ev);
   for (PinBuf& b : e->pin_x) b.release();
   for (PinBuf& b : e->pin_res) b.release();
   if (e->comp) cudaStreamDestroy(e->comp);
@@ -1251,9 +1281,15 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     GWG_CUDA_TRY(e->rot.ensure(size_t(e->np) * mb * sizeof(double)));
   GWG_CUDA_TRY(e->rot_sq.ensure(size_t(e->np) * mb * sizeof(double)));
   // before the rotation: it writes this slab's genotype verdict (word 2)
-  if (int rc = reset_errors(e, st)) return rc;
+  if (int rc = begin_epoch(e, st)) return rc;
   e->i8_input = false;
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_r0, e->comp));
+  if (e->timings.size() <= e->timings_used) {
+    gwg_engine::SlabTiming tm;
+    for (cudaEvent_t& ev : tm.ev) GWG_CUDA_TRY(cudaEventCreate(&ev));
+    e->timings.push_back(tm);
+  }
+  gwg_engine::SlabTiming& tmg = e->timings[e->timings_used++];
+  GWG_CUDA_TRY(cudaEventRecord(tmg.ev[0], e->comp));
   if (is_rotated) {
     if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;
     if (int rc = square_rotated(e, mb, st)) return rc;
@@ -1268,7 +1304,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     }
     if (int rc = rotate_snps(e, src, raw_ld(e), mb, st)) return rc;
   }
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_r1, e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(tmg.ev[1], e->comp));
   double* dev_out = b_out;
   if (out_where != GWG_DEVICE) {
     GWG_CUDA_TRY(e->out[0].ensure(size_t(mb) * t * p * sizeof(double)));
@@ -1276,12 +1312,17 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
   }
   const int64_t si = layout == GWG_LAYOUT_NUMPY ? t : 1;
   const int64_t sj = layout == GWG_LAYOUT_NUMPY ? 1 : (out_where == GWG_DEVICE ? ldo : mb);
-  const int64_t m_total = i0 + mb;
   e->split_timed = false;
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_k0, e->comp));
-  if (int rc = launch_slab(e, e->rot.d(), e->rot_sq.d(), mb, i0, m_total, dev_out, si, sj, st))
-    return rc;
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_k1, e->comp));
+  GWG_CUDA_TRY(cudaEventRecord(tmg.ev[2], e->comp));
+  e->split_ev = tmg.ev + 4;
+  const int lrc = launch_slab(e, e->rot.d(), e->rot_sq.d(), mb, i0, kKeyStride, dev_out, si, sj, st);
+  e->split_ev = nullptr;
+  if (lrc) return lrc;
+  tmg.split = e->split_timed;
+  GWG_CUDA_TRY(cudaEventRecord(tmg.ev[3], e->comp));
+  // a device output is asynchronous, like the device work that produces it:
+  // the epoch stays open and its errors surface at the next synchronising call
+  if (out_where == GWG_DEVICE) return GWG_OK;
   if (out_where != GWG_DEVICE) {
     if (layout == GWG_LAYOUT_NUMPY) {
       GWG_CUDA_TRY(cudaMemcpyAsync(b_out, dev_out, size_t(mb) * t * p * sizeof(double),
@@ -1293,17 +1334,8 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     }
     e->counters.bytes_stored += uint64_t(mb) * t * p * 8;
   }
-  if (int rc = read_errors(e, st, true)) return rc;
-  float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, e->ev_k0, e->ev_k1) == cudaSuccess) e->counters.grid_kernel_ms += ms;
-  if (cudaEventElapsedTime(&ms, e->ev_r0, e->ev_r1) == cudaSuccess) e->counters.rotate_ms += ms;
-  if (e->split_timed) {
-    // ev_s: [0] before gls_sbr_kernel, [1] before linear_solve_kernel, [2] after
-    if (cudaEventElapsedTime(&ms, e->ev_s[0], e->ev_s[1]) == cudaSuccess) e->counters.quad_ms += ms;
-    if (cudaEventElapsedTime(&ms, e->ev_s[1], e->ev_s[2]) == cudaSuccess) e->counters.linear_ms += ms;
-  }
-  // Error coordinates are global: key = j * (i0 + mb) + (i0 + il).
-  return raise_cell_error(e, m_total, st);
+  // Error coordinates are global: key = j * kKeyStride + (i0 + il).
+  return end_epoch(e, st);
 }
 
 int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st) {
@@ -1393,7 +1425,9 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
   if (int rc = check_engine(e, st)) return rc;
   GWG_CUDA_TRY(cudaStreamSynchronize(e->h2d));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->d2h));
-  // a trait failure queued by gwg_set_traits surfaces here at the latest
+  // errors of asynchronous solves, and a trait failure queued by
+  // gwg_set_traits, surface here at the latest
+  if (e->epoch_open) return end_epoch(e, st);
   if (e->have_traits) return read_errors(e, st, false);
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
   return GWG_OK;

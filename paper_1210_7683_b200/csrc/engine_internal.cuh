@@ -168,9 +168,27 @@ struct gwg_engine {
 
   cudaEvent_t ev_h2d[2], ev_rot_done[2], ev_comp[2], ev_d2h_done[2];
   cudaEvent_t ev_k0, ev_k1, ev_r0, ev_r1;
-  cudaEvent_t ev_wait = nullptr;  // gwg_wait_stream
+  cudaEvent_t ev_wait = nullptr;    // gwg_wait_stream
+  cudaEvent_t ev_signal = nullptr;  // gwg_signal_stream
   cudaEvent_t ev_s[3];     // split grid: before gls_sbr, before linear_solve, after it
   bool split_timed = false;
+  // where launch_split records its three events (null: ev_s)
+  cudaEvent_t* split_ev = nullptr;
+  // Error epochs: the cell-error key (word 1) and the genotype verdict
+  // (word 2) accumulate over every slab queued since the last synchronising
+  // call; the first slab of an epoch resets them.  Asynchronous
+  // device-output solves leave the epoch open (their errors surface at the
+  // next gwg_synchronize / host-output solve / run_grid).
+  bool epoch_open = false;
+  // per-slab CUDA events of the open epoch's solves, turned into counters
+  // when the epoch closes: [rotate begin, rotate end, grid begin, grid end,
+  // sbr begin, linear begin, linear end]
+  struct SlabTiming {
+    cudaEvent_t ev[7] = {};
+    bool split = false;
+  };
+  std::vector<SlabTiming> timings;
+  size_t timings_used = 0;
   std::vector<cudaEvent_t> slab_events;
 
   gwg_counters counters{};
@@ -223,7 +241,16 @@ int reset_errors(gwg_engine* e, gwg_status* st);
 int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
                 gwg_status* st);
-int raise_cell_error(gwg_engine* e, int64_t m_total, gwg_status* st);
+// Cell error keys are j * kKeyStride + i (global SNP index i < 2^34, trait
+// j < 2^30): the minimum is the first failing cell in trait-major order
+// whatever slabs, shards or calls produced it.
+constexpr int64_t kKeyStride = int64_t(1) << 34;
+int raise_cell_error(gwg_engine* e, gwg_status* st);
+// Open an error epoch (reset the slab words) unless one is open.
+int begin_epoch(gwg_engine* e, gwg_status* st);
+// Close it: wait for the compute stream, fold pending slab timings into the
+// counters, report (trait, genotype, cell) errors in that order.
+int end_epoch(gwg_engine* e, gwg_status* st);
 // rot_sq <- rot .* rot for `cols` already-rotated columns
 int square_rotated(gwg_engine* e, int64_t cols, gwg_status* st);
 int64_t default_slab(const gwg_engine* e, int64_t m);

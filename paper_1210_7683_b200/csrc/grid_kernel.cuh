@@ -144,7 +144,16 @@ struct GridArgs {
 //   beta_B = (b_B - l.z_T) / pivot     (= ((b_B - l.z_T)/lambda)/lambda;
 //                                       reciprocal by rcp.approx + Newton)
 //   beta_T = L^-T (z_T - l beta_B)
-template <int P>
+// Context loads: read-only global (__ldg) or, SMEM, a shared-memory copy.
+template <bool SMEM>
+__device__ __forceinline__ double ctx_ld(const double* p) {
+  if constexpr (SMEM)
+    return *p;
+  else
+    return __ldg(p);
+}
+
+template <int P, bool SMEM = false>
 __device__ __forceinline__ bool solve_cell(const double* acc, const double* __restrict__ cx,
                                            double* beta) {
   using L = CtxLayout<P>;
@@ -154,17 +163,17 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   for (int a = 0; a < P1; ++a) {
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c < a; ++c) s = fma(__ldg(cx + L::OFF + L::off_idx(a, c)), l[c], s);
-    l[a] = (acc[a] - s) * __ldg(cx + L::INVD + a);
+    for (int c = 0; c < a; ++c) s = fma(ctx_ld<SMEM>(cx + L::OFF + L::off_idx(a, c)), l[c], s);
+    l[a] = (acc[a] - s) * ctx_ld<SMEM>(cx + L::INVD + a);
   }
   double sq = 0.0, lz = 0.0;
 #pragma unroll
   for (int a = 0; a < P1; ++a) {
     sq = fma(l[a], l[a], sq);
-    lz = fma(l[a], __ldg(cx + L::Z + a), lz);
+    lz = fma(l[a], ctx_ld<SMEM>(cx + L::Z + a), lz);
   }
   const double pivot = acc[P] - sq;
-  const bool ok = !(pivot <= 0.0) && __ldg(cx + L::FLAG) == 0.0;
+  const bool ok = !(pivot <= 0.0) && ctx_ld<SMEM>(cx + L::FLAG) == 0.0;
   // 1/pivot: MUFU approximation + two Newton steps (<= 1 ulp; far cheaper on
   // the FP64 pipe than an IEEE division, which the other ping-pong group's
   // DMMAs are competing for)
@@ -181,10 +190,10 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   beta[P1] = bb;
 #pragma unroll
   for (int a = P1 - 1; a >= 0; --a) {
-    double r = __ldg(cx + L::Z + a) - l[a] * bb;
+    double r = ctx_ld<SMEM>(cx + L::Z + a) - l[a] * bb;
 #pragma unroll
-    for (int c = a + 1; c < P1; ++c) r -= __ldg(cx + L::OFF + L::off_idx(c, a)) * beta[c];
-    beta[a] = r * __ldg(cx + L::INVD + a);
+    for (int c = a + 1; c < P1; ++c) r -= ctx_ld<SMEM>(cx + L::OFF + L::off_idx(c, a)) * beta[c];
+    beta[a] = r * ctx_ld<SMEM>(cx + L::INVD + a);
   }
   return ok;
 }
@@ -196,7 +205,7 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
 // different rounding (well-conditioned S_TL); the pivot test is unchanged.
 //   l = L^-1 s_bl,  pivot = s_br - |l|^2,  beta_B = (b_B - l.z_T) / pivot,
 //   beta_T = L^-T (z_T - l beta_B)
-template <int P>
+template <int P, bool SMEM = false>
 __device__ __forceinline__ bool solve_cell_inv(const double* acc, const double* __restrict__ cx,
                                                double* beta) {
   using L = CtxLayout<P>;
@@ -206,27 +215,27 @@ __device__ __forceinline__ bool solve_cell_inv(const double* acc, const double* 
   for (int a = 0; a < P1; ++a) {
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c <= a; ++c) s = fma(__ldg(cx + L::LINV + L::linv_idx(a, c)), acc[c], s);
+    for (int c = 0; c <= a; ++c) s = fma(ctx_ld<SMEM>(cx + L::LINV + L::linv_idx(a, c)), acc[c], s);
     l[a] = s;
   }
   double sq = 0.0, lz = 0.0;
 #pragma unroll
   for (int a = 0; a < P1; ++a) {
     sq = fma(l[a], l[a], sq);
-    lz = fma(l[a], __ldg(cx + L::Z + a), lz);
+    lz = fma(l[a], ctx_ld<SMEM>(cx + L::Z + a), lz);
   }
   const double pivot = acc[P] - sq;
-  const bool ok = !(pivot <= 0.0) && __ldg(cx + L::FLAG) == 0.0;
+  const bool ok = !(pivot <= 0.0) && ctx_ld<SMEM>(cx + L::FLAG) == 0.0;
   const double bb = (acc[P1] - lz) / pivot;
   beta[P1] = bb;
   double r[P1 > 0 ? P1 : 1];
 #pragma unroll
-  for (int a = 0; a < P1; ++a) r[a] = fma(-l[a], bb, __ldg(cx + L::Z + a));
+  for (int a = 0; a < P1; ++a) r[a] = fma(-l[a], bb, ctx_ld<SMEM>(cx + L::Z + a));
 #pragma unroll
   for (int c = 0; c < P1; ++c) {
     double s = 0.0;
 #pragma unroll
-    for (int a = c; a < P1; ++a) s = fma(__ldg(cx + L::LINV + L::linv_idx(a, c)), r[a], s);
+    for (int a = c; a < P1; ++a) s = fma(ctx_ld<SMEM>(cx + L::LINV + L::linv_idx(a, c)), r[a], s);
     beta[c] = s;
   }
   return ok;

@@ -24,7 +24,7 @@ namespace gwg {
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
 template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1,
-          int PAIR_AXIS_ = 0>
+          int PAIR_AXIS_ = 0, uint32_t EXTRA_ = 0>
 struct I8Tile {
   // CLUSTER = 2: CTA pairs (a thread-block cluster) work on SNP tiles 2u and
   // 2u+1 against the same B rows; each CTA loads half of the B tile (4 of the
@@ -62,8 +62,10 @@ struct I8Tile {
   static constexpr int OUT_Q = 16;        // output box: 16 doubles (128 B) x 32 SNPs
   static constexpr uint32_t OUT_TILE = OUT_Q * 32 * 8;     // one 4 KB staging tile
   static constexpr uint32_t OUT_BYTES = OUT_BUFS * OUT_TILE;  // staging per epilogue warp
+  // kernel-specific shared memory after the staging tiles (1024-aligned)
+  static constexpr uint32_t EXTRA = (EXTRA_ + 15) / 16 * 16;
   static constexpr size_t SMEM_BYTES =
-      size_t(STAGES) * STAGE_BYTES + size_t(EPI_WARPS) * OUT_BYTES + 1024 + 256;
+      size_t(STAGES) * STAGE_BYTES + size_t(EPI_WARPS) * OUT_BYTES + EXTRA + 1024 + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(BN % 16 == 0 && BN <= 256 && RB % 8 == 0, "UMMA N / swizzle atoms");
   static_assert(BN <= SLOTS * RB, "the MMA reads only loaded (or zero-filled) slot rows");
@@ -277,6 +279,7 @@ template <class C>
 struct I8Smem {
   unsigned char* base;     // STAGES x (A | B), 1024-aligned for SWIZZLE_128B
   unsigned char* staging;  // [epilogue warp][OUT_BYTES]
+  unsigned char* extra;    // C::EXTRA bytes for the kernel's own use
   uint64_t* full;
   uint64_t* empty;
   uint64_t* acc_full;      // [ACC_BUFS]
@@ -286,7 +289,8 @@ struct I8Smem {
     base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
                                             ~uintptr_t(1023));
     staging = base + C::STAGES * C::STAGE_BYTES;
-    full = reinterpret_cast<uint64_t*>(staging + C::EPI_WARPS * C::OUT_BYTES);
+    extra = staging + C::EPI_WARPS * C::OUT_BYTES;
+    full = reinterpret_cast<uint64_t*>(extra + C::EXTRA);
     empty = full + C::STAGES;
     acc_full = empty + C::STAGES;
     acc_empty = acc_full + C::ACC_BUFS;

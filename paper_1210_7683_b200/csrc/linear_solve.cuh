@@ -45,6 +45,23 @@ namespace gwg {
 #define LIN_WIDE_MAXP 16
 #endif
 
+#ifndef LIN_EARLY_RELEASE
+#define LIN_EARLY_RELEASE 1
+#endif
+
+// S_BR: the context warp prefetches each tile's S_BR rows into L2 (bulk
+// prefetch) and the epilogue loads them after the TMEM release, instead of
+// holding a register prefetch from HBM across the accumulator wait
+#ifndef LIN_SBR_L2PF
+#define LIN_SBR_L2PF 1
+#endif
+
+// Per-tile trait contexts and W-row scales staged in shared memory by bulk
+// copies (warp 2) instead of per-cell __ldg / shuffles in the epilogue.
+#ifndef LIN_CTX_SMEM
+#define LIN_CTX_SMEM 1
+#endif
+
 template <int P, int CL = 1>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
@@ -76,17 +93,31 @@ struct LinCfg {
   static constexpr int OUT_BUFS = TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
   static constexpr int STAGES_0 = WIDE ? 3 : 4;
   static constexpr uint32_t STAGE_B = 128 * 128 + 8 * RB * 128;
+  // shared-memory context staging, per accumulator buffer: the tile's KT trait
+  // contexts (CtxLayout, contiguous in global memory) and RB W-row scales,
+  // then the ctx_full / ctx_empty mbarriers
+  static constexpr bool CTX_SMEM = LIN_CTX_SMEM != 0;
+  static constexpr int CTX_DOUBLES = KT * CtxLayout<P>::STRIDE;
+  static constexpr uint32_t CTX_BYTES = CTX_DOUBLES * 8;
+  static constexpr uint32_t SCALE_OFF = ACC * CTX_BYTES;
+  static constexpr uint32_t BAR_OFF = SCALE_OFF + ACC * RB * 8;
+  static constexpr uint32_t EXTRA = CTX_SMEM ? BAR_OFF + 2 * ACC * 8 : 0;
   static constexpr int STAGES =
-      size_t(STAGES_0) * STAGE_B + size_t(EPI) * OUT_BUFS * 4096 + 1280 <= 227 * 1024
+      size_t(STAGES_0) * STAGE_B + size_t(EPI) * OUT_BUFS * 4096 + (EXTRA + 15) / 16 * 16 + 1280 <=
+              227 * 1024
           ? STAGES_0
           : STAGES_0 - 1;
   // CL = 3: CTA pairs along the trait axis sharing (multicasting) the SNP tile
-  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 3 ? 2 : CL, CL == 3 ? 1 : 0>;
+  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 3 ? 2 : CL, CL == 3 ? 1 : 0, EXTRA>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
-  static constexpr int PAIR = GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
+  // EARLY: recombine every cell of the warp's tile share from TMEM first,
+  // release the accumulator buffer, then solve and store: the MMA of tile
+  // lt + ACC waits only for the recombination, not for the solves
+  static constexpr bool EARLY = LIN_EARLY_RELEASE != 0 && CELLS * P <= 16;
+  static constexpr int PAIR = !EARLY && GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
   // large p: triangular solves as products with L^-1 (independent dot
   // products instead of serial substitution chains)
 #ifndef LIN_INV_MINP
@@ -139,6 +170,16 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const I8Sched<C> sch(a.tiles_m, a.tiles_r);
   const int my_tiles = sch.my_tiles;
+  double* const ctx_sm = reinterpret_cast<double*>(sm.extra);
+  double* const scale_sm = reinterpret_cast<double*>(sm.extra + L::SCALE_OFF);
+  uint64_t* const ctx_full = reinterpret_cast<uint64_t*>(sm.extra + L::BAR_OFF);
+  uint64_t* const ctx_empty = ctx_full + L::ACC;
+  if (L::CTX_SMEM && threadIdx.x == 0) {  // fenced and published by i8_setup
+    for (int b = 0; b < L::ACC; ++b) {
+      mbar_init(&ctx_full[b], 1);
+      mbar_init(&ctx_empty[b], 4 * L::HMAX);
+    }
+  }
   // HMAX warps per quarter release each tile's buffer
   const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * L::HMAX);
 
@@ -147,6 +188,34 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
                                     a.b_resident != 0);
   } else if (warp == 1) {
     if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
+  } else if (warp == 2) {
+    // context producer: tile lt's KT trait contexts and RB W-row scales into
+    // the slot of its accumulator buffer once the epilogue of tile lt - ACC
+    // released it (two bulk copies completing on ctx_full)
+    if (L::CTX_SMEM && lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      for (int lt = 0; lt < my_tiles; ++lt) {
+        const int buf = lt % L::ACC;
+        if (lt >= L::ACC) mbar_wait(&ctx_empty[buf], uint32_t((lt / L::ACC) - 1) & 1);
+        int tm, tr;
+        sch.coords(lt, tm, tr);
+        const int j0 = tr * L::KT;
+        const int nt = min(L::KT, a.t - j0);
+        const uint32_t cbytes = uint32_t(nt) * CX::STRIDE * 8;
+        mbar_arrive_expect_tx(&ctx_full[buf], cbytes + C::RB * 8);
+        bulk_load(ctx_sm + buf * L::CTX_DOUBLES, a.ctx + int64_t(j0) * CX::STRIDE, cbytes,
+                  &ctx_full[buf], pol);
+        bulk_load(scale_sm + buf * C::RB, a.scale + int64_t(tr) * C::RB, C::RB * 8,
+                  &ctx_full[buf], pol);
+        if (LIN_SBR_L2PF) {  // this tile's S_BR rows [j][tm*BM, +BM) into L2
+          const int64_t i_lo = int64_t(tm) * C::BM;
+          const int64_t cnt = min(int64_t(C::BM), a.rows - i_lo);
+          const uint32_t bytes = uint32_t((cnt + 1) & ~int64_t(1)) * 8;  // ld_s is even
+          for (int u = 0; u < nt; ++u)
+            bulk_prefetch_l2(a.sbr + int64_t(j0 + u) * a.ld_s + i_lo, bytes);
+        }
+      }
+    }
   } else if (warp >= 4) {
     // warp w owns TMEM lane quarter w % 4; the two warps of a quarter take
     // alternate tiles (= alternate accumulator buffers), each doing all KT
@@ -173,29 +242,39 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       const int j0 = tr * L::KT;  // first trait of the tile
       if (!active) {  // KT = 1 under WIDE: nothing to do but keep the buffer protocol
         mbar_wait(&sm.acc_full[buf], par);
+        if (L::CTX_SMEM) mbar_wait(&ctx_full[buf], par);
         __syncwarp();
-        if (lane == 0) i8_acc_release<C>(sm, buf);
+        if (lane == 0) {
+          i8_acc_release<C>(sm, buf);
+          if (L::CTX_SMEM) mbar_arrive(&ctx_empty[buf]);
+        }
         continue;
       }
+      constexpr bool SBR_LATE = L::CTX_SMEM && L::EARLY && LIN_SBR_L2PF;
       double sbr[L::CELLS];
+      auto load_sbr = [&]() {
 #pragma unroll
-      for (int cc = 0; cc < L::CELLS; ++cc) {
-        const int j = j0 + cell0 + cc;
-        if (LIN_EXPERIMENT == 2 || LIN_EXPERIMENT >= 5)
-          sbr[cc] = 1e6 + lane;
-        else
-          sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
-      }
-      // lane r holds the slice scale of the tile's W row r (RB <= 32), shuffled
-      // to the recombination below: no per-column memory round trip
-      const double sc_lane =
-          lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) * 0x1p-55 : 0.0;  // sigma 2^-55, exact
+        for (int cc = 0; cc < L::CELLS; ++cc) {
+          const int j = j0 + cell0 + cc;
+          if (LIN_EXPERIMENT == 2 || LIN_EXPERIMENT >= 5)
+            sbr[cc] = 1e6 + lane;
+          else
+            sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
+        }
+      };
+      if (!SBR_LATE) load_sbr();
+      // without the staged copy, lane r holds the slice scale (sigma 2^-55) of
+      // the tile's W row r (RB <= 32), shuffled to the recombination below
+      const double sc_lane = !L::CTX_SMEM && lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
+      const double* const cx_tile = ctx_sm + buf * L::CTX_DOUBLES;
+      const double* const sc_tile = scale_sm + buf * C::RB;
 #if LIN_TRACE
       const int tix = (lt - h) / L::ACC;
       const bool tr_on = blockIdx.x == 0 && lane == 0 && tix < 48;
       if (tr_on) g_lin_trace[ew][tix][0] = clock64();
 #endif
       mbar_wait(&sm.acc_full[buf], par);
+      if (L::CTX_SMEM) mbar_wait(&ctx_full[buf], par);
 #if LIN_TRACE
       if (tr_on) g_lin_trace[ew][tix][1] = clock64();
 #endif
@@ -229,8 +308,9 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
               for (int r = 0; r < L::CW; ++r) {
                 if (c0 + r < P) {
-                  const double sc =
-                      __shfl_sync(0xffffffffu, sc_lane, (cb + u0 + u) * L::P8 + c0 + r);
+                  const int wrow = (cb + u0 + u) * L::P8 + c0 + r;
+                  const double sc = L::CTX_SMEM ? sc_tile[wrow]
+                                                : __shfl_sync(0xffffffffu, sc_lane, wrow);
                   if (LIN_EXPERIMENT == 5)
                     dst[u0 + u][c0 + r] = double(v[u][0][r] + v[u][1][r] + v[u][2][r] +
                                                  v[u][3][r] + v[u][4][r] + v[u][5][r] +
@@ -249,15 +329,31 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
         __syncwarp();
         if (lane == 0) i8_acc_release<C>(sm, buf);  // TMEM buffer free for tile lt + ACC
       };
+      double lin_all[L::EARLY ? L::CELLS : 1][P];
+      if constexpr (L::EARLY) {
+        recombine(cell0, L::CELLS, lin_all);
+        release();
+        if (SBR_LATE) load_sbr();
+#if LIN_TRACE
+        if (tr_on) g_lin_trace[ew][tix][2] = clock64();
+#endif
+      }
 #pragma unroll
       for (int g0 = 0; g0 < L::CELLS; g0 += L::GROUP) {
         double lin[L::GROUP][P];
-        recombine(cell0 + g0, L::GROUP, lin);
-        if (g0 + L::GROUP >= L::CELLS) {
-          release();
+        if constexpr (L::EARLY) {
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) lin[u][c] = lin_all[g0 + u][c];
+        } else {
+          recombine(cell0 + g0, L::GROUP, lin);
+          if (g0 + L::GROUP >= L::CELLS) {
+            release();
 #if LIN_TRACE
-          if (tr_on) g_lin_trace[ew][tix][2] = clock64();
+            if (tr_on) g_lin_trace[ew][tix][2] = clock64();
 #endif
+          }
         }
         double beta[L::GROUP][P];
         bool ok[L::GROUP];
@@ -269,14 +365,15 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
           cell[P] = sbr[g0 + u];
-          const double* cx = a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
+          const double* cx = L::CTX_SMEM ? cx_tile + (cell0 + g0 + u) * CX::STRIDE
+                                         : a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
           if (LIN_EXPERIMENT >= 3) {
 #pragma unroll
             for (int c = 0; c < P; ++c) beta[u][c] = cell[c] + cell[P];
             ok[u] = true;
           } else {
-            ok[u] = (L::INV_SOLVE ? solve_cell_inv<P>(cell, cx, beta[u])
-                                  : solve_cell<P>(cell, cx, beta[u])) || !cv;
+            ok[u] = (L::INV_SOLVE ? solve_cell_inv<P, L::CTX_SMEM>(cell, cx, beta[u])
+                                  : solve_cell<P, L::CTX_SMEM>(cell, cx, beta[u])) || !cv;
           }
         }
 #pragma unroll
@@ -367,6 +464,10 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             for (int c = 0; c < P; ++c) st_evict_first(dst + c, beta[u][c], pol_out);
           }
         }
+      }
+      if (L::CTX_SMEM) {  // this warp is done with the tile's contexts and scales
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctx_empty[buf]);
       }
       if (tma) nchunk += L::ROW / L::CHUNK;
 #if LIN_TRACE

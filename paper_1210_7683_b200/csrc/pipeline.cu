@@ -81,7 +81,7 @@ int run_pipeline(gwg_engine* e, const PipeSpec& sp, PipeStats* stats, gwg_status
   const size_t slab_in = size_t(n) * mb * elem;
   const size_t slab_out = size_t(mb) * t * p * sizeof(double);
   const int64_t slabs = ceil_div(m, mb);
-  const int64_t m_total = sp.i0 + m;                    // error keys: j * m_total + i
+  const int64_t m_total = kKeyStride;                   // error keys: j * kKeyStride + i
 
   // ---- buffers (pinned staging cached by the engine) ----
   if (staged_in)
@@ -112,7 +112,7 @@ int run_pipeline(gwg_engine* e, const PipeSpec& sp, PipeStats* stats, gwg_status
   cudaEvent_t* ev_hx = e->pipe_events.data();
   cudaEvent_t* ev_res = e->pipe_events.data() + 2;
 
-  if (int rc = reset_errors(e, st)) return rc;
+  if (int rc = begin_epoch(e, st)) return rc;
   for (int b = 0; b < 2; ++b) {  // fresh pipeline: every buffer starts free
     GWG_CUDA_TRY(cudaEventRecord(e->ev_rot_done[b], e->comp));
     GWG_CUDA_TRY(cudaEventRecord(e->ev_d2h_done[b], e->comp));
@@ -365,10 +365,17 @@ int run_grid_impl(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host
   e->counters.bytes_loaded += ps.loaded;
   e->counters.bytes_stored += ps.stored;
   e->counters.io_stall_ms += ps.stall_ms;
+  if (rc != GWG_OK || ps.io_error) {  // the failed run's epoch ends here
+    e->epoch_open = false;
+    e->timings_used = 0;
+  }
   if (ps.io_error == 2 && sink)
     return set_status(st, GWG_IO, -1, -1, "result sink aborted the run");
-  if (rc != GWG_OK) return rc;
-  if (int r = read_errors(e, st, true)) return r;
+  if (rc != GWG_OK) {
+    e->epoch_open = false;
+    return rc;
+  }
+  const int erc = end_epoch(e, st);  // trait, genotype and cell errors
   if (sp.checksum) {
     unsigned long long sum = 0;
     GWG_CUDA_TRY(cudaMemcpy(&sum, e->csum.ptr, sizeof(sum), cudaMemcpyDeviceToHost));
@@ -378,7 +385,7 @@ int run_grid_impl(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host
   e->counters.wall_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
   if (counters) *counters = e->counters;
-  return raise_cell_error(e, i0 + m, st);
+  return erc;
 }
 
 }  // namespace gwg_host
@@ -399,6 +406,16 @@ int32_t gwg_wait_stream(gwg_engine* e, void* stream, gwg_status* st) {
   if (!e->ev_wait) GWG_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_wait, cudaEventDisableTiming));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_wait, static_cast<cudaStream_t>(stream)));
   GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_wait, 0));
+  return GWG_OK;
+}
+
+int32_t gwg_signal_stream(gwg_engine* e, void* stream, gwg_status* st) {
+  clear_status(st);
+  if (int rc = check_engine(e, st)) return rc;
+  if (!e->ev_signal)
+    GWG_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_signal, cudaEventDisableTiming));
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_signal, e->comp));
+  GWG_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->ev_signal, 0));
   return GWG_OK;
 }
 

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int row = r0 + c * 8 + r;
-          sc[r] = row < a.n ? __ldg(a.scale + row) * 0x1p-55 : 0.0;  // exact
+          sc[r] = row < a.n ? __ldg(a.scale + row) : 0.0;  // sigma 2^-55
         }
         int32_t v[C::SLICES][8];
 #pragma unroll
@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(256) snp_to_i8_kernel(const double* __restrict
   if (!ok) *bad = 0;  // error words are reset to all ones
 }
 
-// Z (n x ncols, ld ldz) -> slices [s][r][kp] int8 and scale[r] = sigma_r: one
+// Z (n x ncols, ld ldz) -> slices [s][r][kp] int8 and scale[r] = sigma_r 2^-55 (the
+// factor that turns the recombined integer into the value, exact): one
 // block per column r (an eigenvector of Z, or a column of W for the split grid).
 // v = z / sigma (exact, |v| <= 1/2), N = rint(v 2^55) (|N| <= 2^54), written
 // in balanced base 256: N = sum_s d_s 256^(6-s) with d_6..d_1 in [-128, 127]
@@ -189,7 +190,7 @@ __global__ void slice_basis_kernel(const double* __restrict__ z, int64_t ldz, in
     int e = 0;
     frexp(m > 0.0 ? m : 1.0, &e);  // m = f 2^e, f in [0.5, 1)
     red[0] = ldexp(1.0, e + 1);
-    scale[r] = red[0];
+    scale[r] = red[0] * 0x1p-55;
   }
   __syncthreads();
   const double inv = 1.0 / red[0];  // exact: power of two

@@ -275,11 +275,18 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
   const int rc = run_pipeline(e, sp, &ps, st);
   const uint64_t loaded = ps.loaded, stored = ps.stored;
   e->counters.io_stall_ms += ps.stall_ms;
+  if (rc != GWG_OK || ps.io_error) {  // the failed run's epoch ends here
+    e->epoch_open = false;
+    e->timings_used = 0;
+  }
   if (ps.io_error)
     return set_status(st, GWG_IO, -1, -1, ps.io_error == 1 ? "short read in %s" : "short write to %s",
                       ps.io_error == 1 ? snps_path : out_path);
-  if (rc != GWG_OK) return rc;
-  if (int r = read_errors(e, st, true)) return r;
+  if (rc != GWG_OK) {
+    e->epoch_open = false;
+    return rc;
+  }
+  const int erc = end_epoch(e, st);
   e->counters.bytes_loaded += loaded;
   e->counters.bytes_stored += stored;
   e->counters.wall_ms =
@@ -287,7 +294,7 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
   if (counters) *counters = e->counters;
   // A failing cell leaves the output incomplete, like the reference (the
   // exception skips out.finalize(), grid.cpp:640; test_grid.cpp:769-771).
-  if (int r = raise_cell_error(e, m, st)) return r;
+  if (erc) return erc;
   const unsigned char zero = 0;
   if (!pwrite_all(fd_out, &zero, 1, 33))
     return set_status(st, GWG_IO, -1, -1, "cannot finalize %s", out_path);

@@ -300,7 +300,12 @@ class Engine:
 
         Returns ``out``: (mb, t, p) for layout "numpy"; (t, mb, p) for
         "stream" (the GWG1 result order (j*m + i)*p).  A torch CUDA ``out``
-        (float64, on the engine's device) keeps the results on the device.
+        (float64, on the engine's device) keeps the results on the device
+        and makes the call asynchronous, like the device work itself: it
+        returns once the work is queued on the engine's stream (torch's
+        stream.synchronize or torch.cuda.synchronize waits for it), and a
+        failing cell or trait is raised by the next synchronising call
+        (synchronize, a host-output solve, run_grid) with its coordinates.
         """
         mb = int(np.shape(x_r)[1])
         x = self._operand(x_r, (self.n, mb), "snps")
@@ -330,8 +335,16 @@ class Engine:
         try:
             self._call(self._lib.gwg_solve_snp_slab, int(i0), mb, x.ptr, x.where, int(rotated),
                        optr, owhere, lay, mb)
-        finally:
+        except BaseException:
             self._synced()
+            raise
+        if owhere != nat.GWG_DEVICE:  # synchronous: the operands were consumed
+            self._synced()
+        elif _is_torch(out):  # torch work queued after this call reads `out` in order
+            import torch
+
+            self._call(self._lib.gwg_signal_stream,
+                       torch.cuda.current_stream(out.device).cuda_stream)
         return out
 
     def run_grid(self, snps, out=None, layout: str = "numpy", mb: int = 0,

@@ -305,3 +305,28 @@ def test_config3_shape_reduced_m_checksum_and_spot_checks():
     chol = orc.cholesky_cells(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
                               ds["sigma2"], ii[:6], jj[:6])
     assert (np.linalg.norm(got[:6] - chol, axis=1) / np.linalg.norm(chol, axis=1)).max() < 1e-10
+
+
+def test_device_output_solves_are_asynchronous_with_deferred_errors(case):
+    """A device-output solve_snp_slab queues its work and returns; errors of
+    every slab since the last synchronising call surface there, the first
+    failing cell in trait-major order over all of them, with global
+    coordinates; torch work after the call is ordered after it."""
+    ds, basis, values, base = case
+    snps = ds["snps"].copy()
+    snps[:, 733] = 0.0
+    snps[:, 120] = 0.0
+    x = torch.from_numpy(snps).cuda()
+    out = torch.empty((1000, 70, 4), dtype=torch.float64, device="cuda")
+    with engine(ds, basis, values) as eng:
+        eng.solve_snp_slab(x[:, 500:].contiguous(), out=out[500:], i0=500)  # no raise yet
+        eng.solve_snp_slab(x[:, :500].contiguous(), out=out[:500], i0=0)
+        with pytest.raises(gw.NotPositiveDefiniteError) as e:
+            eng.synchronize()
+        assert (e.value.snp_index, e.value.trait_index) == (120, 0)
+        eng.synchronize()  # the epoch closed: nothing left to report
+        good = torch.from_numpy(ds["snps"]).cuda()
+        eng.solve_snp_slab(good, out=out)
+        got = out.cpu().numpy()  # torch's stream waits for the engine
+        eng.synchronize()
+    assert np.array_equal(got, base)
