@@ -216,7 +216,7 @@ int begin_epoch(gwg_engine* e, gwg_status* st) {
 
 int end_epoch(gwg_engine* e, gwg_status* st) {
   const int rc = read_errors(e, st, true);  // synchronises the compute stream
-  for (size_t k = 0; k < e->timings_used; ++k) {
+  for (size_t k = e->timings_first; k < e->timings_used; ++k) {
     const auto& tm = e->timings[k];
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, tm.ev[0], tm.ev[1]) == cudaSuccess) e->counters.rotate_ms += ms;
@@ -227,7 +227,7 @@ int end_epoch(gwg_engine* e, gwg_status* st) {
     }
   }
   cudaGetLastError();  // an event of a failed launch never recorded
-  e->timings_used = 0;
+  e->timings_used = e->timings_first = 0;
   e->epoch_open = false;
   if (rc) return rc;
   return raise_cell_error(e, st);
@@ -1414,6 +1414,7 @@ void gwg_reset_counters(gwg_engine* e) {
   if (!e) return;
   e->counters = gwg_counters{};
   e->csum_cells = 0;
+  e->timings_first = e->timings_used;  // queued solves belong to before the reset
   if (e->csum.ptr) {
     cudaSetDevice(e->device);
     cudaMemsetAsync(e->csum.ptr, 0, sizeof(unsigned long long), e->comp);

@@ -189,6 +189,7 @@ struct gwg_engine {
   };
   std::vector<SlabTiming> timings;
   size_t timings_used = 0;
+  size_t timings_first = 0;  // pending timings before a counter reset are not counted
   std::vector<cudaEvent_t> slab_events;
 
   gwg_counters counters{};

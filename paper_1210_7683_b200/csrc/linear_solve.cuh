@@ -52,8 +52,9 @@ namespace gwg {
 // S_BR: the context warp prefetches each tile's S_BR rows into L2 (bulk
 // prefetch) and the epilogue loads them after the TMEM release, instead of
 // holding a register prefetch from HBM across the accumulator wait
+// (measured slower at c1: 2.68 vs 2.45 ms; off)
 #ifndef LIN_SBR_L2PF
-#define LIN_SBR_L2PF 1
+#define LIN_SBR_L2PF 0
 #endif
 
 // Per-tile trait contexts and W-row scales staged in shared memory by bulk
@@ -200,13 +201,17 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
         int tm, tr;
         sch.coords(lt, tm, tr);
         const int j0 = tr * L::KT;
-        const int nt = min(L::KT, a.t - j0);
+        // a CTA pair along the trait axis (CL = 3) may get a tile past the
+        // last trait: nothing to copy, the phase still completes
+        const int nt = tr < a.tiles_r ? min(L::KT, a.t - j0) : 0;
         const uint32_t cbytes = uint32_t(nt) * CX::STRIDE * 8;
-        mbar_arrive_expect_tx(&ctx_full[buf], cbytes + C::RB * 8);
-        bulk_load(ctx_sm + buf * L::CTX_DOUBLES, a.ctx + int64_t(j0) * CX::STRIDE, cbytes,
-                  &ctx_full[buf], pol);
-        bulk_load(scale_sm + buf * C::RB, a.scale + int64_t(tr) * C::RB, C::RB * 8,
-                  &ctx_full[buf], pol);
+        mbar_arrive_expect_tx(&ctx_full[buf], nt > 0 ? cbytes + C::RB * 8 : 0);
+        if (nt > 0) {
+          bulk_load(ctx_sm + buf * L::CTX_DOUBLES, a.ctx + int64_t(j0) * CX::STRIDE, cbytes,
+                    &ctx_full[buf], pol);
+          bulk_load(scale_sm + buf * C::RB, a.scale + int64_t(tr) * C::RB, C::RB * 8,
+                    &ctx_full[buf], pol);
+        }
         if (LIN_SBR_L2PF) {  // this tile's S_BR rows [j][tm*BM, +BM) into L2
           const int64_t i_lo = int64_t(tm) * C::BM;
           const int64_t cnt = min(int64_t(C::BM), a.rows - i_lo);

@@ -367,7 +367,7 @@ int run_grid_impl(gwg_engine* e, int64_t m, const void* x_r_host, double* b_host
   e->counters.io_stall_ms += ps.stall_ms;
   if (rc != GWG_OK || ps.io_error) {  // the failed run's epoch ends here
     e->epoch_open = false;
-    e->timings_used = 0;
+    e->timings_used = e->timings_first = 0;
   }
   if (ps.io_error == 2 && sink)
     return set_status(st, GWG_IO, -1, -1, "result sink aborted the run");

@@ -277,7 +277,7 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
   e->counters.io_stall_ms += ps.stall_ms;
   if (rc != GWG_OK || ps.io_error) {  // the failed run's epoch ends here
     e->epoch_open = false;
-    e->timings_used = 0;
+    e->timings_used = e->timings_first = 0;
   }
   if (ps.io_error)
     return set_status(st, GWG_IO, -1, -1, ps.io_error == 1 ? "short read in %s" : "short write to %s",
