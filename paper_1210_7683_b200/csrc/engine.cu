@@ -669,6 +669,26 @@ int build_split(gwg_engine* e, gwg_status* st) {
     if (int rc = rotate(e, e->vmat.d(), ncols, e->wmat.d(), st, np, nullptr, e->basis_t.d()))
       return rc;
   }
+  if (LIN_FOLD && p > 1) {  // W_j L_j^-T and W_y - W' z_T (split_prep.cuh)
+    const gwg::CtxOffsets co = gwg::ctx_offsets(int(p));
+    gwg::FoldArgs f;
+    f.w = e->wmat.d();
+    f.n = n;
+    f.np = np;
+    f.t = int32_t(t);
+    f.p = int32_t(p);
+    f.kt = e->lops.kt;
+    f.p8 = e->lops.p8;
+    f.rb = e->lops.rb;
+    f.ctx = e->ctx.d();
+    f.stride = co.stride;
+    f.z = co.z;
+    f.flag = co.flag;
+    f.linv = co.linv;
+    gwg::fold_w_kernel<<<int(t), 256, 0, e->comp>>>(f);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+  }
   GWG_CUDA_TRY(e->wslices.ensure(size_t(I8Cfg::SLICES) * ncols * kp));
   GWG_CUDA_TRY(e->wscale.ensure(size_t(ncols) * sizeof(double)));
   gwg::slice_basis_kernel<<<int(ncols), 256, 0, e->comp>>>(e->wmat.d(), np, int32_t(n),

@@ -53,8 +53,9 @@
 namespace gwg {
 
 // Per-trait epilogue context: 1/L_aa (p-1), strictly-lower L (packed by rows),
-// z = L^-1 b_T (p-1), flag (0 ok, else chol(S_TL) failed), then the full
-// lower triangle of L^-1 (packed by rows) for solve_cell_inv.
+// z = L^-1 b_T (p-1), flag (0 ok, else chol(S_TL) failed), the full lower
+// triangle of L^-1 (packed by rows) for solve_cell_inv, and c_T = L^-T z
+// (= S_TL^-1 b_T, p-1) for the genotype grid's folded solve.
 template <int P>
 struct CtxLayout {
   static constexpr int P1 = P - 1;
@@ -65,7 +66,8 @@ struct CtxLayout {
   static constexpr int FLAG = 2 * P1 + NOFF;
   static constexpr int LINV = FLAG + 1;
   static constexpr int NLINV = P1 * (P1 + 1) / 2;
-  static constexpr int STRIDE = (LINV + NLINV + 1) & ~1;
+  static constexpr int CT = LINV + NLINV;
+  static constexpr int STRIDE = (CT + P1 + 1) & ~1;
   __host__ __device__ static constexpr int off_idx(int a, int c) { return a * (a - 1) / 2 + c; }
   __host__ __device__ static constexpr int linv_idx(int a, int c) { return a * (a + 1) / 2 + c; }
 };
@@ -239,6 +241,63 @@ __device__ __forceinline__ bool solve_cell_inv(const double* acc, const double* 
     beta[c] = s;
   }
   return ok;
+}
+
+// The genotype grid's solve with L^-1 folded into W on the trait side
+// (fold_w_kernel): the int8 MMA already yields l = L^-1 s_bl (acc[0..p-2])
+// and num = b_B - l.z_T (acc[p-1]), so per cell
+//   pivot = s_br - |l|^2,  beta_B = num / pivot,
+//   beta_T = L^-T (z_T - l beta_B) = c_T - (L^-T l) beta_B
+// with u = L^-T l an independent product (L^-1 packed by rows) that overlaps
+// the reciprocal.  Same algebra as solve_cell, a shorter dependency chain and
+// ~10 fewer FP64 operations; the pivot test is unchanged.
+template <int P, bool SMEM = false>
+__device__ __forceinline__ bool solve_cell_folded(const double* acc, const double* __restrict__ cx,
+                                                  double* beta) {
+  using L = CtxLayout<P>;
+  constexpr int P1 = L::P1;
+  double sq = 0.0;
+#pragma unroll
+  for (int a = 0; a < P1; ++a) sq = fma(acc[a], acc[a], sq);
+  double u[P1 > 0 ? P1 : 1];
+#pragma unroll
+  for (int c = 0; c < P1; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = c; a < P1; ++a) s = fma(ctx_ld<SMEM>(cx + L::LINV + L::linv_idx(a, c)), acc[a], s);
+    u[c] = s;
+  }
+  const double pivot = acc[P] - sq;
+  const bool ok = !(pivot <= 0.0) && ctx_ld<SMEM>(cx + L::FLAG) == 0.0;
+  double bb;
+  if (P <= GWG_RCP_MAXP) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(pivot));
+    r = fma(r, fma(-pivot, r, 1.0), r);
+    r = fma(r, fma(-pivot, r, 1.0), r);
+    bb = acc[P1] * r;
+  } else {
+    bb = acc[P1] / pivot;
+  }
+  beta[P1] = bb;
+#pragma unroll
+  for (int c = 0; c < P1; ++c) beta[c] = fma(-u[c], bb, ctx_ld<SMEM>(cx + L::CT + c));
+  return ok;
+}
+
+// Runtime offsets of CtxLayout<p> (host launches of the trait-side kernels).
+struct CtxOffsets {
+  int z, flag, linv, ct, stride;
+};
+__host__ __device__ inline CtxOffsets ctx_offsets(int p) {
+  const int p1 = p - 1, noff = p1 > 1 ? p1 * (p1 - 1) / 2 : 0;
+  CtxOffsets o;
+  o.z = p1 + noff;
+  o.flag = 2 * p1 + noff;
+  o.linv = o.flag + 1;
+  o.ct = o.linv + p1 * (p1 + 1) / 2;
+  o.stride = (o.ct + p1 + 1) & ~1;
+  return o;
 }
 
 // Issue the TMA/bulk loads of global k-iteration g (tile g / kchunks of this

@@ -49,6 +49,26 @@ namespace gwg {
 #define LIN_EARLY_RELEASE 1
 #endif
 
+// W folded with L_j^-1 on the trait side (fold_w_kernel): the epilogue runs
+// solve_cell_folded (the engine folds W exactly when this is on)
+#ifndef LIN_FOLD
+#define LIN_FOLD 1
+#endif
+
+// Register reallocation between warpgroups (setmaxnreg): the producer / MMA /
+// context warpgroup drops to 40 registers and the epilogue warpgroups rise to
+// LIN_MAXNREG (0 = off), with deeper per-warp interleaving (LIN_GMAX cells
+// solved together, LIN_PAIR cells per TMEM round trip) in that budget
+#ifndef LIN_MAXNREG
+#define LIN_MAXNREG 0
+#endif
+#ifndef LIN_GMAX
+#define LIN_GMAX 0
+#endif
+#ifndef LIN_PAIR
+#define LIN_PAIR 0
+#endif
+
 // S_BR: the context warp prefetches each tile's S_BR rows into L2 (bulk
 // prefetch) and the epilogue loads them after the TMEM release, instead of
 // holding a register prefetch from HBM across the accumulator wait
@@ -112,13 +132,15 @@ struct LinCfg {
   using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 3 ? 2 : CL, CL == 3 ? 1 : 0, EXTRA>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
-  static constexpr int GMAX = WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
+  static constexpr int GMAX = LIN_GMAX > 0 && P <= 4 ? LIN_GMAX
+                              : WIDE ? (P <= 4 ? 2 : 1) : (P <= 4 ? 4 : (P <= 16 ? 2 : 1));
   static constexpr int GROUP = CELLS < GMAX ? CELLS : GMAX;
   // EARLY: recombine every cell of the warp's tile share from TMEM first,
   // release the accumulator buffer, then solve and store: the MMA of tile
   // lt + ACC waits only for the recombination, not for the solves
   static constexpr bool EARLY = LIN_EARLY_RELEASE != 0 && CELLS * P <= 16;
-  static constexpr int PAIR = !EARLY && GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
+  static constexpr int PAIR = LIN_PAIR > 0 && P <= 4 && CELLS % LIN_PAIR == 0 ? LIN_PAIR
+                              : !EARLY && GROUP >= 2 && P8 <= 8 ? 2 : 1;  // cells per TMEM round trip
   // large p: triangular solves as products with L^-1 (independent dot
   // products instead of serial substitution chains)
 #ifndef LIN_INV_MINP
@@ -183,6 +205,12 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   }
   // HMAX warps per quarter release each tile's buffer
   const uint32_t tmem_base = i8_setup<C>(sm, warp, 4 * L::HMAX);
+#if LIN_MAXNREG
+  if (warp < 4)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+  else
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LIN_MAXNREG) : "memory");
+#endif
 
   if (warp == 0) {
     if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, sch, a.kstages,
@@ -377,8 +405,10 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             for (int c = 0; c < P; ++c) beta[u][c] = cell[c] + cell[P];
             ok[u] = true;
           } else {
-            ok[u] = (L::INV_SOLVE ? solve_cell_inv<P, L::CTX_SMEM>(cell, cx, beta[u])
-                                  : solve_cell<P, L::CTX_SMEM>(cell, cx, beta[u])) || !cv;
+            ok[u] = (LIN_FOLD ? solve_cell_folded<P, L::CTX_SMEM>(cell, cx, beta[u])
+                     : L::INV_SOLVE ? solve_cell_inv<P, L::CTX_SMEM>(cell, cx, beta[u])
+                                    : solve_cell<P, L::CTX_SMEM>(cell, cx, beta[u])) ||
+                    !cv;
           }
         }
 #pragma unroll

@@ -52,6 +52,38 @@ __global__ void __launch_bounds__(256) split_prep_kernel(const SplitPrepArgs a) 
   }
 }
 
+// Fold L_j^-1 into the trait's W columns (the genotype grid's linear terms),
+// so linear_solve_kernel's MMA yields the solve's intermediates directly:
+//   W'_c = sum_{d<=c} (L^-1)_{c,d} W_d   (c < p-1:  x^T W'_c = (L^-1 s_bl)_c)
+//   W'_y = W_y - sum_c z_c W'_c           (x^T W'_y = b_B - l.z_T)
+// in place, one CTA per trait, a thread per row (descending c keeps the
+// W_d it reads intact).  A trait whose chol(S_TL) failed is left as it is
+// (its cells fail through the context flag).
+struct FoldArgs {
+  double* w;          // W columns (ld np) at (j/kt)*rb + (j%kt)*p8 + c
+  int64_t n, np;
+  int32_t t, p, kt, p8, rb;
+  const double* ctx;  // CtxLayout<p> per trait
+  int32_t stride, z, flag, linv;
+};
+__global__ void __launch_bounds__(256) fold_w_kernel(const FoldArgs a) {
+  const int j = blockIdx.x;
+  const double* cx = a.ctx + size_t(j) * a.stride;
+  if (cx[a.flag] != 0.0) return;
+  const int p1 = a.p - 1;
+  double* w = a.w + (size_t(j / a.kt) * a.rb + size_t(j % a.kt) * a.p8) * a.np;
+  for (int64_t k = threadIdx.x; k < a.n; k += blockDim.x) {
+    for (int c = p1 - 1; c >= 0; --c) {
+      double v = 0.0;
+      for (int d = 0; d <= c; ++d) v = fma(cx[a.linv + c * (c + 1) / 2 + d], w[d * a.np + k], v);
+      w[c * a.np + k] = v;
+    }
+    double y = w[p1 * a.np + k];
+    for (int c = 0; c < p1; ++c) y = fma(-cx[a.z + c], w[c * a.np + k], y);
+    w[p1 * a.np + k] = y;
+  }
+}
+
 // Z^T into a separate buffer (both ld np) so the DMMA rotation kernel, which
 // computes Basis^T src, can form W = Z V.
 __global__ void transpose_kernel(const double* __restrict__ src, double* __restrict__ dst,

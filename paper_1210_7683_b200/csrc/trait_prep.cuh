@@ -188,6 +188,12 @@ __global__ void __launch_bounds__(256) trait_prep_kernel(const PrepArgs a) {
           cx[L::LINV + L::linv_idx(r, c)] = v / l[r * LD + r];
         }
       }
+      // c_T = L^-T z = S_TL^-1 b_T (back substitution) for the folded solve
+      for (int r = P1 - 1; r >= 0; --r) {
+        double v = z[r];
+        for (int q = r + 1; q < P1; ++q) v -= l[q * LD + r] * cx[L::CT + q];
+        cx[L::CT + r] = v / l[r * LD + r];
+      }
     }
     cx[L::FLAG] = ok ? 0.0 : 1.0;
   }
