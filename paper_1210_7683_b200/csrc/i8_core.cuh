@@ -15,6 +15,9 @@
 #ifndef I8_PROFILE
 #define I8_PROFILE 0
 #endif
+#ifndef I8_NO_MMA
+#define I8_NO_MMA 0
+#endif
 
 namespace gwg {
 
@@ -286,8 +289,10 @@ struct I8Smem {
   uint64_t* acc_empty;     // [ACC_BUFS]
   uint32_t* tmem_slot;
   __device__ explicit I8Smem(unsigned char* raw) {
-    base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
-                                            ~uintptr_t(1023));
+    // align by pointer arithmetic on `raw` (not through an integer cast), so
+    // the compiler keeps the shared-memory provenance of every derived
+    // pointer and emits LDS/STS instead of generic loads and stores
+    base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
     staging = base + C::STAGES * C::STAGE_BYTES;
     extra = staging + C::EPI_WARPS * C::OUT_BYTES;
     full = reinterpret_cast<uint64_t*>(extra + C::EXTRA);
@@ -480,10 +485,12 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
       tc_fence_after();
       const uint32_t sa = smem_u32(sm.base + s * C::STAGE_BYTES);
       const uint32_t sb = sa + C::A_BYTES;
+#if !I8_NO_MMA  // timing ablation only: the barrier protocol without the MMAs
 #pragma unroll
       for (int k = 0; k < C::BK / C::UK; ++k)
         umma_i8(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK), idesc,
                 (ks | k) != 0);
+#endif
       // frees the smem stage (in every CTA of the pair) when these MMAs finish
       if (C::CLUSTER > 1)
         umma_commit_mc(&sm.empty[s], mask);

@@ -48,7 +48,7 @@ def run(name, steps):
     with gw.Engine(n, p) as eng:
         eng.set_spectrum(basis, values)
         eng.set_covariates(xl)
-        eng.set_snp_coding(os.environ.get("GWG_SNP_CODING", "real"))
+        eng.set_snp_coding(os.environ.get("GWG_SNP_CODING", "genotypes"))
         stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
 
         def step():
@@ -62,6 +62,7 @@ def run(name, steps):
         e0.record(stream)
         for _ in range(steps):
             step()
+        eng.synchronize()  # device-output solves are asynchronous: read their error words
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
