@@ -36,6 +36,13 @@
 #include "rotate_kernel.cuh"
 #include "slab_kernels.cuh"
 
+#ifndef LIN_RASTER
+#define LIN_RASTER 0  // trait tiles fastest: measured 2.49-2.54 vs 2.45-2.46 ms at c1 (off)
+#endif
+#ifndef ROT_RASTER
+#define ROT_RASTER 0  // eigen-row tiles fastest: neutral at c1 (off)
+#endif
+
 namespace gwg_host {
 
 using gwg::kBK;
@@ -303,6 +310,7 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   a.gate = gate_word(e);
   a.gate_codes = e->gate_want;
+  a.raster = (ROT_RASTER == 2 || (ROT_RASTER == 1 && a.b_resident)) ? 1 : 0;
   // CTA pairs multicasting the B (Z-slice) tile when it streams from HBM
   // (measured at n = 10,000: 69.2 -> 49.0 ms; neutral at n = 1000)
   const int cl = e->i8_cluster ? (e->i8_cluster == 3 ? 2 : e->i8_cluster) : (e->n >= 4096 ? 2 : 1);
@@ -832,6 +840,9 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
   a.gate = gate_word(e);
   a.gate_codes = e->gate_want;
+  // numpy-order results with L2-resident W slices: trait tiles fastest, so
+  // the tiles in flight write contiguous rows of b (I8Sched raster)
+  a.raster = (LIN_RASTER == 2 || (LIN_RASTER == 1 && out_sj == 1 && a.b_resident)) ? 1 : 0;
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   (void)tiles;

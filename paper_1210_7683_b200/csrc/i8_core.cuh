@@ -373,10 +373,15 @@ __device__ __forceinline__ void i8_tile_coords(int tile, int tiles_m, int tiles_
 
 // Persistent static schedule over scheduling units (one CTA, or one CTA pair
 // for CLUSTER = 2: the pair takes SNP tiles 2u and 2u+1 of one B tile).
+// raster = 1: the B-tile index fastest over the whole grid instead — the 148
+// tiles in flight then cover one or two SNP tiles x every B tile, so results
+// in numpy order (SNP-major rows of t*p doubles) are written as a few
+// contiguous megabytes instead of thousands of scattered 256-byte pieces
+// (B must then stay L2-resident: the W slices of every trait)
 template <class C>
 struct I8Sched {
-  int rank, unit, units, tm_units, tiles_r, my_tiles;
-  __device__ I8Sched(int tiles_m, int tiles_r_) : tiles_r(tiles_r_) {
+  int rank, unit, units, tm_units, tiles_r, my_tiles, raster;
+  __device__ I8Sched(int tiles_m, int tiles_r_, int raster_ = 0) : tiles_r(tiles_r_), raster(raster_) {
     rank = C::CLUSTER > 1 ? int(blockIdx.x % C::CLUSTER) : 0;
     unit = int(blockIdx.x / C::CLUSTER);
     units = int(gridDim.x / C::CLUSTER);
@@ -389,7 +394,13 @@ struct I8Sched {
   int tr_units;
   __device__ void coords(int lt, int& tm, int& tr) const {
     int tu, ru;
-    i8_tile_coords(unit + lt * units, tm_units, tr_units, tu, ru);
+    if (raster) {
+      const int idx = unit + lt * units;
+      tu = idx / tr_units;
+      ru = idx - tu * tr_units;
+    } else {
+      i8_tile_coords(unit + lt * units, tm_units, tr_units, tu, ru);
+    }
     tm = C::PAIR_AXIS ? tu : tu * C::CLUSTER + rank;
     tr = C::PAIR_AXIS ? ru * 2 + rank : ru;
   }

@@ -169,6 +169,7 @@ struct LinArgs {
   unsigned long long* err_key;
   const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
   int32_t gate_codes = 0;
+  int32_t raster = 0;   // I8Sched raster: 1 = trait tiles fastest (numpy-order results)
 };
 
 #if LIN_TRACE
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   extern __shared__ __align__(1024) unsigned char smem_ls[];
   const I8Smem<C> sm(smem_ls);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const I8Sched<C> sch(a.tiles_m, a.tiles_r);
+  const I8Sched<C> sch(a.tiles_m, a.tiles_r, a.raster);
   const int my_tiles = sch.my_tiles;
   double* const ctx_sm = reinterpret_cast<double*>(sm.extra);
   double* const scale_sm = reinterpret_cast<double*>(sm.extra + L::SCALE_OFF);

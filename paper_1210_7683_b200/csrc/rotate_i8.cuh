@@ -41,6 +41,7 @@ struct I8Args {
   int32_t b_resident;   // sliced operand fits L2: keep it resident
   const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
   int32_t gate_codes = 0;
+  int32_t raster = 0;   // I8Sched raster (1: eigen-row tiles fastest)
 };
 
 // ---- the rotation kernel -------------------------------------------------------
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
   extern __shared__ __align__(1024) unsigned char smem_i8[];
   const I8Smem<C> sm(smem_i8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const I8Sched<C> sch(a.tiles_m, a.tiles_r);
+  const I8Sched<C> sch(a.tiles_m, a.tiles_r, a.raster);
   const int my_tiles = sch.my_tiles;
   const uint32_t tmem_base = i8_setup<C>(sm, warp);
 
