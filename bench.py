@@ -68,6 +68,8 @@ def parse():
                     help="skip timing the other SNP coding on the same data")
     ap.add_argument("--no-cpu", action="store_true",
                     help="skip the CPU baseline (and with it the every-cell parity)")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="engine option (gwg_set_option), e.g. i8_cluster=2; for A/B timing")
     return ap.parse_args()
 
 
@@ -177,6 +179,9 @@ def run_ours(args):
     eng.set_spectrum(shared["basis"], shared["values"])
     eng.set_covariates(shared["xl"])
     eng.set_snp_coding(args.snp_coding)
+    for opt in args.option:
+        name, value = opt.split("=", 1)
+        eng.set_option(name, int(value))
     x_dev = x_host_t.to(dev, non_blocking=False).t()  # (n, m) column-major on device
     b_dev = torch.empty((m, t, p), dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
@@ -399,6 +404,8 @@ def run_ours(args):
             "other_coding": alt,
             "preloop_eig_s": shared.get("eig_s"),
         }
+        if args.option:
+            line["config"]["engine_options"] = args.option
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
