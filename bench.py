@@ -68,6 +68,10 @@ def parse():
                     help="skip timing the other SNP coding on the same data")
     ap.add_argument("--no-cpu", action="store_true",
                     help="skip the CPU baseline (and with it the every-cell parity)")
+    ap.add_argument("--layout", default="stream", choices=["numpy", "stream"],
+                    help="result order: the reference's compute_tile ResultTile / run_grid "
+                         "result-stream order (j*m + i)*p (grid.hpp:129-148, stream.hpp:31-34; "
+                         "default), or numpy (m, t, p) as gwgrid.solve_grid reorders it on the host")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="engine option (gwg_set_option), e.g. i8_cluster=2; for A/B timing")
     return ap.parse_args()
@@ -183,12 +187,13 @@ def run_ours(args):
         name, value = opt.split("=", 1)
         eng.set_option(name, int(value))
     x_dev = x_host_t.to(dev, non_blocking=False).t()  # (n, m) column-major on device
-    b_dev = torch.empty((m, t, p), dtype=torch.float64, device=dev)
+    shape = (m, t, p) if args.layout == "numpy" else (t, m, p)
+    b_dev = torch.empty(shape, dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
 
     def step():
         eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
-        eng.solve_snp_slab(x_dev, out=b_dev, i0=i0)
+        eng.solve_snp_slab(x_dev, out=b_dev, i0=i0, layout=args.layout)
 
     def barrier():
         if world > 1:
@@ -296,7 +301,7 @@ def run_ours(args):
 
         def alt_step():
             eng.set_traits(shared["y"], shared["h2"], shared["sigma2"])
-            eng.solve_snp_slab(x_dev, out=b_alt, i0=i0)
+            eng.solve_snp_slab(x_dev, out=b_alt, i0=i0, layout=args.layout)
 
         alt_step()
         barrier()
@@ -310,7 +315,7 @@ def run_ours(args):
         barrier()
         alt_ms = a0.elapsed_time(a1) / args.steps
         acnt = eng.counters()
-        rel = ((b_alt - b_dev).norm(dim=2) / b_dev.norm(dim=2)).max().item()
+        rel = ((b_alt - b_dev).norm(dim=-1) / b_dev.norm(dim=-1)).max().item()
         alt = {"snp_coding": other, "value": cells / (alt_ms * 1e-3), "ms_per_step": alt_ms,
                "grid_kernel_ms": acnt["grid_kernel_ms"] / args.steps,
                "max_normwise_rel_diff_vs_headline": rel}
@@ -320,6 +325,9 @@ def run_ours(args):
     # ---- e2e through gwg_set_traits + gwg_run_grid with pinned host buffers --
     e2e = e2e_i8 = None
     if not args.no_e2e:
+        # e2e returns b the way gwgrid.solve_grid does, (m, t, p) in host
+        # memory: one contiguous D2H run per slab (the stream order would
+        # need a strided 2-D copy, measured slower over PCIe)
         b_host_t = torch.empty((m, t, p), dtype=torch.float64).pin_memory()
         b_host = b_host_t.numpy()
         y_host_t = torch.empty((t, n), dtype=torch.float64).pin_memory()
@@ -334,7 +342,7 @@ def run_ours(args):
         def timed_e2e(snps):
             def e2e_step():
                 eng.set_traits(y_host, h2_host, s2_host)
-                eng.run_grid(snps, out=b_host, i0=i0)
+                eng.run_grid(snps, out=b_host, i0=i0, layout="numpy")
 
             for _ in range(max(1, args.warmup - 1)):
                 e2e_step()
@@ -345,7 +353,8 @@ def run_ours(args):
                 e2e_step()
             barrier()
             e2e_s = max_over_ranks(time.perf_counter() - t0)
-            same = bool(np.array_equal(b_host, b_dev.cpu().numpy()))
+            dv = b_dev.cpu().numpy()
+            same = bool(np.array_equal(b_host, dv if args.layout == "numpy" else dv.transpose(1, 0, 2)))
             c = eng.counters()
             return e2e_s, same, c
 
@@ -355,7 +364,8 @@ def run_ours(args):
                "d2h_bytes_per_step": m * t * p * 8, "ms_per_step": 1e3 * e2e_s / args.steps,
                "io_stall_ms_per_step": c["io_stall_ms"] / args.steps,
                "api": "Engine.set_traits + Engine.run_grid (gwg_set_traits + gwg_run_grid), "
-                      "X_R as float64 (BASELINE's storage)",
+                      "X_R as float64 (BASELINE's storage), b returned as (m, t, p) like "
+                      "gwgrid.solve_grid",
                "bitwise_equal_to_device_path": same}
         e2e_s, same, c = timed_e2e(codes)
         e2e_i8 = {"value": cells * args.steps / e2e_s, "unit": "GLS/s",
@@ -372,7 +382,8 @@ def run_ours(args):
         from oracle.parity import parity_metrics
 
         cpu, ref = cpu_baseline(args, shared, x_host)
-        parity = parity_metrics(b_dev.cpu().numpy(), ref)
+        got = b_dev.cpu().numpy()
+        parity = parity_metrics(got if args.layout == "numpy" else got.transpose(1, 0, 2), ref)
         del ref
 
     if rank == 0:
@@ -384,7 +395,7 @@ def run_ours(args):
             "config": {"workload": "c1", "n": n, "p": p, "m_per_gpu": m, "t": t,
                        "cells_per_step": cells, "parallelism": f"snp-shard x{world}",
                        "l2": "inputs larger than L2 (X_R %.1f GB per GPU per step)" % (n * m * 8 / 1e9),
-                       "snp_coding": args.snp_coding,
+                       "snp_coding": args.snp_coding, "result_layout": args.layout,
                        "step": ("rotate Y (DMMA) and X_R (exact int8 tcgen05) + trait contexts "
                                 "+ split grid: S_BR = (X'.X')^T D on DMMA, linear terms x^T W exact "
                                 "on int8 tcgen05 fused with the bordered Cholesky"

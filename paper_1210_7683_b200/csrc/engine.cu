@@ -39,6 +39,9 @@
 #ifndef LIN_RASTER
 #define LIN_RASTER 0  // trait tiles fastest: measured 2.49-2.54 vs 2.45-2.46 ms at c1 (off)
 #endif
+#ifndef LIN_STREAM_TMA
+#define LIN_STREAM_TMA 1
+#endif
 #ifndef ROT_RASTER
 #define ROT_RASTER 0  // eigen-row tiles fastest: neutral at c1 (off)
 #endif
@@ -804,21 +807,36 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb,
                          e->lops.b_slices_box[cl - 1], st, e->lops.a_box_rows[cl - 1]))
     return rc;
-  // numpy layout with a 16-byte pitch and base: results leave by TMA store
-  const bool use_tma = out_sj == 1 && (out_si * p) % 2 == 0 &&
-                       (reinterpret_cast<uintptr_t>(dev_out) & 15) == 0;
+  // numpy layout with a 16-byte pitch and base: results leave by TMA store;
+  // stream layout ((j*ldo + i)*p, out_si = 1) by TMA boxes {32p, cells} when
+  // the trait pitch is 16-byte aligned
+  const bool aligned = (reinterpret_cast<uintptr_t>(dev_out) & 15) == 0;
+  const int use_tma = (out_sj == 1 && (out_si * p) % 2 == 0 && aligned) ? 1
+                      : (out_si == 1 && e->lops.stream_tma && (out_sj * p) % 2 == 0 && aligned &&
+                         LIN_STREAM_TMA) ? 2 : 0;
   {
     auto encode = get_encode();
-    const cuuint64_t gdim[2] = {cuuint64_t(t * p), cuuint64_t(rows)};
-    const cuuint64_t gstride[1] = {cuuint64_t(use_tma ? out_si * p * 8 : 16)};
-    // 16-double swizzled chunks, or one unswizzled {row, 32} box per warp tile
-    const bool tma_row = e->lops.tma_row;
-    const cuuint32_t box[2] = {tma_row ? cuuint32_t(e->lops.row) : gwg::I8Cfg::OUT_Q, 32};
-    const cuuint32_t es[2] = {1, 1};
-    CUresult r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box,
-                        es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        tma_row ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (use_tma == 2) {
+      const cuuint64_t gdim[2] = {cuuint64_t(rows * p), cuuint64_t(t)};
+      const cuuint64_t gstride[1] = {cuuint64_t(out_sj * p * 8)};
+      const cuuint32_t box[2] = {cuuint32_t(32 * p), cuuint32_t(e->lops.cells)};
+      const cuuint32_t es[2] = {1, 1};
+      r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      const cuuint64_t gdim[2] = {cuuint64_t(t * p), cuuint64_t(rows)};
+      const cuuint64_t gstride[1] = {cuuint64_t(use_tma ? out_si * p * 8 : 16)};
+      // 16-double swizzled chunks, or one unswizzled {row, 32} box per warp tile
+      const bool tma_row = e->lops.tma_row;
+      const cuuint32_t box[2] = {tma_row ? cuuint32_t(e->lops.row) : gwg::I8Cfg::OUT_Q, 32};
+      const cuuint32_t es[2] = {1, 1};
+      r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 tma_row ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (use_tma && r != CUDA_SUCCESS)
       return set_status(st, GWG_CUDA, -1, -1, "tensor map (results) failed (%d)", int(r));
   }
@@ -830,7 +848,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.out = dev_out;
   a.out_si = out_si;
   a.out_sj = out_sj;
-  a.use_tma = use_tma ? 1 : 0;
+  a.use_tma = use_tma;
   a.t = int32_t(t);
   a.rows = rows;
   a.i0 = i0;

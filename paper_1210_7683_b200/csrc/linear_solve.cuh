@@ -32,7 +32,7 @@ namespace gwg {
 // Timing ablations only (never in a shipped build): 1 = no result stores,
 // 2 = no S_BR loads, 3 = no solve, 4 = neither solve nor stores, 5 = 4 and
 // no S_BR loads and a plain sum for the recombination, 6 = 5 without the
-// TMEM loads.
+// TMEM loads, 7 = every TMA result store to the same 4 KB (no DRAM writes).
 #ifndef LIN_EXPERIMENT
 #define LIN_EXPERIMENT 0
 #endif
@@ -110,6 +110,10 @@ struct LinCfg {
   // (an odd row's last double is stored directly: a box row is a multiple of
   // 16 bytes)
   static constexpr bool TMA_ROW = !TMA_OUT && ROW >= 2 && ROW <= 33;
+  // stream order ((j*ldo + i)*p, the reference's ResultTile / result-stream
+  // layout): a warp's results are, per trait, 32 SNPs x p contiguous doubles;
+  // staged [cell][lane*p + c] and stored as one TMA box {32p, CELLS}
+  static constexpr bool STREAM_TMA = 32 * P <= 256 && CELLS * 32 * P * 8 <= 4096;
   static constexpr int BW = ROW & ~1;                     // doubles per TMA box row
   static constexpr int OUT_BUFS = TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
   static constexpr int STAGES_0 = WIDE ? 3 : 4;
@@ -157,7 +161,7 @@ struct LinArgs {
   double* out;
   int64_t out_si;       // cell strides of out
   int64_t out_sj;
-  int32_t use_tma;      // out through tmap_out (numpy layout, 16-byte pitch)
+  int32_t use_tma;      // out through tmap_out: 1 numpy layout, 2 stream layout
   int32_t t;
   int64_t rows;
   int64_t i0;
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #endif
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(qd * 32) << 16) + uint32_t(buf * C::BN);
-      const bool tma = L::TMA_OUT && a.use_tma;
+      const bool tma = L::TMA_OUT && a.use_tma == 1;
       // GROUP cells at a time: recombine their linear terms from TMEM (PAIR
       // cells per TMEM round trip), release TMEM after the last group, then
       // solve the group's independent cells together and store them.
@@ -429,6 +433,22 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < P; ++c) acc += beta[u][c];
           if (acc == 1.2345e300) a.out[il] = acc;
+        } else if (L::STREAM_TMA && a.use_tma == 2) {
+          if (g0 == 0) {
+            if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
+            __syncwarp();
+          }
+          double* rowp = reinterpret_cast<double*>(stg);
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) rowp[((g0 + u) * 32 + lane) * P + c] = beta[u][c];
+          if (g0 + L::GROUP >= L::CELLS) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0)
+              tma_store_2d(&tmap_out, stg, (tm * C::BM + qd * 32) * P, j0 + cell0);
+          }
         } else if (tma) {
           // flat index f = (g0+u)*P + c of this row; 128-byte chunks of 16
           // doubles, 16-byte units XOR-swizzled by row (SWIZZLE_128B), one
@@ -455,12 +475,17 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
               if (f % L::CHUNK == L::CHUNK - 1) {
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0)
-                  tma_store_2d(&tmap_out, tile_buf, (j0 + cell0) * P + (f / L::CHUNK) * L::CHUNK,
-                               tm * C::BM + qd * 32);
+                if (lane == 0) {
+                  if (LIN_EXPERIMENT == 7)  // timing only: the same instructions, one 4 KB target
+                    tma_store_2d(&tmap_out, tile_buf, 0, 0);
+                  else
+                    tma_store_2d(&tmap_out, tile_buf,
+                                 (j0 + cell0) * P + (f / L::CHUNK) * L::CHUNK,
+                                 tm * C::BM + qd * 32);
+                }
               }
             }
-        } else if (L::TMA_ROW && a.use_tma) {
+        } else if (L::TMA_ROW && a.use_tma == 1) {
           // the warp's ROW results per SNP row, unswizzled [lane][ROW] in the
           // staging tile, one TMA box {ROW, 32} after the tile's last group
           if (g0 == 0) {
@@ -543,6 +568,8 @@ struct LinOps {
   int b_slices_box[3] = {8, 4, 8};  // slice slots per TMA box
   int a_box_rows[3] = {128, 128, 64};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
+  int cells = 0;         // traits per epilogue warp and tile (LinCfg::CELLS)
+  bool stream_tma = false;  // stream-layout results by TMA boxes {32p, cells}
   bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
 };
 
@@ -556,6 +583,8 @@ LinOps make_lin_ops() {
   o.launch[1] = &launch_linear_solve<P, 2>;
   o.launch[2] = &launch_linear_solve<P, 3>;
   o.row = LinCfg<P>::BW;
+  o.cells = LinCfg<P>::CELLS;
+  o.stream_tma = LinCfg<P>::STREAM_TMA;
   o.tma_row = LinCfg<P>::TMA_ROW;
   return o;
 }
