@@ -146,6 +146,16 @@ struct GridArgs {
 //   beta_B = (b_B - l.z_T) / pivot     (= ((b_B - l.z_T)/lambda)/lambda;
 //                                       reciprocal by rcp.approx + Newton)
 //   beta_T = L^-T (z_T - l beta_B)
+// 1/x by the MUFU approximation and two Newton steps (<= 1 ulp for normal
+// x; far cheaper on the FP64 pipe than an IEEE division).  Flushes subnormal
+// x to zero (callers divide exactly in that case).
+__device__ __forceinline__ double rcp_newton(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
 // Context loads: read-only global (__ldg) or, SMEM, a shared-memory copy.
 template <bool SMEM>
 __device__ __forceinline__ double ctx_ld(const double* p) {
@@ -182,10 +192,11 @@ __device__ __forceinline__ bool solve_cell(const double* acc, const double* __re
   double bb;
   if (P <= GWG_RCP_MAXP) {
     double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(pivot));
-    r = fma(r, fma(-pivot, r, 1.0), r);
-    r = fma(r, fma(-pivot, r, 1.0), r);
+    r = rcp_newton(pivot);
     bb = (acc[P1] - lz) * r;
+    // a subnormal pivot is flushed by the approximation: divide exactly (the
+    // reference's LLT accepts any positive pivot)
+    if (pivot < 0x1p-1022 && pivot > 0.0) bb = (acc[P1] - lz) / pivot;
   } else {  // large p: the O(p^2) substitutions dominate; keep register pressure low
     bb = (acc[P1] - lz) / pivot;
   }
@@ -272,10 +283,9 @@ __device__ __forceinline__ bool solve_cell_folded(const double* acc, const doubl
   double bb;
   if (P <= GWG_RCP_MAXP) {
     double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(pivot));
-    r = fma(r, fma(-pivot, r, 1.0), r);
-    r = fma(r, fma(-pivot, r, 1.0), r);
+    r = rcp_newton(pivot);
     bb = acc[P1] * r;
+    if (pivot < 0x1p-1022 && pivot > 0.0) bb = acc[P1] / pivot;  // subnormal: exact division
   } else {
     bb = acc[P1] / pivot;
   }

@@ -84,3 +84,31 @@ def test_every_cell_matches_oracle(grid, coding):
               f"component {c}: device {b[w['i'], w['j'], c]!r} oracle {ref[w['i'], w['j'], c]!r} "
               f"cholesky {chol[c]!r}")
         assert dev_err < 1e-10 and orc_err < 1e-10
+
+
+@pytest.mark.parametrize("name,n,p,m,t,s", [
+    ("c2 (n = 10,000) slab", 10_000, 4, 1000, 1000, 20_000),
+    ("c4 (p = 20) slab", 2000, 20, 2000, 2000, 2000),
+])
+def test_every_cell_of_a_full_n_p_t_slab(name, n, p, m, t, s):
+    """Configs 2 and 4 at their full n, p and t, every cell of an m-SNP slab
+    (the full grids are sums of such slabs; configs 2 and 3 at full shape are
+    spot-checked in tools/run_configs_e2e.py) against the oracle, through the
+    default auto (int8) path."""
+    ds = datagen.generate(n, p, m, t, seed=31, s=s)
+    basis, values = gw.eigendecompose(ds["kinship"], device=0 if n >= 4096 else None)
+    workers = os.cpu_count() or 1
+    orc.set_blas_threads(workers)
+    ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"]),
+                           orc.rotate(basis, ds["traits"]), ds["h2"], ds["sigma2"],
+                           workers=workers)
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        b = eng.run_grid(ds["snps"])
+    assert not np.isnan(b).any()
+    res = parity_metrics(b, ref)
+    print(f"\n{name}: " + json.dumps({k: v for k, v in res.items() if k != "reference"}))
+    assert res["normwise_max"] <= 1e-10, res
+    assert res["floored5_componentwise_max"] <= 1e-8, res

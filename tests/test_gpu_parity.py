@@ -350,3 +350,30 @@ def test_engine_argument_errors():
             eng.solve_snp_slab(np.ones((15, 2)))
         with pytest.raises(gw.DimensionError):
             eng.run_grid(np.ones((16, 0)))
+
+
+def test_subnormal_pivot_is_solved_not_flushed():
+    """A positive but subnormal Schur pivot (x nearly in the span of X_L, all
+    scaled by 1e-150) is a valid cell for the reference's LLT; the device's
+    reciprocal approximation flushes subnormals, so such pivots take an exact
+    division (advisor finding: it used to give a silent NaN)."""
+    n, p, t = 16, 3, 2
+    rng = np.random.default_rng(5)
+    xl = rng.standard_normal((n, p - 1))
+    e = rng.standard_normal(n)
+    e -= xl @ np.linalg.lstsq(xl, e, rcond=None)[0]  # orthogonal to X_L
+    x = 1e-150 * (xl @ np.array([0.7, -1.3]) + 1e-5 * e / np.linalg.norm(e))
+    y = rng.standard_normal((n, t))
+    values = np.ones(n)
+    with gw.Engine(n, p) as eng:
+        eng.set_snp_coding("real")
+        eng.set_spectrum(np.eye(n), values)
+        eng.set_covariates(xl)
+        eng.set_traits(y, np.zeros(t), np.ones(t), rotated=True)
+        got = eng.solve_snp_slab(x.reshape(n, 1), rotated=True)
+    pivot = 1e-300 * 1e-10  # |x_perp|^2: subnormal
+    assert pivot < 2.2250738585072014e-308
+    ref = orc.compute_grid(values, xl, x.reshape(n, 1), y, np.zeros(t), np.ones(t))
+    assert np.isfinite(got).all()
+    rel = np.linalg.norm(got - ref, axis=2) / np.linalg.norm(ref, axis=2)
+    assert rel.max() < 1e-3, rel.max()  # the pivot itself carries ~1e-6 relative rounding
