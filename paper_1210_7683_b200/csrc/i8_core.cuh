@@ -247,9 +247,14 @@ __device__ __forceinline__ double i8_recombine(const int32_t a0, const int32_t a
 // default policy made L2 fetch the written lines from HBM first (rotation:
 // 0.49 GB of DRAM reads for 0.74 GB written; with the hint 0.11 GB, the
 // algorithmic input bytes, and 4.5% faster).
+#ifndef I8_STORE_POLICY
+#define I8_STORE_POLICY 0  // 0 evict_first, 1 evict_normal, 2 evict_last
+#endif
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
                                              int32_t c1) {
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = I8_STORE_POLICY == 1   ? policy_evict_normal()
+                       : I8_STORE_POLICY == 2 ? policy_evict_last()
+                                              : policy_evict_first();
   asm volatile(
       "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint"
       " [%0, {%1, %2}], [%3], %4;" ::"l"(reinterpret_cast<uint64_t>(map)),

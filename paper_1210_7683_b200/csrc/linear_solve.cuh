@@ -76,6 +76,9 @@ namespace gwg {
 #ifndef LIN_SBR_L2PF
 #define LIN_SBR_L2PF 0
 #endif
+#ifndef LIN_SBR_LATE  // with the L2 prefetch: load after the release (1) or before the wait (0)
+#define LIN_SBR_LATE 1
+#endif
 
 // Per-tile trait contexts and W-row scales staged in shared memory by bulk
 // copies (warp 2) instead of per-cell __ldg / shuffles in the epilogue.
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
         }
         continue;
       }
-      constexpr bool SBR_LATE = L::CTX_SMEM && L::EARLY && LIN_SBR_L2PF;
+      constexpr bool SBR_LATE = L::CTX_SMEM && L::EARLY && LIN_SBR_L2PF && LIN_SBR_LATE;
       double sbr[L::CELLS];
       auto load_sbr = [&]() {
 #pragma unroll
