@@ -30,3 +30,37 @@ for (n, p, m, t) in ((130, 4, 150, 37), (96, 1, 40, 9), (200, 8, 70, 20), (64, 2
     print(n, p, m, t, "verify", err)
 z2, l2 = gw.eigendecompose(datagen.kinship(1, 300, 600), device=0)
 print("ok")
+
+# round-2 paths: int8 input, sinks, checksum, asynchronous device solves in
+# both layouts, the device group
+import torch  # noqa: E402
+
+ds = datagen.generate(200, 4, 300, 40, seed=9)
+z, lam = gw.eigendecompose(ds["kinship"])
+codes = ds["snps"].astype(np.int8)
+with gw.Engine(200, 4) as eng:
+    eng.set_spectrum(z, lam)
+    eng.set_covariates(ds["xl"])
+    eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+    b = eng.run_grid(codes, checksum=True, mb=70)
+    got = np.empty_like(b)
+
+    def sink(i0, cells):
+        got[i0:i0 + cells.shape[0]] = cells
+
+    eng.run_grid(ds["snps"], sink=sink, mb=64, ring=3)
+    assert np.array_equal(got, b)
+    x = torch.from_numpy(ds["snps"]).cuda()
+    out = torch.empty((300, 40, 4), dtype=torch.float64, device="cuda")
+    outs = torch.empty((40, 300, 4), dtype=torch.float64, device="cuda")
+    eng.solve_snp_slab(x, out=out)
+    eng.solve_snp_slab(x, out=outs, layout="stream")
+    eng.synchronize()
+    assert np.array_equal(out.cpu().numpy(), b)
+    assert np.array_equal(outs.cpu().numpy().transpose(1, 0, 2), b)
+with gw.Group(200, 4, [0, 0]) as g:
+    g.set_spectrum(z, lam)
+    g.set_covariates(ds["xl"])
+    g.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+    assert np.array_equal(g.run_grid(codes, mb=50), b)
+print("round-2 paths ok")
