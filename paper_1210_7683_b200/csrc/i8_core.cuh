@@ -18,6 +18,9 @@
 #ifndef I8_NO_MMA
 #define I8_NO_MMA 0
 #endif
+#ifndef I8_PREFETCH  // stages ahead the producer prefetches into L2 (B not L2-resident)
+#define I8_PREFETCH 0  // measured: 4-16 stages ahead made c2 rotation 44.7 -> 72-78 ms, c4 linear 30.8 -> 41.7 ms
+#endif
 
 namespace gwg {
 
@@ -168,6 +171,21 @@ __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
       "h"(cta_mask), "l"(policy)
       : "memory");
+}
+
+// TMA prefetch of a box into L2 (no shared-memory destination, no barrier).
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 
 // 2-D TMA load multicast to the CTAs in cta_mask.
@@ -424,6 +442,11 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
   // -> 2.70 ms at c1); the results stream out evict_first (tma_store_2d).
   const uint64_t pol_x = policy_evict_normal();
   const uint64_t pol_b = b_resident ? policy_evict_last() : policy_evict_normal();
+  // B streaming from HBM (large n): prefetch the operand boxes of the stage
+  // I8_PREFETCH stages ahead into L2, so the stage ring (4 x 48 KB, ~1,800 MMA
+  // cycles) only has to cover L2 latency, not HBM latency
+  const int pf = b_resident ? 0 : I8_PREFETCH;
+  const int total = sch.my_tiles * kstages;
   int g = 0;
 #if I8_PROFILE
   long long t_empty = 0, t0 = clock64();
@@ -443,6 +466,17 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
       t_empty += clock64() - te;
 #endif
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
+      if (pf && g + pf < total) {
+        const int gf = g + pf, ltf = gf / kstages, ksf = gf - ltf * kstages;
+        int tmf, trf;
+        sch.coords(ltf, tmf, trf);
+        if (C::PAIR_AXIS == 1) {
+          tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, 0);
+        } else {
+          tma_prefetch_2d(tmap_x, ksf * C::BK, tmf * C::BM);
+          tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, sch.rank * C::B_SLICES_PER_CTA);
+        }
+      }
       mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
       if constexpr (C::PAIR_AXIS == 1) {
         // half of the shared SNP tile each (box 128 k x 64 SNPs), multicast;
