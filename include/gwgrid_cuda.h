@@ -334,7 +334,9 @@ int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
  *                       column; 0: the single fused kernel.
  *   GWG_OPT_I8_CLUSTER  0 (default, auto), 1 single CTAs, 2 CTA pairs
  *                       multicasting the W/Z-slice tile, 3 CTA pairs
- *                       multicasting the SNP tile (bitwise identical).
+ *                       multicasting the SNP tile, 4 CTA pairs running one
+ *                       cta_group::2 MMA with half of the slice tile each
+ *                       (32-row tiles; else 2) — all bitwise identical.
  *   GWG_OPT_SBR_CFG     gls_sbr_kernel tile configuration index (default 0). */
 enum gwg_option {
   GWG_OPT_SPLIT = 1,

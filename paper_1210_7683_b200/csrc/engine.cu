@@ -243,11 +243,20 @@ int end_epoch(gwg_engine* e, gwg_status* st) {
   return raise_cell_error(e, st);
 }
 
+// The int8 kernels' default launch geometry: CTA pairs running one
+// cta_group::2 MMA (half of the sliced operand per CTA, deeper operand rings)
+// once a tile has at least 16 K stages; below that the B-multicast pairs.
+// Measured (ms; B pairs -> pair MMA): rotation n = 1000 0.686 -> 0.745,
+// n = 2000 1.104 -> 1.092, n = 4000 3.85 -> 3.64, n = 10,000 44.4 -> 41.1;
+// linear_solve p = 4 n = 1000 2.40 -> 2.77, n = 2000 2.15 -> 2.10, n = 4000
+// 4.02 -> 3.69, n = 6000 6.01 -> 5.21, n = 10,000 22.1 -> 18.3.
+inline bool pair_mma_default(int64_t kp) { return kp / gwg::I8Cfg::BK >= 16; }
+
 // 2-D uint8 map over a K-major int8 operand (kp x cols) and 3-D map over
 // SLICES planes of (kp x ncols), both SWIZZLE_128B boxes for tcgen05.
 int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensorMap* tb,
               const void* slices, int64_t ncols, int rb, int slices_box, gwg_status* st,
-              int a_rows) {
+              int a_rows, CUtensorMap* tbh) {
   using gwg::I8Cfg;
   auto encode = get_encode();
   if (!encode) return set_status(st, GWG_CUDA, -1, -1, "cuTensorMapEncodeTiled unavailable");
@@ -273,6 +282,18 @@ int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensor
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 slices) failed (%d)", int(r));
+    // the half-slot box of the pair MMA (I8Tile MMA2): rb/2 rows of one slice;
+    // otherwise the same map as tb
+    const cuuint32_t hbox[3] = {I8Cfg::BK, cuuint32_t(rb / 2), 1};
+    r = tbh == nullptr ? CUDA_SUCCESS
+        : slices_box == 3
+            ? encode(tbh, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(slices), gdim,
+                     gstride, hbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+            : (*tbh = *tb, CUDA_SUCCESS);
+    if (r != CUDA_SUCCESS)
+      return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 half slices) failed (%d)", int(r));
   }
   return GWG_OK;
 }
@@ -317,18 +338,26 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   // CTA pairs multicasting the B (Z-slice) tile: halves its L2 -> SMEM
   // traffic (the rotation runs at ~77% of L2 throughput with single CTAs);
   // measured at n = 10,000: 69.2 -> 49.0 ms, at n = 1000: 0.704 -> 0.692 ms
-  const int cl = e->i8_cluster ? (e->i8_cluster == 3 ? 2 : e->i8_cluster) : 2;
-  CUtensorMap tx, tb;
+  // GWG_OPT_I8_CLUSTER = 4: CTA pairs running one cta_group::2 MMA with half
+  // of the Z-slice tile each — the default from 16 K stages (n > 1920) on
+  // (pair_mma_default)
+  const int cl = e->i8_cluster ? (e->i8_cluster == 3 ? 2 : e->i8_cluster)
+                               : pair_mma_default(kp) ? 4 : 2;
+  CUtensorMap tx, tb, tbh;
   if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB,
-                         I8Cfg::SLOTS / cl, st, I8Cfg::BM))
+                         cl == 4 ? 3 : I8Cfg::SLOTS / cl, st, I8Cfg::BM, &tbh))
     return rc;
-  const int64_t units = int64_t((a.tiles_m + cl - 1) / cl) * a.tiles_r;
-  if (cl == 2)
+  const int pair = cl >= 2 ? 2 : 1;
+  const int64_t units = int64_t((a.tiles_m + pair - 1) / pair) * a.tiles_r;
+  if (cl == 4)
+    GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<4>>(gwg::rotate_i8_kernel<4>, units, e->sms,
+                                                  e->comp, tx, tb, td[0], td[1], a, tbh));
+  else if (cl == 2)
     GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<2>>(gwg::rotate_i8_kernel<2>, units, e->sms,
-                                                  e->comp, tx, tb, td[0], td[1], a));
+                                                  e->comp, tx, tb, td[0], td[1], a, tbh));
   else
     GWG_CUDA_TRY(gwg::i8_launch<gwg::RotI8Cfg<1>>(gwg::rotate_i8_kernel<1>, units, e->sms,
-                                                  e->comp, tx, tb, td[0], td[1], a));
+                                                  e->comp, tx, tb, td[0], td[1], a, tbh));
   e->counters.kernel_launches += 1;
   return GWG_OK;
 }
@@ -802,10 +831,13 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   // the last measured slower even with one or two traits per tile (c4 33.2
   // -> 35.6 ms, p = 12 5.25 -> 5.62), so the SNP tile's L2 traffic is not
   // what bounds those configs.
-  const int cl = e->i8_cluster ? e->i8_cluster : 2;
-  CUtensorMap tx, tw, tout;
+  // GWG_OPT_I8_CLUSTER = 4: pairs running one cta_group::2 MMA (32-row W
+  // tiles; other tilings take the B pairs)
+  int cl = e->i8_cluster ? e->i8_cluster : pair_mma_default(kp) ? 4 : 2;
+  if (cl == 4 && !e->lops.launch[3]) cl = 2;
+  CUtensorMap tx, tw, tout, twh;
   if (int rc = encode_i8(&tx, e->xi8.ptr, kp, rows, &tw, e->wslices.ptr, ncols, e->lops.rb,
-                         e->lops.b_slices_box[cl - 1], st, e->lops.a_box_rows[cl - 1]))
+                         e->lops.b_slices_box[cl - 1], st, e->lops.a_box_rows[cl - 1], &twh))
     return rc;
   // numpy layout with a 16-byte pitch and base: results leave by TMA store;
   // stream layout ((j*ldo + i)*p, out_si = 1) by TMA boxes {32p, cells} when
@@ -865,7 +897,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.err_key = static_cast<unsigned long long*>(e->err.ptr) + 1;
   const int64_t tiles = int64_t(a.tiles_m) * a.tiles_r;
   (void)tiles;
-  GWG_CUDA_TRY(e->lops.launch[cl - 1](tx, tw, tout, a, e->sms, e->comp));
+  GWG_CUDA_TRY(e->lops.launch[cl - 1](tx, tw, tout, a, e->sms, e->comp, twh));
   GWG_CUDA_TRY(cudaEventRecord(sev[2], e->comp));
   e->split_timed = true;
   e->counters.kernel_launches += 1;
@@ -1423,8 +1455,8 @@ int32_t gwg_set_option(gwg_engine* e, int32_t option, int64_t value, gwg_status*
     case GWG_OPT_REAL_SPLIT:
       return flag(e->real_split);
     case GWG_OPT_I8_CLUSTER:
-      if (value < 0 || value > 3)
-        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_I8_CLUSTER takes 0..3 (got %lld)",
+      if (value < 0 || value > 4)
+        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_I8_CLUSTER takes 0..4 (got %lld)",
                           (long long)value);
       e->i8_cluster = int(value);
       return GWG_OK;

@@ -18,6 +18,9 @@
 #ifndef I8_NO_MMA
 #define I8_NO_MMA 0
 #endif
+#ifndef I8_NO_TMA  // timing ablation only: stages marked full without loading them
+#define I8_NO_TMA 0
+#endif
 #ifndef I8_PREFETCH  // stages ahead the producer prefetches into L2 (B not L2-resident)
 #define I8_PREFETCH 0  // measured: 4-16 stages ahead made c2 rotation 44.7 -> 72-78 ms, c4 linear 30.8 -> 41.7 ms
 #endif
@@ -30,7 +33,7 @@ namespace gwg {
 // rows of the sliced operand (RB = 32 for the rotation, 24 or 32 for the
 // linear terms of the split grid), K = 128 samples per stage.
 template <int RB_, int STAGES_ = 4, int OUT_BUFS_ = 1, int EPI_WARPS_ = 8, int CLUSTER_ = 1,
-          int PAIR_AXIS_ = 0, uint32_t EXTRA_ = 0>
+          int PAIR_AXIS_ = 0, uint32_t EXTRA_ = 0, bool MMA2_ = false, bool WS_ = true>
 struct I8Tile {
   // CLUSTER = 2: CTA pairs (a thread-block cluster) work on SNP tiles 2u and
   // 2u+1 against the same B rows; each CTA loads half of the B tile (4 of the
@@ -43,6 +46,20 @@ struct I8Tile {
   // the SNP tile is re-read once per trait tile and dominates L2 traffic.
   static constexpr int PAIR_AXIS = PAIR_AXIS_;
   static_assert(PAIR_AXIS == 0 || CLUSTER == 2, "trait pairs need a CTA pair");
+  // MMA2 (CLUSTER = 2, SNP-tile pairs): the pair runs ONE
+  // tcgen05.mma.cta_group::2 of M = 256 issued by the even CTA.  Each CTA
+  // keeps its own A tile and HALF of the B tile — 112 of the 224 slice rows
+  // (the even CTA slots 0-2 and rows 0-15 of slot 3, the odd CTA rows 16-31
+  // of slot 3 and slots 4-6) — and each CTA's TMEM receives its own 128 SNP
+  // rows x 224 columns, in the same column order as the single-CTA MMA.  Per
+  // CTA and stage, shared memory written by TMA and read by the MMA drops
+  // from 16 + 28 KB to 16 + 14 KB (the single-CTA kernels' operand feed is
+  // bound by shared-memory bandwidth, not by the tensor core), and the
+  // smaller stages make the ring deeper.
+  static constexpr bool MMA2 = MMA2_;
+  // WS: the producer and MMA warps run converged and one elected lane issues
+  // (see GWG_ELECT_BEGIN); otherwise one thread (lane 0) runs each loop
+  static constexpr bool WS = WS_;
   static constexpr int BM = 128;          // SNPs per tile (UMMA M, TMEM lanes)
   static constexpr int RB = RB_;          // rows of the sliced operand per tile
   // Seven signed 8-bit slices (base-256 digits of a 55-bit integer, see
@@ -59,7 +76,10 @@ struct I8Tile {
   static constexpr uint32_t B_BYTES = SLOTS * RB * BK;  // <= 32 KB of smem (slots)
   static constexpr int B_SLICES_PER_CTA = PAIR_AXIS ? SLOTS : SLOTS / CLUSTER;
   static constexpr uint32_t B_PART = PAIR_AXIS ? B_BYTES : B_BYTES / CLUSTER;  // loaded per CTA
-  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t B_SMEM = MMA2 ? SLICES * RB * BK / 2 : B_BYTES;  // B held per CTA
+  static_assert(!MMA2 || (CLUSTER == 2 && PAIR_AXIS == 0 && RB == 32),
+                "pair MMA: SNP-tile pairs on 32-row B tiles (112 rows = 14 swizzle atoms per CTA)");
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_SMEM;
   static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
   static constexpr int TMEM_COLS = 512;   // ACC_BUFS accumulator buffers x BN
@@ -79,6 +99,8 @@ struct I8Tile {
 using I8Cfg = I8Tile<32>;
 
 // ---- tcgen05 primitives --------------------------------------------------------
+
+__device__ __forceinline__ bool lane_is_0() { return (threadIdx.x & 31) == 0; }
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   // K-major SWIZZLE_128B canonical layout: 8-row x 128B atoms, SBO = 1024 B,
@@ -210,6 +232,231 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask)
       : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) primitives ----
+
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// completion of the pair's MMAs -> arrive on the same-offset mbarrier of both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+// shared::cluster address of the same-offset location in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA loads into this CTA's shared memory completing on an mbarrier that may
+// live in the peer CTA of the pair (cluster address; cta_group::2).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, uint32_t bar_cluster,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint32_t bar_cluster,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster),
+      "l"(policy)
+      : "memory");
+}
+
+// ---- warp-collective issue (the producer and MMA warps run converged) ----
+// Every lane computes the same (warp-uniform) operands, so they live in
+// uniform registers, and one lane chosen by elect.sync issues the
+// instruction.  Measured on the B200 (tools/i8_peak.cu): a single thread
+// inside a lane-0 branch issuing tcgen05.mma pays a per-instruction
+// waterfall (ELECT / R2UR.BROADCAST / BRA.U.ANY) that capped an M128 N224
+// K32 MMA stream with a commit per 4 MMAs at 2,932 TOP/s; the same stream
+// issued warp-collectively runs at 4,439 TOP/s.  elect.sync with a full
+// mask elects the same (lowest) lane every time, so a commit tracks the
+// MMAs the same lane issued.  In the kernels, where operand arrival and the
+// epilogue pace the MMA, the gain is smaller and not uniform (c1
+// linear_solve 2.39 -> 2.35 ms, c4 30.3 -> 29.3 ms; but the rotation 0.686
+// -> 0.736 ms and the cta_group::2 linear_solve at c2 18.3 -> 20.6 ms), so
+// each kernel configuration chooses (I8Tile WS).
+#define GWG_ELECT_BEGIN "{\n.reg .pred e_;\nelect.sync _|e_, 0xffffffff;\n"
+// WS = true: the warp-collective form (elected lane); false: the plain
+// instruction for a caller that is already one thread
+#define GWG_ISSUE(WS, INSTR, ...)                                    \
+  do {                                                               \
+    if constexpr (WS)                                                \
+      asm volatile(GWG_ELECT_BEGIN "@e_ " INSTR "\n}\n" __VA_ARGS__); \
+    else                                                             \
+      asm volatile(INSTR __VA_ARGS__);                               \
+  } while (0)
+
+// Barrier waits of the loops: every lane polls.  (Lane 0 polling and a
+// __syncwarp before the elected issue measured far slower: c1 linear_solve
+// 2.35 -> 3.60 ms.)
+template <bool WS>
+__device__ __forceinline__ void mbar_wait_w(uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+}
+template <bool WS>
+__device__ __forceinline__ void mbar_wait_cluster_w(uint64_t* bar, uint32_t parity) {
+  mbar_wait_cluster(bar, parity);
+}
+
+template <bool WS>
+__device__ __forceinline__ void umma_i8_w(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  if constexpr (WS)
+    asm volatile(
+        GWG_ELECT_BEGIN ".reg .pred p_;\nsetp.ne.b32 p_, %4, 0;\n"
+        "@e_ tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p_;\n}\n" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    umma_i8(tmem_d, a_desc, b_desc, idesc, accumulate);
+}
+template <bool WS>
+__device__ __forceinline__ void umma_i8_pair_w(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  if constexpr (WS)
+    asm volatile(
+        GWG_ELECT_BEGIN ".reg .pred p_;\nsetp.ne.b32 p_, %4, 0;\n"
+        "@e_ tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p_;\n}\n" ::"r"(tmem_d),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    umma_i8_pair(tmem_d, a_desc, b_desc, idesc, accumulate);
+}
+template <bool WS>
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  GWG_ISSUE(WS, "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];",
+            ::"r"(smem_u32(bar))
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void umma_commit_mc_w(uint64_t* bar, uint16_t cta_mask) {
+  GWG_ISSUE(WS,
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;",
+            ::"r"(smem_u32(bar)), "h"(cta_mask)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void umma_commit_pair_w(uint64_t* bar) {
+  GWG_ISSUE(WS,
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;",
+            ::"r"(smem_u32(bar)), "h"(uint16_t(3))
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  GWG_ISSUE(WS, "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;",
+            ::"r"(smem_u32(bar)), "r"(bytes)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  GWG_ISSUE(WS, "mbarrier.arrive.shared::cta.b64 _, [%0];", ::"r"(smem_u32(bar)) : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_2d_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                              int32_t c1, uint64_t* bar, uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(smem_u32(bar)), "l"(policy)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_3d_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                              int32_t c1, int32_t c2, uint64_t* bar,
+                                              uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_3d_mc_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint64_t* bar,
+                                                 uint16_t cta_mask, uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(c2), "r"(smem_u32(bar)), "h"(cta_mask), "l"(policy)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_2d_mc_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                                 int32_t c1, uint64_t* bar, uint16_t cta_mask,
+                                                 uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(smem_u32(bar)), "h"(cta_mask), "l"(policy)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_2d_pair_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                                   int32_t c1, uint32_t bar_cluster,
+                                                   uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(bar_cluster), "l"(policy)
+            : "memory");
+}
+template <bool WS>
+__device__ __forceinline__ void tma_load_3d_pair_w(void* dst, const CUtensorMap* map, int32_t c0,
+                                                   int32_t c1, int32_t c2, uint32_t bar_cluster,
+                                                   uint64_t policy) {
+  GWG_ISSUE(WS,
+            "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;",
+            ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+            "r"(c2), "r"(bar_cluster), "l"(policy)
+            : "memory");
+}
+
 // All threads of the cluster (release/acquire: barrier inits, smem writes).
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -334,21 +581,32 @@ __device__ __forceinline__ uint32_t i8_setup(const I8Smem<C>& sm, int warp,
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], C::CLUSTER);  // the MMA of every CTA reading this stage
+      // the MMA of every CTA reading this stage (MMA2: the pair's one MMA)
+      mbar_init(&sm.empty[s], C::MMA2 ? 1 : C::CLUSTER);
     }
     for (int b = 0; b < C::ACC_BUFS; ++b) {
       mbar_init(&sm.acc_full[b], 1);
-      mbar_init(&sm.acc_empty[b], acc_arrivals);  // one arrive per epilogue warp using it
+      // one arrive per epilogue warp using it (MMA2: of both CTAs, at the even CTA)
+      mbar_init(&sm.acc_empty[b], C::MMA2 ? 2 * acc_arrivals : acc_arrivals);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile(
-        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-            smem_u32(sm.tmem_slot)),
-        "n"(C::TMEM_COLS)
-        : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (C::MMA2) {  // both CTAs of the pair, collectively
+      asm volatile(
+          "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+              smem_u32(sm.tmem_slot)),
+          "n"(C::TMEM_COLS)
+          : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile(
+          "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+              smem_u32(sm.tmem_slot)),
+          "n"(C::TMEM_COLS)
+          : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   if (C::CLUSTER > 1)
@@ -365,16 +623,26 @@ __device__ __forceinline__ void i8_teardown(uint32_t tmem_base, int warp) {
     cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
   else
     __syncthreads();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
+  if (warp == 1) {
+    if constexpr (C::MMA2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+  }
 }
 
-// Epilogue warp: this tile's accumulator buffer may be overwritten.
+// Epilogue warp: this tile's accumulator buffer may be overwritten (MMA2: the
+// arrival goes to the even CTA, whose thread issues the pair's MMAs).
 template <class C>
 __device__ __forceinline__ void i8_acc_release(const I8Smem<C>& sm, int buf) {
-  mbar_arrive(&sm.acc_empty[buf]);
+  if constexpr (C::MMA2)
+    mbar_arrive_cluster(mapa_u32(&sm.acc_empty[buf], 0));
+  else
+    mbar_arrive(&sm.acc_empty[buf]);
 }
 
 // Tile rasterisation shared by producer and epilogues: groups of I8_GROUP_M
@@ -429,13 +697,16 @@ struct I8Sched {
   }
 };
 
-// Warp 0, one thread: A = int8 SNP tile (box 128 k x 128 SNPs), B = RB rows
+// Warp 0, all lanes converged (one elected lane issues): A = int8 SNP tile (box 128 k x 128 SNPs), B = RB rows
 // of all 8 slices (box 128 k x RB x 8).  Tiles: i8_tile_coords (the rows
 // of the sliced operand fastest, so the SNP tile is reused from L2).
+// MMA2: tmap_bh is the half-slot map (box 128 k x 16 rows x 1 slot) for the
+// B rows split between the two CTAs.
 template <class C>
 __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMap* tmap_x,
                                            const CUtensorMap* tmap_b, const I8Sched<C>& sch,
-                                           int kstages, bool b_resident) {
+                                           int kstages, bool b_resident,
+                                           const CUtensorMap* tmap_bh = nullptr) {
   // B small enough to stay in L2 for the whole launch: keep it (evict_last).
   // A (the int8 SNP tile) is re-read by every B tile of its group, so it is
   // NOT evict_first (measured: linear_solve DRAM reads 2.66 -> 1.61 GB, 2.84
@@ -461,51 +732,111 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
 #if I8_PROFILE
       long long te = clock64();
 #endif
-      if (g >= C::STAGES) mbar_wait(&sm.empty[s], ((g / C::STAGES) - 1) & 1);
+      if (g >= C::STAGES) mbar_wait_w<C::WS>(&sm.empty[s], ((g / C::STAGES) - 1) & 1);
 #if I8_PROFILE
       t_empty += clock64() - te;
 #endif
       unsigned char* st = sm.base + s * C::STAGE_BYTES;
+      if (I8_NO_TMA) {
+        if (!C::MMA2 || sch.rank == 0) mbar_arrive_w<C::WS>(&sm.full[s]);
+        continue;
+      }
+      if constexpr (C::MMA2) {
+        // both CTAs' loads complete on the even CTA's full[s], which expects
+        // the pair's bytes (a peer transfer landing first only drives the
+        // transaction count negative until then)
+        if (sch.rank == 0) mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], 2 * C::STAGE_BYTES);
+        const uint32_t fb = mapa_u32(&sm.full[s], 0);
+        tma_load_2d_pair_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, fb, pol_x);
+        unsigned char* sb = st + C::A_BYTES;
+        const int r0 = tr * C::RB;
+        constexpr int H = C::RB / 2;
+        if (sch.rank == 0) {  // B rows 0-111: slots 0-2, slot 3 rows 0-15
+          tma_load_3d_pair_w<C::WS>(sb, tmap_b, ks * C::BK, r0, 0, fb, pol_b);
+          tma_load_3d_pair_w<C::WS>(sb + 3 * C::RB * C::BK, tmap_bh, ks * C::BK, r0, 3, fb, pol_b);
+        } else {              // B rows 112-223: slot 3 rows 16-31, slots 4-6
+          tma_load_3d_pair_w<C::WS>(sb, tmap_bh, ks * C::BK, r0 + H, 3, fb, pol_b);
+          tma_load_3d_pair_w<C::WS>(sb + H * C::BK, tmap_b, ks * C::BK, r0, 4, fb, pol_b);
+        }
+        continue;
+      }
       if (pf && g + pf < total) {
         const int gf = g + pf, ltf = gf / kstages, ksf = gf - ltf * kstages;
         int tmf, trf;
         sch.coords(ltf, tmf, trf);
         if (C::PAIR_AXIS == 1) {
-          tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, 0);
+          if (lane_is_0()) tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, 0);
         } else {
-          tma_prefetch_2d(tmap_x, ksf * C::BK, tmf * C::BM);
-          tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, sch.rank * C::B_SLICES_PER_CTA);
+          if (lane_is_0()) tma_prefetch_2d(tmap_x, ksf * C::BK, tmf * C::BM);
+          if (lane_is_0()) tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, sch.rank * C::B_SLICES_PER_CTA);
         }
       }
-      mbar_arrive_expect_tx(&sm.full[s], C::STAGE_BYTES);
+      mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], C::STAGE_BYTES);
       if constexpr (C::PAIR_AXIS == 1) {
         // half of the shared SNP tile each (box 128 k x 64 SNPs), multicast;
         // this CTA's own B tile, all 8 slots
-        tma_load_2d_mc(st + sch.rank * (C::A_BYTES / 2), tmap_x, ks * C::BK,
+        tma_load_2d_mc_w<C::WS>(st + sch.rank * (C::A_BYTES / 2), tmap_x, ks * C::BK,
                        tm * C::BM + sch.rank * (C::BM / 2), &sm.full[s], 3, pol_x);
-        tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
+        tma_load_3d_w<C::WS>(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
         continue;
       }
-      tma_load_2d(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
+      tma_load_2d_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
       if (C::CLUSTER > 1)
-        tma_load_3d_mc(st + C::A_BYTES + sch.rank * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
+        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sch.rank * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
                        sch.rank * C::B_SLICES_PER_CTA, &sm.full[s],
                        uint16_t((1u << C::CLUSTER) - 1), pol_b);
       else
-        tma_load_3d(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
+        tma_load_3d_w<C::WS>(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
     }
   }
 #if I8_PROFILE
-  if (blockIdx.x < 4)
+  if (blockIdx.x < 4 && lane_is_0())
     printf("I8PROF producer cta %d total %lld wait_empty %lld\n", int(blockIdx.x), clock64() - t0,
            t_empty);
 #endif
 }
 
-// Warp 1, one thread: BK/UK tcgen05.mma per stage into the tile's TMEM buffer.
+// MMA2, even CTA only: one M = 256 tcgen05.mma.cta_group::2 per K step (its
+// 128 SNP rows and half of B here, the peer's at the same shared-memory
+// offsets), committed to both CTAs' barriers.
+template <class C>
+__device__ __forceinline__ void i8_mma_pair(const I8Smem<C>& sm, uint32_t tmem_base,
+                                            int my_tiles, int kstages) {
+  constexpr uint32_t idesc = i8_instr_desc<C::BN, 2 * C::BM>();
+  int g = 0;
+  for (int lt = 0; lt < my_tiles; ++lt) {
+    const int buf = lt % C::ACC_BUFS;
+    if (lt >= C::ACC_BUFS)
+      mbar_wait_cluster_w<C::WS>(&sm.acc_empty[buf], ((lt / C::ACC_BUFS) - 1) & 1);
+    tc_fence_after();
+    const uint32_t tmem_d = tmem_base + uint32_t(buf * C::BN);
+    for (int ks = 0; ks < kstages; ++ks, ++g) {
+      const int s = g % C::STAGES;
+      mbar_wait_w<C::WS>(&sm.full[s], (g / C::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(sm.base + s * C::STAGE_BYTES);
+      const uint32_t sb = sa + C::A_BYTES;
+#if !I8_NO_MMA
+#pragma unroll
+      for (int k = 0; k < C::BK / C::UK; ++k)
+        umma_i8_pair_w<C::WS>(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK),
+                     idesc, (ks | k) != 0);
+#endif
+      umma_commit_pair_w<C::WS>(&sm.empty[s]);  // frees stage s in both CTAs
+    }
+    umma_commit_pair_w<C::WS>(&sm.acc_full[buf]);  // both CTAs' accumulators ready
+  }
+}
+
+// Warp 1, all lanes converged (one elected lane issues): BK/UK tcgen05.mma per
+// stage into the tile's TMEM buffer.
 template <class C>
 __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, int my_tiles,
                                        int kstages) {
+  if constexpr (C::MMA2) {
+    if (blockIdx.x % 2 == 0) i8_mma_pair<C>(sm, tmem_base, my_tiles, kstages);
+    return;
+  }
   constexpr uint16_t mask = uint16_t((1u << C::CLUSTER) - 1);
   constexpr uint32_t idesc = i8_instr_desc<C::BN, C::BM>();
   int g = 0;
@@ -517,7 +848,7 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
 #if I8_PROFILE
     long long ta = clock64();
 #endif
-    if (lt >= C::ACC_BUFS) mbar_wait(&sm.acc_empty[buf], ((lt / C::ACC_BUFS) - 1) & 1);
+    if (lt >= C::ACC_BUFS) mbar_wait_w<C::WS>(&sm.acc_empty[buf], ((lt / C::ACC_BUFS) - 1) & 1);
 #if I8_PROFILE
     t_acc += clock64() - ta;
 #endif
@@ -528,7 +859,7 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
 #if I8_PROFILE
       long long tf = clock64();
 #endif
-      mbar_wait(&sm.full[s], (g / C::STAGES) & 1);
+      mbar_wait_w<C::WS>(&sm.full[s], (g / C::STAGES) & 1);
 #if I8_PROFILE
       t_full += clock64() - tf;
 #endif
@@ -538,19 +869,19 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
 #if !I8_NO_MMA  // timing ablation only: the barrier protocol without the MMAs
 #pragma unroll
       for (int k = 0; k < C::BK / C::UK; ++k)
-        umma_i8(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK), idesc,
+        umma_i8_w<C::WS>(tmem_d, umma_desc_sw128(sa + k * C::UK), umma_desc_sw128(sb + k * C::UK), idesc,
                 (ks | k) != 0);
 #endif
       // frees the smem stage (in every CTA of the pair) when these MMAs finish
       if (C::CLUSTER > 1)
-        umma_commit_mc(&sm.empty[s], mask);
+        umma_commit_mc_w<C::WS>(&sm.empty[s], mask);
       else
-        umma_commit(&sm.empty[s]);
+        umma_commit_w<C::WS>(&sm.empty[s]);
     }
-    umma_commit(&sm.acc_full[buf]);  // accumulator ready for the epilogue
+    umma_commit_w<C::WS>(&sm.acc_full[buf]);  // accumulator ready for the epilogue
   }
 #if I8_PROFILE
-  if (blockIdx.x < 4)
+  if (blockIdx.x < 4 && lane_is_0())
     printf("I8PROF mma cta %d tiles %d total %lld wait_acc_empty %lld wait_full %lld\n",
            int(blockIdx.x), my_tiles, clock64() - t0, t_acc, t_full);
 #endif

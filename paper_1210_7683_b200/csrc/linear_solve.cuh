@@ -82,6 +82,11 @@ namespace gwg {
 
 // Per-tile trait contexts and W-row scales staged in shared memory by bulk
 // copies (warp 2) instead of per-cell __ldg / shuffles in the epilogue.
+// producer and MMA loops run warp-collectively (I8Tile WS)
+#ifndef LIN_WS
+#define LIN_WS 1
+#endif
+
 #ifndef LIN_CTX_SMEM
 #define LIN_CTX_SMEM 1
 #endif
@@ -119,8 +124,12 @@ struct LinCfg {
   static constexpr bool STREAM_TMA = 32 * P <= 256 && CELLS * 32 * P * 8 <= 4096;
   static constexpr int BW = ROW & ~1;                     // doubles per TMA box row
   static constexpr int OUT_BUFS = TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
-  static constexpr int STAGES_0 = WIDE ? 3 : 4;
-  static constexpr uint32_t STAGE_B = 128 * 128 + 8 * RB * 128;
+  // CL = 4: CTA pairs running one cta_group::2 MMA, half of B per CTA
+  // (I8Tile MMA2; 32-row W tiles only)
+  static constexpr bool MMA2 = CL == 4;
+  static_assert(!MMA2 || RB == 32, "pair MMA on 32-row W tiles");
+  static constexpr int STAGES_0 = MMA2 ? (WIDE ? 5 : 6) : WIDE ? 3 : 4;
+  static constexpr uint32_t STAGE_B = MMA2 ? 128 * 128 + 7 * RB * 64 : 128 * 128 + 8 * RB * 128;
   // shared-memory context staging, per accumulator buffer: the tile's KT trait
   // contexts (CtxLayout, contiguous in global memory) and RB W-row scales,
   // then the ctx_full / ctx_empty mbarriers
@@ -130,13 +139,15 @@ struct LinCfg {
   static constexpr uint32_t SCALE_OFF = ACC * CTX_BYTES;
   static constexpr uint32_t BAR_OFF = SCALE_OFF + ACC * RB * 8;
   static constexpr uint32_t EXTRA = CTX_SMEM ? BAR_OFF + 2 * ACC * 8 : 0;
-  static constexpr int STAGES =
-      size_t(STAGES_0) * STAGE_B + size_t(EPI) * OUT_BUFS * 4096 + (EXTRA + 15) / 16 * 16 + 1280 <=
-              227 * 1024
-          ? STAGES_0
-          : STAGES_0 - 1;
+  static constexpr size_t FIXED_B = size_t(EPI) * OUT_BUFS * 4096 + (EXTRA + 15) / 16 * 16 + 1280;
+  static constexpr int STAGES = size_t(STAGES_0) * STAGE_B + FIXED_B <= 227 * 1024 ? STAGES_0
+                                : size_t(STAGES_0 - 1) * STAGE_B + FIXED_B <= 227 * 1024
+                                    ? STAGES_0 - 1
+                                    : STAGES_0 - 2;
   // CL = 3: CTA pairs along the trait axis sharing (multicasting) the SNP tile
-  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 3 ? 2 : CL, CL == 3 ? 1 : 0, EXTRA>;
+  // warp-collective issue except for the pair MMA (measured, see i8_core.cuh)
+  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL >= 2 ? 2 : 1, CL == 3 ? 1 : 0, EXTRA, MMA2,
+                      LIN_WS != 0 && !MMA2>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = LIN_GMAX > 0 && P <= 4 ? LIN_GMAX
@@ -191,7 +202,8 @@ template <int P, int CL>
 __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     linear_solve_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const __grid_constant__ CUtensorMap tmap_w,
-                        const __grid_constant__ CUtensorMap tmap_out, const LinArgs a) {
+                        const __grid_constant__ CUtensorMap tmap_out, const LinArgs a,
+                        const __grid_constant__ CUtensorMap tmap_wh) {
   if (gate_closed(a.gate, a.gate_codes)) return;
   using L = LinCfg<P, CL>;
   using C = typename L::Tile;
@@ -221,10 +233,10 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #endif
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_w, sch, a.kstages,
-                                    a.b_resident != 0);
+    if (C::WS || lane == 0)
+      i8_produce<C>(sm, &tmap_x, &tmap_w, sch, a.kstages, a.b_resident != 0, &tmap_wh);
   } else if (warp == 1) {
-    if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
+    if (C::WS || lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
   } else if (warp == 2) {
     // context producer: tile lt's KT trait contexts and RB W-row scales into
     // the slot of its accumulator buffer once the epilogue of tile lt - ACC
@@ -554,22 +566,25 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 template <int P, int CL>
 cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int sms,
-                                cudaStream_t s) {
+                                cudaStream_t s, const CUtensorMap& twh) {
   using C = typename LinCfg<P, CL>::Tile;
   const int64_t units = C::PAIR_AXIS ? int64_t(a.tiles_m) * ((a.tiles_r + 1) / 2)
-                                     : int64_t((a.tiles_m + CL - 1) / CL) * a.tiles_r;
-  return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a);
+                                     : int64_t((a.tiles_m + C::CLUSTER - 1) / C::CLUSTER) *
+                                           a.tiles_r;
+  return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a, twh);
 }
 
 // Per-p entry of the split grid (kernels_lin_*.cu).
 struct LinOps {
   int kt = 0, p8 = 0, rb = 0;
   // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile;
-  // [2]: CTA pairs on two B tiles sharing (multicasting) the SNP tile
-  cudaError_t (*launch[3])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                           const LinArgs&, int, cudaStream_t) = {nullptr, nullptr, nullptr};
-  int b_slices_box[3] = {8, 4, 8};  // slice slots per TMA box
-  int a_box_rows[3] = {128, 128, 64};  // SNP rows per TMA box of the A tile
+  // [2]: CTA pairs on two B tiles sharing (multicasting) the SNP tile;
+  // [3]: CTA pairs running one cta_group::2 MMA (32-row W tiles; else null)
+  cudaError_t (*launch[4])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                           const LinArgs&, int, cudaStream_t, const CUtensorMap&) = {
+      nullptr, nullptr, nullptr, nullptr};
+  int b_slices_box[4] = {8, 4, 8, 3};  // slice slots per TMA box (pair MMA: + a half-slot box)
+  int a_box_rows[4] = {128, 128, 64, 128};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
   int cells = 0;         // traits per epilogue warp and tile (LinCfg::CELLS)
   bool stream_tma = false;  // stream-layout results by TMA boxes {32p, cells}
@@ -585,6 +600,7 @@ LinOps make_lin_ops() {
   o.launch[0] = &launch_linear_solve<P, 1>;
   o.launch[1] = &launch_linear_solve<P, 2>;
   o.launch[2] = &launch_linear_solve<P, 3>;
+  if constexpr (LinCfg<P>::RB == 32) o.launch[3] = &launch_linear_solve<P, 4>;
   o.row = LinCfg<P>::BW;
   o.cells = LinCfg<P>::CELLS;
   o.stream_tma = LinCfg<P>::STREAM_TMA;

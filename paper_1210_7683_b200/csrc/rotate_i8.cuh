@@ -46,16 +46,22 @@ struct I8Args {
 
 // ---- the rotation kernel -------------------------------------------------------
 
-// CL: 1 single CTAs, 2 CTA pairs multicasting B
+// CL: 1 single CTAs, 2 CTA pairs multicasting B, 4 CTA pairs running one
+// cta_group::2 MMA with half of B each (30 KB stages, 6 deep)
+#ifndef ROT_WS  // producer and MMA loops warp-collective (I8Tile WS; measured slower here)
+#define ROT_WS 0
+#endif
 template <int CL>
-using RotI8Cfg = I8Tile<32, 4, 1, 8, CL>;
+using RotI8Cfg = std::conditional_t<CL == 4, I8Tile<32, 6, 1, 8, 2, 0, 0, true, ROT_WS != 0>,
+                                    I8Tile<32, 4, 1, 8, CL, 0, 0, false, ROT_WS != 0>>;
 
 template <int CL>
 __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
     rotate_i8_kernel(const __grid_constant__ CUtensorMap tmap_x,
                      const __grid_constant__ CUtensorMap tmap_z,
                      const __grid_constant__ CUtensorMap tmap_d,
-                     const __grid_constant__ CUtensorMap tmap_d2, const I8Args a) {
+                     const __grid_constant__ CUtensorMap tmap_d2, const I8Args a,
+                     const __grid_constant__ CUtensorMap tmap_zh) {
   if (gate_closed(a.gate, a.gate_codes)) return;
   using C = RotI8Cfg<CL>;
   static_assert(C::ACC_BUFS == 2, "epilogue alternates two accumulator buffers");
@@ -67,10 +73,10 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
   const uint32_t tmem_base = i8_setup<C>(sm, warp);
 
   if (warp == 0) {
-    if (lane == 0) i8_produce<C>(sm, &tmap_x, &tmap_z, sch, a.kstages,
-                                    a.b_resident != 0);
+    if (C::WS || lane == 0)
+      i8_produce<C>(sm, &tmap_x, &tmap_z, sch, a.kstages, a.b_resident != 0, &tmap_zh);
   } else if (warp == 1) {
-    if (lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
+    if (C::WS || lane == 0) i8_mma<C>(sm, tmem_base, my_tiles, a.kstages);
   } else if (warp >= 4) {
     // ---- epilogue: warp w reads TMEM lanes 32*(w%4).. (its SNP quarter) and
     // columns h*16..h*16+15 of every slice; exact int64 recombination (see

@@ -21,13 +21,17 @@ from paper_1210_7683_b200 import datagen  # noqa: E402
 
 PEAK = 37.15
 SLAB = {"c0": 10_000, "c1": 100_000, "c2": 100_000, "c3": 4_736, "c4": 50_000,
-        "p8": 50_000, "p12": 50_000, "p13": 50_000}
+        "p8": 50_000, "p12": 50_000, "p13": 50_000, "n2k": 50_000, "n4k": 50_000,
+        "n6k": 50_000}
 EXTRA = {"p8": datagen.GridConfig("p8", 1000, 8, 50_000, 1000, 2000),
          "p12": datagen.GridConfig("p12", 1000, 12, 50_000, 1000, 2000),
-         "p13": datagen.GridConfig("p13", 1000, 13, 50_000, 1000, 2000)}
+         "p13": datagen.GridConfig("p13", 1000, 13, 50_000, 1000, 2000),
+         "n2k": datagen.GridConfig("n2k", 2000, 4, 50_000, 1000, 4000),
+         "n4k": datagen.GridConfig("n4k", 4000, 4, 50_000, 1000, 8000),
+         "n6k": datagen.GridConfig("n6k", 6000, 4, 50_000, 1000, 12000)}
 
 
-def run(name, steps):
+def run(name, steps, options=()):
     cfg = datagen.CONFIGS.get(name) or EXTRA[name]
     n, p, t, m = cfg.n, cfg.p, cfg.t, SLAB[name]
     seed = 7
@@ -49,6 +53,9 @@ def run(name, steps):
         eng.set_spectrum(basis, values)
         eng.set_covariates(xl)
         eng.set_snp_coding(os.environ.get("GWG_SNP_CODING", "genotypes"))
+        for opt in options:
+            k, v = opt.split("=")
+            eng.set_option(k, int(v))
         stream = torch.cuda.ExternalStream(eng.compute_stream, device=dev)
 
         def step():
@@ -69,7 +76,7 @@ def run(name, steps):
         c = eng.counters()
     kern = c["grid_kernel_ms"] / steps
     grid_flops = m * t * 2 * n * (p + 1)
-    return {"build": os.environ.get("GWG_BUILD_TAG", ""), "config": name, "n": n, "p": p, "t": t, "m_slab": m, "ms_per_step": ms,
+    return {"build": os.environ.get("GWG_BUILD_TAG", ""), "options": list(options), "config": name, "n": n, "p": p, "t": t, "m_slab": m, "ms_per_step": ms,
             "gls_per_s": m * t / (ms * 1e-3), "step_tflops_grid_convention": grid_flops / ms / 1e9,
             "grid_kernel_ms": kern, "grid_kernel_tflops": grid_flops / kern / 1e9,
             "grid_kernel_frac_of_peak": grid_flops / kern / 1e9 / PEAK,
@@ -83,9 +90,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c0,c1,c2,c3,c4")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="engine option (gwg_set_option), e.g. i8_cluster=4")
     args = ap.parse_args()
     for name in args.configs.split(","):
-        print(json.dumps(run(name, args.steps)), flush=True)
+        print(json.dumps(run(name, args.steps, args.option)), flush=True)
 
 
 if __name__ == "__main__":
