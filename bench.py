@@ -39,11 +39,12 @@ METRIC = "GLS problems solved/sec (m·t/s) at n=1000,p=4; FP64 TFLOP/s vs B200 p
 PEAK_FP64_TFLOPS = 37.15  # measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.txt
 I8_SLICES = 7  # int8 slices of W per linear term (i8_core.cuh, slice_basis_kernel)
 # int8 dense tensor peak measured on this pool's B200 (tools/i8_peak.cu:
-# tcgen05.mma kind::i8 M128 N256 K32 from resident smem, 148 CTAs, 1965 MHz);
-# MEASURED_PEAKS.json has no int8 entry
-PEAK_INT8_TOPS = 4346.0
-PEAK_INT8_SOURCE = ("measured: tcgen05.mma.kind::i8 issue loop on this pool's B200 "
-                    "(profiles/r01_i8_peak.txt)")
+# tcgen05.mma kind::i8 M128 N256 K32 from resident smem, warp-collective
+# elected issue, 148 CTAs, 1965 MHz — the best of its issue modes; round 1's
+# single-thread issue loop reached 4346); MEASURED_PEAKS.json has no int8 entry
+PEAK_INT8_TOPS = 4462.0
+PEAK_INT8_SOURCE = ("measured: tcgen05.mma.kind::i8 M128 N256 K32 issue loop (warp-elected) "
+                    "on this pool's B200 (profiles/r02_i8_peak.txt)")
 PEAK_SOURCE = ("measured: DMMA.8x8x4 issue loop on this pool's B200 at 1965 MHz "
                "(profiles/r01_fp64_peak.txt; = 148 SM x 128 flop/clk x 1.965 GHz; "
                "MEASURED_PEAKS.json holds no FP64 figure)")

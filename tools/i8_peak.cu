@@ -2,7 +2,8 @@
 // M128 x N256 x K32 per instruction, operands resident in shared memory (no
 // TMA in the loop), accumulators in TMEM — the ceiling for rotate_i8_kernel and
 // linear_solve_kernel.  One CTA per SM, one issuing thread, commits every 64
-// MMAs to bound the async queue.
+// MMAs to bound the async queue.  Issue modes: one thread in a lane-0 branch,
+// or the whole warp with one lane elected per instruction (the faster form).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I ../paper_1210_7683_b200/csrc i8_peak.cu -o i8_peak
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -108,23 +109,27 @@ int main() {
   cudaFuncSetAttribute(i8_peak_kernel<224, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(i8_peak_kernel<224, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(i8_peak_kernel<224, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(i8_peak_kernel<256, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(i8_peak_kernel<224, 104>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("# NVIDIA B200 SMs=%d clock=%d kHz; tcgen05.mma.kind::i8 M%d N{256,224} K%d\n", sms, clk,
          C::BM, C::UK);
-  for (int v : {0, 1, 2, 3, 4, 5}) {
-    const int bn = v == 0 ? 256 : 224;
+  for (int v : {0, 1, 2, 3, 4, 5, 6}) {
+    const int bn = v == 0 || v == 6 ? 256 : 224;
     auto kern = v == 0 ? i8_peak_kernel<256> : v == 1 ? i8_peak_kernel<224>
                 : v == 2 ? i8_peak_kernel<224, 1> : v == 3 ? i8_peak_kernel<224, 4>
-                : v == 4 ? i8_peak_kernel<224, 100> : i8_peak_kernel<224, 104>;
-    const char* modes[6] = {"two accumulators", "two accumulators", "one accumulator",
+                : v == 4 ? i8_peak_kernel<224, 100> : v == 5 ? i8_peak_kernel<224, 104>
+                : i8_peak_kernel<256, 100>;
+    const char* modes[7] = {"two accumulators (one thread)", "two accumulators (one thread)",
+                            "one accumulator (one thread)",
                             "one accumulator, commit per 4 (one thread)",
                             "one accumulator (warp, elect.sync)",
-                            "one accumulator, commit per 4 (warp, elect.sync)"};
+                            "one accumulator, commit per 4 (warp, elect.sync)",
+                            "one accumulator (warp, elect.sync)"};
     const char* mode = modes[v];
-    for (int iters : {2000}) {
+    for (int iters : {2000, 8000}) {
       kern<<<sms, 128, smem>>>(20, sink);  // warm-up
       cudaEventRecord(e0);
       kern<<<sms, 128, smem>>>(iters, sink);
