@@ -799,6 +799,26 @@ int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t 
   return gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false);
 }
 
+// The trait-side operands of the split grid (W, its slices, E/F) depend only
+// on the spectrum and the traits.  When they are due, mark the fork point on
+// the compute stream before the SNP-side work of the slab (its upload and
+// rotation) is queued: launch_split then builds them on the side stream from
+// that point on — concurrently with the SNP side — and the compute stream
+// joins before the S_BR stage.  Only below 16 K stages (n <= 1920), where the
+// trait-side build is small next to the HBM-bound SNP conversion it overlaps:
+// measured step c0 0.554 -> 0.540 ms, c1 4.43 -> 4.39, p = 12 6.50 -> 6.45;
+// at n = 10,000 the W build (8e11 flop) slowed the concurrent rotation 43.9 ->
+// 55.1 ms (step 87.9 -> 89.8), at n = 2000 (c4) 39.6 -> 40.4.
+int mark_trait_fork(gwg_engine* e, bool rotated_input, gwg_status* st) {
+  e->fork_pending = false;
+  if (!e->split || e->split_valid || rotated_input || e->snp_coding == GWG_SNP_REAL ||
+      e->n >= kMaxGenotypeN || e->t <= 0 || pair_mma_default(round_up(e->n, gwg::I8Cfg::BK)))
+    return GWG_OK;
+  GWG_CUDA_TRY(cudaEventRecord(e->ev_fork, e->comp));
+  e->fork_pending = true;
+  return GWG_OK;
+}
+
 int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, int64_t m_total,
                  double* dev_out, int64_t out_si, int64_t out_sj, gwg_status* st) {
   {
@@ -807,7 +827,20 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     // FP64 path under GWG_SNP_AUTO cannot leave a stale W marked valid.
     const int saved_gate = e->gate_want;
     e->gate_want = -1;
-    const int rc = build_split(e, st);
+    int rc;
+    if (e->fork_pending && !e->split_valid) {  // on the side stream from the fork point
+      e->fork_pending = false;
+      GWG_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+      std::swap(e->comp, e->side);
+      rc = build_split(e, st);
+      std::swap(e->comp, e->side);
+      if (rc == GWG_OK) {
+        GWG_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
+        GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_join, 0));
+      }
+    } else {
+      rc = build_split(e, st);
+    }
     e->gate_want = saved_gate;
     if (rc) return rc;
   }
@@ -1237,6 +1270,10 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     return bail("stream", err);
   if ((err = cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking)) != cudaSuccess)
     return bail("stream", err);
+  if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail("stream", err);
+  cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming);
   for (int b = 0; b < 2; ++b) {
     cudaEventCreateWithFlags(&e->ev_h2d[b], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&e->ev_rot_done[b], cudaEventDisableTiming);
@@ -1267,6 +1304,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->comp) cudaStreamSynchronize(e->comp);
   if (e->h2d) cudaStreamSynchronize(e->h2d);
   if (e->d2h) cudaStreamSynchronize(e->d2h);
+  if (e->side) cudaStreamSynchronize(e->side);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
@@ -1283,7 +1321,7 @@ void gwg_engine_destroy(gwg_engine* e) {
     if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
   }
   for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2],
-                         e->ev_wait, e->ev_signal})
+                         e->ev_wait, e->ev_signal, e->ev_fork, e->ev_join})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->pipe_events) cudaEventDestroy(ev);
@@ -1295,6 +1333,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->comp) cudaStreamDestroy(e->comp);
   if (e->h2d) cudaStreamDestroy(e->h2d);
   if (e->d2h) cudaStreamDestroy(e->d2h);
+  if (e->side) cudaStreamDestroy(e->side);
   delete e;
 }
 
@@ -1371,6 +1410,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     e->timings.push_back(tm);
   }
   gwg_engine::SlabTiming& tmg = e->timings[e->timings_used++];
+  if (int rc = mark_trait_fork(e, is_rotated, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(tmg.ev[0], e->comp));
   if (is_rotated) {
     if (int rc = upload_cols(e, e->rot, x_r, n, mb, where, e->comp, st)) return rc;

@@ -93,6 +93,11 @@ struct gwg_engine {
   gwg::LinOps lops;  // genotype split grid: per-p linear-solve kernel
   gwg::SbrOps sops;  // genotype split grid: S_BR kernel configuration
   cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
+  // trait-side operands of the split grid built concurrently with the SNP
+  // side (mark_trait_fork / launch_split): side stream, fork and join events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool fork_pending = false;
 
   gwg_host::DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
   bool have_spectrum = false, have_covariates = false;
@@ -209,6 +214,7 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
            int64_t ldd = 0);
 // Split-grid trait operands (W slices, D panels) for the current traits.
 int build_split(gwg_engine* e, gwg_status* st);
+int mark_trait_fork(gwg_engine* e, bool rotated_input, gwg_status* st);
 // Genotype split grid on raw slabs: X' is never materialised (only X'.X').
 bool rotated_x_unused(const gwg_engine* e);
 // exact int32 slice products need n * 127 * 128 < 2^31

@@ -168,7 +168,9 @@ int run_pipeline(gwg_engine* e, const PipeSpec& sp, PipeStats* stats, gwg_status
       }
     });
 
-  int rc = GWG_OK;
+  // the split grid's trait-side build runs on the side stream from here on,
+  // under the first slab's upload and rotation
+  int rc = mark_trait_fork(e, sp.rotated, st);
   for (int64_t s = 0; s < slabs && rc == GWG_OK; ++s) {
     const int bd = int(s % nb), hb = int(s & 1);
     const int64_t il0 = s * mb, rows = std::min(mb, m - il0);
