@@ -336,7 +336,9 @@ int32_t gwg_set_snp_coding(gwg_engine* e, int32_t coding, gwg_status* st);
  *                       multicasting the W/Z-slice tile, 3 CTA pairs
  *                       multicasting the SNP tile, 4 CTA pairs running one
  *                       cta_group::2 MMA with half of the slice tile each
- *                       (32-row tiles; else 2) — all bitwise identical.
+ *                       (32-row tiles; else 2), 5 2 x 2 clusters multicasting
+ *                       halves of both operands (linear terms; the rotation
+ *                       takes 2) — all bitwise identical.
  *   GWG_OPT_SBR_CFG     gls_sbr_kernel tile configuration index (default 0). */
 enum gwg_option {
   GWG_OPT_SPLIT = 1,

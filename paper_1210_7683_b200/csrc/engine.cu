@@ -39,6 +39,19 @@
 #ifndef LIN_RASTER
 #define LIN_RASTER 0  // trait tiles fastest: measured 2.49-2.54 vs 2.45-2.46 ms at c1 (off)
 #endif
+#ifndef SNP_I8_BLOCKS  // blocks per SM of the code conversion
+#define SNP_I8_BLOCKS 8
+#endif
+#ifndef GWG_TRAITS_ON_SIDE  // gwg_set_traits' device work on the side stream (split path)
+#define GWG_TRAITS_ON_SIDE 1
+#endif
+#ifndef GWG_SIDE_PRIORITY
+#define GWG_SIDE_PRIORITY 1
+#endif
+// stream layout by direct 256-bit stores (p % 4 == 0) instead of TMA boxes
+#ifndef LIN_STREAM_STG
+#define LIN_STREAM_STG 0
+#endif
 #ifndef LIN_STREAM_TMA
 #define LIN_STREAM_TMA 1
 #endif
@@ -99,12 +112,22 @@ bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-int check_engine(gwg_engine* e, gwg_status* st) {
+int check_engine(gwg_engine* e, gwg_status* st, bool join) {
   if (!e) return set_status(st, GWG_DIMENSION, -1, -1, "null engine");
   cudaError_t err = cudaSetDevice(e->device);
   if (err != cudaSuccess)
     return set_status(st, GWG_CUDA, -1, -1, "cudaSetDevice: %s", cudaGetErrorString(err));
+  if (join) GWG_CUDA_TRY(join_side(e));
   return GWG_OK;
+}
+
+// The compute stream waits for the trait-side work queued on the side stream.
+cudaError_t join_side(gwg_engine* e) {
+  if (!e->side_pending) return cudaSuccess;
+  e->side_pending = false;
+  cudaError_t err = cudaEventRecord(e->ev_join, e->side);
+  if (err == cudaSuccess) err = cudaStreamWaitEvent(e->comp, e->ev_join, 0);
+  return err;
 }
 
 int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int where,
@@ -190,6 +213,7 @@ int rotate(gwg_engine* e, const double* src, int64_t cols, double* dst, gwg_stat
 }
 
 int read_errors(gwg_engine* e, gwg_status* st, bool slab_checks) {
+  GWG_CUDA_TRY(join_side(e));  // the trait word is written by the context build
   GWG_CUDA_TRY(cudaMemcpyAsync(e->err_host, e->err.ptr, 3 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, e->comp));
   GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
@@ -230,6 +254,8 @@ int end_epoch(gwg_engine* e, gwg_status* st) {
     const auto& tm = e->timings[k];
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, tm.ev[0], tm.ev[1]) == cudaSuccess) e->counters.rotate_ms += ms;
+    if (tm.joined && cudaEventElapsedTime(&ms, tm.ev[7], tm.ev[8]) == cudaSuccess)
+      e->counters.rotate_ms -= ms;  // waiting for the trait side is not rotation
     if (cudaEventElapsedTime(&ms, tm.ev[2], tm.ev[3]) == cudaSuccess) e->counters.grid_kernel_ms += ms;
     if (tm.split) {
       if (cudaEventElapsedTime(&ms, tm.ev[4], tm.ev[5]) == cudaSuccess) e->counters.quad_ms += ms;
@@ -341,7 +367,7 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   // GWG_OPT_I8_CLUSTER = 4: CTA pairs running one cta_group::2 MMA with half
   // of the Z-slice tile each — the default from 16 K stages (n > 1920) on
   // (pair_mma_default)
-  const int cl = e->i8_cluster ? (e->i8_cluster == 3 ? 2 : e->i8_cluster)
+  const int cl = e->i8_cluster ? (e->i8_cluster == 3 || e->i8_cluster == 5 ? 2 : e->i8_cluster)
                                : pair_mma_default(kp) ? 4 : 2;
   CUtensorMap tx, tb, tbh;
   if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB,
@@ -388,13 +414,18 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   }
   GWG_CUDA_TRY(e->xi8.ensure(size_t(cols) * kp));
   {
-    const int blocks = int(std::min<int64_t>(cols, int64_t(e->sms) * 16));
+    // a few blocks per SM (snp_to_i8_kernel): HBM-bound, leaves room for
+    // the trait side running concurrently
+    const int64_t items = cols * (kp / 2);
+    const int blocks = int(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(items, 256 * SNP_I8_ITEMS), int64_t(e->sms) * SNP_I8_BLOCKS)));
     gwg::snp_to_i8_kernel<<<blocks, 256, 0, e->comp>>>(
         src, lds, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
         static_cast<unsigned long long*>(e->err.ptr) + 2);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
   }
+  if (int rc = split_build_ahead(e, st)) return rc;
   // the split grid needs only X'.X' (its linear terms come from the codes)
   if (autom) e->gate_want = 1;
   int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
@@ -451,6 +482,7 @@ int rotate_snps_i8(gwg_engine* e, const int8_t* src, int64_t cols, gwg_status* s
       static_cast<unsigned long long*>(e->err.ptr) + 2);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
+  if (int rc = split_build_ahead(e, st)) return rc;
   if (int rc = launch_i8(e, e->xi8.ptr, e->zslices.ptr, cols, n, e->zscale.d(),
                          e->split ? nullptr : e->rot.d(), e->rot_sq.d(), e->np, st))
     return rc;
@@ -698,9 +730,22 @@ int build_split(gwg_engine* e, gwg_status* st) {
     gwg::expsum_e_kernel<<<int(rc_cols), 256, 0, e->comp>>>(x);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
-    // U[k][(c, q)] = sum_l Z[k][l] x_c[l] E[l][q]  (A = Z^T's columns = Z's rows)
+    // U[k][(c, q)] = sum_l Z[k][l] x_c[l] E[l][q]  (A = Z^T's columns = Z's rows):
+    // n x r(p-1) outputs over K = n — a few dozen tiles, so K is split until
+    // the tiles fill the SMs (partials summed in a fixed order)
+    int ksplit = 1;
+    {
+      const int64_t kchunks = np / e->sops.bk;
+      const int64_t units = ceil_div(n, e->sops.bm) * ceil_div(rc_cols, e->sops.bt);
+      while (ksplit < 16 && kchunks % (2 * ksplit) == 0 && kchunks / (2 * ksplit) >= 4 &&
+             ceil_div(units * 2 * ksplit, 2) <= e->sms)
+        ksplit *= 2;
+    }
+    if (ksplit > 1)
+      GWG_CUDA_TRY(e->upart.ensure(size_t(ksplit) * n * rc_cols * sizeof(double)));
     if (int rc = sbr_gemm(e, e->basis_t.d(), n, np, n, e->xepanel.d(), np, rc_cols,
-                          e->umat.d(), rc_cols, true, st))
+                          e->umat.d(), rc_cols, true, st, ksplit,
+                          ksplit > 1 ? e->upart.d() : nullptr, n * rc_cols))
       return rc;
     for (int64_t c = 0; c + 1 < p; ++c)  // W[(j p8 + c) np + k] = sum_q U[k][(c, q)] F[q][j]
       if (int rc = sbr_gemm(e, e->umat.d() + c * r, r, rc_cols, n, e->fpanel.d(), r, t,
@@ -755,7 +800,8 @@ int build_split(gwg_engine* e, gwg_status* st) {
 // the launches around it (gate_want).
 int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
              const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
-             bool rowmajor, gwg_status* st) {
+             bool rowmajor, gwg_status* st, int ksplit, double* partials,
+             int64_t split_stride) {
   const gwg::SbrOps& so = e->sops;
   CUtensorMap map;
   if (int rc = encode_kmajor(&map, a_op, kext, rows, lda, so.bm, st)) return rc;
@@ -772,9 +818,21 @@ int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64
   q.rowmajor = rowmajor ? 1 : 0;
   q.gate = gate_word(e);
   q.gate_codes = e->gate_want;
-  const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t, 2);
+  if (ksplit > 1) {  // partial products into `partials`, summed into dst below
+    q.ksplit = ksplit;
+    q.sbr = partials;
+    q.split_stride = split_stride;
+  }
+  const int64_t supers = ceil_div(int64_t(q.tiles_m) * q.tiles_t * q.ksplit, 2);
   GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
   e->counters.kernel_launches += 1;
+  if (ksplit > 1) {  // dense dst (ldd = cols, rowmajor) = the partials in order
+    gwg::sum_partials_kernel<<<int(std::min<int64_t>(ceil_div(split_stride, 256), 4 * e->sms)),
+                               256, 0, e->comp>>>(partials, split_stride, ksplit, split_stride,
+                                                  dst);
+    GWG_CUDA_TRY(cudaGetLastError());
+    e->counters.kernel_launches += 1;
+  }
   return GWG_OK;
 }
 
@@ -814,8 +872,44 @@ int mark_trait_fork(gwg_engine* e, bool rotated_input, gwg_status* st) {
   if (!e->split || e->split_valid || rotated_input || e->snp_coding == GWG_SNP_REAL ||
       e->n >= kMaxGenotypeN || e->t <= 0 || pair_mma_default(round_up(e->n, gwg::I8Cfg::BK)))
     return GWG_OK;
-  GWG_CUDA_TRY(cudaEventRecord(e->ev_fork, e->comp));
+  // traits still queued on the side stream: the build follows them there
+  if (!e->side_pending) GWG_CUDA_TRY(cudaEventRecord(e->ev_fork, e->comp));
   e->fork_pending = true;
+  return GWG_OK;
+}
+
+// Before the persistent SNP rotation takes every SM: queue the split grid's
+// trait-side build (W, its slices, E/F) on the side stream — behind the
+// trait work gwg_set_traits left there, or from the fork point — and join.
+// The trait side then overlaps the slab's upload and HBM-bound code
+// conversion instead of queueing behind the rotation (its small kernels find
+// no free SM while the rotation runs).  The build is ungated: the operands
+// belong to the traits, not to this slab, so a first slab that takes the FP64
+// path under GWG_SNP_AUTO cannot leave a stale W marked valid.
+int split_build_ahead(gwg_engine* e, gwg_status* st) {
+  if (e->fork_pending && !e->split_valid) {
+    e->fork_pending = false;
+    if (!e->side_pending) GWG_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+    const int saved_gate = e->gate_want;
+    e->gate_want = -1;
+    std::swap(e->comp, e->side);
+    const int rc = build_split(e, st);
+    std::swap(e->comp, e->side);
+    e->gate_want = saved_gate;
+    e->side_pending = true;  // joined below even when the build failed part-way
+    if (rc) {
+      join_side(e);
+      return rc;
+    }
+  }
+  if (e->side_pending && e->join_ev) {
+    GWG_CUDA_TRY(cudaEventRecord(e->join_ev[0], e->comp));
+    GWG_CUDA_TRY(join_side(e));
+    GWG_CUDA_TRY(cudaEventRecord(e->join_ev[1], e->comp));
+    *e->join_timed = true;
+    return GWG_OK;
+  }
+  GWG_CUDA_TRY(join_side(e));
   return GWG_OK;
 }
 
@@ -825,23 +919,16 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     // The trait-derived operands (W, its slices, E/F) belong to the traits,
     // not to this slab: they are built ungated, so a first slab that takes the
     // FP64 path under GWG_SNP_AUTO cannot leave a stale W marked valid.
-    const int saved_gate = e->gate_want;
-    e->gate_want = -1;
     int rc;
     if (e->fork_pending && !e->split_valid) {  // on the side stream from the fork point
-      e->fork_pending = false;
-      GWG_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
-      std::swap(e->comp, e->side);
-      rc = build_split(e, st);
-      std::swap(e->comp, e->side);
-      if (rc == GWG_OK) {
-        GWG_CUDA_TRY(cudaEventRecord(e->ev_join, e->side));
-        GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_join, 0));
-      }
+      rc = split_build_ahead(e, st);
     } else {
+      GWG_CUDA_TRY(join_side(e));
+      const int saved_gate = e->gate_want;
+      e->gate_want = -1;
       rc = build_split(e, st);
+      e->gate_want = saved_gate;
     }
-    e->gate_want = saved_gate;
     if (rc) return rc;
   }
   using gwg::I8Cfg;
@@ -876,13 +963,31 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   // stream layout ((j*ldo + i)*p, out_si = 1) by TMA boxes {32p, cells} when
   // the trait pitch is 16-byte aligned
   const bool aligned = (reinterpret_cast<uintptr_t>(dev_out) & 15) == 0;
-  const int use_tma = (out_sj == 1 && (out_si * p) % 2 == 0 && aligned) ? 1
+  const bool aligned32 = (reinterpret_cast<uintptr_t>(dev_out) & 31) == 0;
+  // no staging tiles (p % 4 == 0): 256-bit stores in either layout, scalar
+  // stores for a base that is not 32-byte aligned; tout is the S_BR map
+  const bool nostage = e->lops.nostage;
+  const int use_tma = nostage ? (aligned32 ? 3 : 0)
+                      : (out_sj == 1 && (out_si * p) % 2 == 0 && aligned) ? 1
+                      : (out_si == 1 && LIN_STREAM_STG && e->lops.stream_stg && aligned32 &&
+                         (out_sj * p) % 4 == 0) ? 3
                       : (out_si == 1 && e->lops.stream_tma && (out_sj * p) % 2 == 0 && aligned &&
                          LIN_STREAM_TMA) ? 2 : 0;
   {
     auto encode = get_encode();
     CUresult r;
-    if (use_tma == 2) {
+    if (e->lops.sbr_tma) {
+      // S_BR [trait][SNP] (ld ld_s, even): one {BM SNPs, KT traits} box per tile
+      const cuuint64_t gdim[2] = {cuuint64_t(rows), cuuint64_t(t)};
+      const cuuint64_t gstride[1] = {cuuint64_t(ld_s * 8)};
+      const cuuint32_t box[2] = {cuuint32_t(I8Cfg::BM), cuuint32_t(e->lops.kt)};
+      const cuuint32_t es[2] = {1, 1};
+      r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, e->sbr.d(), gdim, gstride, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return set_status(st, GWG_CUDA, -1, -1, "tensor map (S_BR) failed (%d)", int(r));
+    } else if (use_tma == 2) {
       const cuuint64_t gdim[2] = {cuuint64_t(rows * p), cuuint64_t(t)};
       const cuuint64_t gstride[1] = {cuuint64_t(out_sj * p * 8)};
       const cuuint32_t box[2] = {cuuint32_t(32 * p), cuuint32_t(e->lops.cells)};
@@ -902,7 +1007,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
                  tma_row ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-    if (use_tma && r != CUDA_SUCCESS)
+    if ((use_tma == 1 || use_tma == 2) && r != CUDA_SUCCESS)
       return set_status(st, GWG_CUDA, -1, -1, "tensor map (results) failed (%d)", int(r));
   }
   gwg::LinArgs a;
@@ -941,6 +1046,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
 int launch_slab(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,
                 int64_t m_total, double* dev_out, int64_t out_si, int64_t out_sj,
                 gwg_status* st) {
+  GWG_CUDA_TRY(join_side(e));  // the grid reads the trait operands
   const uint64_t cells = uint64_t(rows) * uint64_t(e->t);
   e->counters.grid_flops += cells * 2ull * uint64_t(e->n) * uint64_t(e->p + 1);
   e->counters.loop_flops += cells * uint64_t(e->n) * (5 + 2 * uint64_t(e->p - 1));
@@ -1117,7 +1223,7 @@ int set_covariates_impl(gwg_engine* e, const double* xl, int64_t ldx, int where,
 // Traits: Y (raw or rotated, leading dimension ldy, on y_where) and h2/sigma2
 // (on s_where).  Nothing here waits for the device: the weight-floor verdict
 // stays in error word 0 until the next synchronising call reads it.
-int set_traits_impl(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int y_where,
+int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int y_where,
                     const double* h2, const double* sigma2, int s_where, bool rotated,
                     gwg_status* st) {
   if (!e->have_covariates)
@@ -1202,6 +1308,32 @@ int set_traits_impl(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
   return GWG_OK;
 }
 
+// gwg_set_traits: on the split path (genotype / auto coding at the sizes
+// that fork the split build, mark_trait_fork) the trait work — uploads, the
+// Y rotation, the exponential sum's range, the contexts — is queued on the
+// side stream from this point of the compute stream, so it overlaps the next
+// slab's upload and code conversion; whatever reads it joins first
+// (join_side).  Elsewhere it runs on the compute stream.
+int set_traits_impl(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int y_where,
+                    const double* h2, const double* sigma2, int s_where, bool rotated,
+                    gwg_status* st) {
+  const bool on_side = GWG_TRAITS_ON_SIDE && e->split && e->snp_coding != GWG_SNP_REAL &&
+                       e->n < kMaxGenotypeN && !pair_mma_default(round_up(e->n, gwg::I8Cfg::BK));
+  if (!on_side) {
+    GWG_CUDA_TRY(join_side(e));
+    return set_traits_body(e, t, y, ldy, y_where, h2, sigma2, s_where, rotated, st);
+  }
+  if (!e->side_pending) {  // the side stream starts from here
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_fork, e->comp));
+    GWG_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+  }
+  e->side_pending = true;
+  std::swap(e->comp, e->side);
+  const int rc = set_traits_body(e, t, y, ldy, y_where, h2, sigma2, s_where, rotated, st);
+  std::swap(e->comp, e->side);
+  return rc;
+}
+
 }  // namespace gwg_host
 
 using namespace gwg_host;
@@ -1270,8 +1402,16 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
     return bail("stream", err);
   if ((err = cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking)) != cudaSuccess)
     return bail("stream", err);
-  if ((err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking)) != cudaSuccess)
-    return bail("stream", err);
+  {
+    // the side stream (trait-side split build) at the highest priority: its
+    // small kernels take SMs as the HBM-bound SNP conversion's blocks drain,
+    // instead of queueing behind it and the persistent rotation
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if ((err = cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking,
+                                            GWG_SIDE_PRIORITY ? greatest : least)) != cudaSuccess)
+      return bail("stream", err);
+  }
   cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming);
   for (int b = 0; b < 2; ++b) {
@@ -1309,7 +1449,7 @@ void gwg_engine_destroy(gwg_engine* e) {
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
                     &e->wslices, &e->wscale, &e->dpanel, &e->sbr, &e->epanel, &e->fpanel,
-                    &e->gmat, &e->exps, &e->xepanel, &e->umat, &e->raw8[0], &e->raw8[1], &e->csum})
+                    &e->gmat, &e->exps, &e->xepanel, &e->umat, &e->upart, &e->raw8[0], &e->raw8[1], &e->csum})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   if (e->range_host) cudaFreeHost(e->range_host);
@@ -1373,7 +1513,7 @@ int32_t gwg_set_traits(gwg_engine* e, int64_t t, const double* y, const double* 
                        const double* sigma2, int32_t where, int32_t is_rotated, gwg_status* st) {
   NvtxRange nvtx_("gwg_set_traits");
   clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
+  if (int rc = check_engine(e, st, false)) return rc;
   return set_traits_impl(e, t, y, e->n, where, h2, sigma2, where, is_rotated != 0, st);
 }
 
@@ -1382,7 +1522,7 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
                            int32_t layout, int64_t ldo, gwg_status* st) {
   NvtxRange nvtx_("gwg_solve_snp_slab");
   clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
+  if (int rc = check_engine(e, st, false)) return rc;
   if (!e->have_traits)
     return set_status(st, GWG_DIMENSION, -1, -1, "gwg_set_traits must come first");
   if (mb < 1 || i0 < 0 || !x_r || !b_out)
@@ -1410,6 +1550,13 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     e->timings.push_back(tm);
   }
   gwg_engine::SlabTiming& tmg = e->timings[e->timings_used++];
+  tmg.joined = false;
+  e->join_ev = tmg.ev + 7;
+  e->join_timed = &tmg.joined;
+  struct JoinEvReset {  // never left pointing into `timings` past this call
+    gwg_engine* e;
+    ~JoinEvReset() { e->join_ev = nullptr, e->join_timed = nullptr; }
+  } join_ev_reset{e};
   if (int rc = mark_trait_fork(e, is_rotated, st)) return rc;
   GWG_CUDA_TRY(cudaEventRecord(tmg.ev[0], e->comp));
   if (is_rotated) {
@@ -1427,6 +1574,8 @@ int32_t gwg_solve_snp_slab(gwg_engine* e, int64_t i0, int64_t mb, const double* 
     if (int rc = rotate_snps(e, src, raw_ld(e), mb, st)) return rc;
   }
   GWG_CUDA_TRY(cudaEventRecord(tmg.ev[1], e->comp));
+  e->join_ev = nullptr;
+  e->join_timed = nullptr;
   double* dev_out = b_out;
   if (out_where != GWG_DEVICE) {
     GWG_CUDA_TRY(e->out[0].ensure(size_t(mb) * t * p * sizeof(double)));
@@ -1495,8 +1644,8 @@ int32_t gwg_set_option(gwg_engine* e, int32_t option, int64_t value, gwg_status*
     case GWG_OPT_REAL_SPLIT:
       return flag(e->real_split);
     case GWG_OPT_I8_CLUSTER:
-      if (value < 0 || value > 4)
-        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_I8_CLUSTER takes 0..4 (got %lld)",
+      if (value < 0 || value > 5)
+        return set_status(st, GWG_DIMENSION, -1, -1, "GWG_OPT_I8_CLUSTER takes 0..5 (got %lld)",
                           (long long)value);
       e->i8_cluster = int(value);
       return GWG_OK;

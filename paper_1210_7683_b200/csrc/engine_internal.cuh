@@ -98,6 +98,12 @@ struct gwg_engine {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool fork_pending = false;
+  // trait-side device work queued on the side stream and not yet joined into
+  // the compute stream (gwg_set_traits on the split path, then the split
+  // build): join_side before anything on comp reads it
+  bool side_pending = false;
+  cudaEvent_t* join_ev = nullptr;  // the current slab's ev[7] (solve_snp_slab)
+  bool* join_timed = nullptr;
 
   gwg_host::DevBuf basis, lambda, xl_raw, xl_rot;  // basis / xl_* / y_* / rot: leading dimension np
   bool have_spectrum = false, have_covariates = false;
@@ -153,7 +159,7 @@ struct gwg_engine {
   // D column (GWG_OPT_REAL_SPLIT = 0 keeps the fused S_BR)
   bool real_split = true;
   gwg_host::DevBuf epanel, fpanel, gmat, exps;
-  gwg_host::DevBuf xepanel, umat;  // W build through the factorisation: diag(X_L'_c) E, Z diag(X_L'_c) E
+  gwg_host::DevBuf xepanel, umat, upart;  // upart: split-K partials of U  // W build through the factorisation: diag(X_L'_c) E, Z diag(X_L'_c) E
   // host copies of lambda / h2 / sigma2 when they were passed from the host:
   // the factorisation's range is then found without a device round trip
   std::vector<double> h2_host, s2_host;
@@ -189,8 +195,12 @@ struct gwg_engine {
   // when the epoch closes: [rotate begin, rotate end, grid begin, grid end,
   // sbr begin, linear begin, linear end]
   struct SlabTiming {
-    cudaEvent_t ev[7] = {};
+    // 0/1 around the SNP upload + rotation, 2/3 around the grid, 4/5/6 the
+    // split grid's stages, 7/8 around the rotation's wait for the trait side
+    // (split_build_ahead; not counted as rotation time)
+    cudaEvent_t ev[9] = {};
     bool split = false;
+    bool joined = false;
   };
   std::vector<SlabTiming> timings;
   size_t timings_used = 0;
@@ -203,7 +213,11 @@ struct gwg_engine {
 
 namespace gwg_host {
 
-int check_engine(gwg_engine* e, gwg_status* st);
+// join = false (gwg_set_traits, gwg_solve_snp_slab): trait-side work queued
+// on the side stream stays there; every other entry point joins it first
+int check_engine(gwg_engine* e, gwg_status* st, bool join = true);
+cudaError_t join_side(gwg_engine* e);
+int split_build_ahead(gwg_engine* e, gwg_status* st);
 int upload(gwg_engine* e, DevBuf& dst, const double* src, size_t count, int where,
            gwg_status* st);
 int upload_cols(gwg_engine* e, DevBuf& dst, const double* src, int64_t lds, int64_t cols,
@@ -226,7 +240,8 @@ inline const unsigned long long* gate_word(const gwg_engine* e) {
 int prepare_expsum(gwg_engine* e, gwg_status* st);
 int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
              const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
-             bool rowmajor, gwg_status* st);
+             bool rowmajor, gwg_status* st, int ksplit = 1, double* partials = nullptr,
+             int64_t split_stride = 0);
 int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
                      gwg_status* st);
 int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,

@@ -72,6 +72,11 @@ struct SbrArgs {
   int32_t kchunks;
   int64_t np;        // K extent of one D panel (its stride between trait tiles)
   int32_t rowmajor;  // 1: store out[i * ld + j] instead (j < t, t a multiple of BT)
+  // split K: every output tile is computed as ksplit partial products over
+  // kchunks / ksplit consecutive k-chunks each, partial s stored at
+  // sbr + s * split_stride (summed in a fixed order by sum_partials_kernel)
+  int32_t ksplit = 1;
+  int64_t split_stride = 0;
   const unsigned long long* gate = nullptr;  // GWG_SNP_AUTO path gate (gate_closed)
   int32_t gate_codes = 0;
 };
@@ -85,9 +90,11 @@ __device__ __forceinline__ void sbr_issue(const CUtensorMap* tmap_q, const SbrAr
   const int s = g % Cfg::STAGES;
   const int use = g / Cfg::STAGES;
   if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-  const int local_tile = g / args.kchunks;
-  const int kc = g - local_tile * args.kchunks;
-  const int tile = (blockIdx.x + local_tile * gridDim.x) * Cfg::GROUPS + group;
+  const int kc_per = args.kchunks / args.ksplit;
+  const int local_tile = g / kc_per;
+  const int vt = (blockIdx.x + local_tile * gridDim.x) * Cfg::GROUPS + group;
+  const int tile = vt / args.ksplit;
+  const int kc = (g - local_tile * kc_per) + (vt - tile * args.ksplit) * kc_per;
   const int tm = tile / args.tiles_t;
   const int tt = tile - tm * args.tiles_t;
   mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
@@ -125,12 +132,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* go = bars + G * 2 * Cfg::STAGES;
 
-  const int ntiles = args.tiles_m * args.tiles_t;
+  const int ntiles = args.tiles_m * args.tiles_t * args.ksplit;  // (tile, k-split) units
+  const int kc_per = args.kchunks / args.ksplit;
   const int nsuper = (ntiles + G - 1) / G;
   const int my_super = blockIdx.x < nsuper ? (nsuper - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   int my_tiles = my_super;
   if (my_super > 0 && (blockIdx.x + (my_super - 1) * gridDim.x) * G + group >= ntiles) --my_tiles;
-  const int total_iters = my_tiles * args.kchunks;
+  const int total_iters = my_tiles * kc_per;
 
   if (threadIdx.x == 0) {
     for (int q = 0; q < G * 2 * Cfg::STAGES; q += 2 * Cfg::STAGES)
@@ -154,12 +162,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 
   const int wm = lw % Cfg::WARPS_M;
   const int wt = lw / Cfg::WARPS_M;
-  const int half = args.kchunks / 2;
+  const int half = kc_per / 2;
   if (group > 0 && my_tiles > 0) mbar_wait(go, 0);  // start half a tile late
   if (group == 0 && lw == 0 && lane == 0 && my_tiles == 0) mbar_arrive(go);
   int g = 0;
   for (int lt = 0; lt < my_tiles; ++lt) {
-    const int tile = (blockIdx.x + lt * gridDim.x) * G + group;
+    const int vt = (blockIdx.x + lt * gridDim.x) * G + group;
+    const int tile = vt / args.ksplit;
+    double* const out = args.sbr + int64_t(vt - tile * args.ksplit) * args.split_stride;
     const int tm = tile / args.tiles_t;
     const int tt = tile - tm * args.tiles_t;
 
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
       for (int w = 0; w < TW; ++w) acc[o][w][0] = acc[o][w][1] = 0.0;
 
-    for (int kc = 0; kc < args.kchunks; ++kc, ++g) {
+    for (int kc = 0; kc < kc_per; ++kc, ++g) {
       if (group == 0 && lt == 0 && kc == half && lw == 0 && lane == 0) mbar_arrive(go);
       const int s = g % Cfg::STAGES;
       mbar_wait(&full[s], (g / Cfg::STAGES) & 1);
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int o = 0; o < WO; ++o) {
           const int64_t il = int64_t(tm) * Cfg::BM + (wm * WO + o) * 8 + (lane >> 2);
           if (il < args.rows)
-            *reinterpret_cast<double2*>(args.sbr + il * args.ld + j) =
+            *reinterpret_cast<double2*>(out + il * args.ld + j) =
                 make_double2(acc[o][w][0], acc[o][w][1]);
         }
       }
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int e = 0; e < 2; ++e) {
         const int j = tt * Cfg::BT + (wt * TW + w) * 8 + 2 * (lane & 3) + e;
         if (j >= args.t) continue;
-        double* col = args.sbr + int64_t(j) * args.ld;
+        double* col = out + int64_t(j) * args.ld;
 #pragma unroll
         for (int o = 0; o < WO; ++o) {
           const int64_t il = int64_t(tm) * Cfg::BM + (wm * WO + o) * 8 + (lane >> 2);
@@ -225,6 +235,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
       }
     }
+  }
+}
+
+// dst[i] = sum_{s < ksplit} part[s * stride + i], s in order (split-K GEMMs).
+static __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t stride, int ksplit,
+                                    int64_t count, double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double v = part[i];
+    for (int s = 1; s < ksplit; ++s) v += part[s * stride + i];
+    dst[i] = v;
   }
 }
 

@@ -43,6 +43,7 @@ int group_ok(gwg_group* g, gwg_status* st) {
 int publish_from_first(gwg_group* g, gwg_status* st) {
   gwg_engine* e0 = g->engines[0];
   GWG_CUDA_TRY(cudaSetDevice(e0->device));
+  GWG_CUDA_TRY(join_side(e0));  // e0's trait work may still be on its side stream
   GWG_CUDA_TRY(cudaEventRecord(g->ready, e0->comp));
   for (size_t k = 1; k < g->engines.size(); ++k) {
     GWG_CUDA_TRY(cudaSetDevice(g->engines[k]->device));

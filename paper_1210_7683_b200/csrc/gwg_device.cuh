@@ -102,6 +102,15 @@ __device__ __forceinline__ void st_evict_first(double* p, double v, uint64_t pol
                : "memory");
 }
 
+// Four consecutive doubles in one 256-bit store (STG.E.ENL2.256; 32-byte
+// aligned address) with an L2 cache policy.
+__device__ __forceinline__ void st4_policy(double* p, double a, double b, double c, double d,
+                                           uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a),
+               "d"(b), "d"(c), "d"(d), "l"(pol)
+               : "memory");
+}
+
 // FP64 tensor-core MMA, 8x8x4 (SASS DMMA.8x8x4): C[8x8] += A[8x4] B[4x8].
 // Fragment ownership (lane l): a = A[l>>2][l&3], b = B[l&3][l>>2],
 // c = C[l>>2][2(l&3) + {0,1}].

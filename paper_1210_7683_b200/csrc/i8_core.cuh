@@ -44,8 +44,17 @@ struct I8Tile {
   // same SNP tile instead, and each CTA loads half of the A tile (64 SNP
   // rows) and multicasts it — for one or two traits per tile (p >= 9), where
   // the SNP tile is re-read once per trait tile and dominates L2 traffic.
+  // PAIR_AXIS = 2 (CLUSTER = 4): 2 x 2 clusters — SNP tiles 2u, 2u+1 x B
+  // tiles 2v, 2v+1 (rank = SNP bit | B bit << 1).  Each CTA loads half of
+  // its A tile (64 SNP rows) multicast to the CTA of the other B tile, and
+  // half of its B tile (4 of the 8 slots) multicast to the CTA of the other
+  // SNP tile: 8 + 16 KB issued per CTA and stage instead of 16 + 16 (B pairs)
+  // or 16 + 32 (single CTAs), for the same 48 KB landing in each CTA.
   static constexpr int PAIR_AXIS = PAIR_AXIS_;
-  static_assert(PAIR_AXIS == 0 || CLUSTER == 2, "trait pairs need a CTA pair");
+  static_assert(PAIR_AXIS == 0 || (PAIR_AXIS == 1 && CLUSTER == 2) ||
+                    (PAIR_AXIS == 2 && CLUSTER == 4),
+                "trait pairs need a CTA pair, 2 x 2 clusters four CTAs");
+  static_assert(CLUSTER <= 2 || PAIR_AXIS == 2, "clusters of four are 2 x 2");
   // MMA2 (CLUSTER = 2, SNP-tile pairs): the pair runs ONE
   // tcgen05.mma.cta_group::2 of M = 256 issued by the even CTA.  Each CTA
   // keeps its own A tile and HALF of the B tile — 112 of the 224 slice rows
@@ -74,8 +83,9 @@ struct I8Tile {
   static constexpr int OUT_BUFS = OUT_BUFS_;     // staging tiles per epilogue warp
   static constexpr uint32_t A_BYTES = BM * BK;  // 16 KB
   static constexpr uint32_t B_BYTES = SLOTS * RB * BK;  // <= 32 KB of smem (slots)
-  static constexpr int B_SLICES_PER_CTA = PAIR_AXIS ? SLOTS : SLOTS / CLUSTER;
-  static constexpr uint32_t B_PART = PAIR_AXIS ? B_BYTES : B_BYTES / CLUSTER;  // loaded per CTA
+  static constexpr int B_SLICES_PER_CTA = PAIR_AXIS == 1 ? SLOTS : PAIR_AXIS == 2 ? SLOTS / 2
+                                                                     : SLOTS / CLUSTER;
+  static constexpr uint32_t B_PART = B_BYTES / SLOTS * B_SLICES_PER_CTA;  // loaded per CTA
   static constexpr uint32_t B_SMEM = MMA2 ? SLICES * RB * BK / 2 : B_BYTES;  // B held per CTA
   static_assert(!MMA2 || (CLUSTER == 2 && PAIR_AXIS == 0 && RB == 32),
                 "pair MMA: SNP-tile pairs on 32-row B tiles (112 rows = 14 swizzle atoms per CTA)");
@@ -676,8 +686,9 @@ struct I8Sched {
     rank = C::CLUSTER > 1 ? int(blockIdx.x % C::CLUSTER) : 0;
     unit = int(blockIdx.x / C::CLUSTER);
     units = int(gridDim.x / C::CLUSTER);
-    // unit grid: (SNP-tile pairs x B tiles), or (SNP tiles x B-tile pairs)
-    tm_units = C::PAIR_AXIS ? tiles_m : (tiles_m + C::CLUSTER - 1) / C::CLUSTER;
+    // unit grid: (SNP-tile pairs x B tiles), (SNP tiles x B-tile pairs) or,
+    // for 2 x 2 clusters, (SNP-tile pairs x B-tile pairs)
+    tm_units = C::PAIR_AXIS == 1 ? tiles_m : (tiles_m + 1) / (C::CLUSTER > 1 ? 2 : 1);
     tr_units = C::PAIR_AXIS ? (tiles_r + 1) / 2 : tiles_r;
     const int ntiles = tm_units * tr_units;
     my_tiles = unit < ntiles ? (ntiles - 1 - unit) / units + 1 : 0;
@@ -692,8 +703,13 @@ struct I8Sched {
     } else {
       i8_tile_coords(unit + lt * units, tm_units, tr_units, tu, ru);
     }
-    tm = C::PAIR_AXIS ? tu : tu * C::CLUSTER + rank;
-    tr = C::PAIR_AXIS ? ru * 2 + rank : ru;
+    if constexpr (C::PAIR_AXIS == 2) {
+      tm = tu * 2 + (rank & 1);
+      tr = ru * 2 + (rank >> 1);
+    } else {
+      tm = C::PAIR_AXIS ? tu : tu * C::CLUSTER + rank;
+      tr = C::PAIR_AXIS ? ru * 2 + rank : ru;
+    }
   }
 };
 
@@ -772,6 +788,20 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
         }
       }
       mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], C::STAGE_BYTES);
+      if constexpr (C::PAIR_AXIS == 2) {
+        // 2 x 2: A rows [rb * 64, +64) to both CTAs of this SNP tile (ranks
+        // sb, sb + 2), B slots [sb * 4, +4) to both CTAs of this B tile
+        // (ranks 2 rb, 2 rb + 1); partial tiles past either edge still load
+        // (zero-filled) boxes so every barrier completes
+        const int sb = sch.rank & 1, rb = sch.rank >> 1;
+        tma_load_2d_mc_w<C::WS>(st + rb * (C::A_BYTES / 2), tmap_x, ks * C::BK,
+                                tm * C::BM + rb * (C::BM / 2), &sm.full[s],
+                                uint16_t((1u << sb) | (1u << (sb + 2))), pol_x);
+        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sb * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
+                                sb * C::B_SLICES_PER_CTA, &sm.full[s], uint16_t(3u << (2 * rb)),
+                                pol_b);
+        continue;
+      }
       if constexpr (C::PAIR_AXIS == 1) {
         // half of the shared SNP tile each (box 128 k x 64 SNPs), multicast;
         // this CTA's own B tile, all 8 slots
@@ -895,10 +925,8 @@ cudaError_t i8_launch(void (*kern)(KArgs...), int64_t units, int sms, cudaStream
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(C::SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  const int64_t max_units = sms / C::CLUSTER;
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, max_units))) * C::CLUSTER;
+  int64_t max_units = sms / C::CLUSTER;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = s;
@@ -909,6 +937,24 @@ cudaError_t i8_launch(void (*kern)(KArgs...), int64_t units, int sms, cudaStream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (C::CLUSTER > 2) {
+    // clusters of four need four free SMs in one GPC: launch only as many
+    // as can be co-resident (a persistent static schedule must not leave a
+    // second wave), once per kernel (the answer depends on the device only)
+    static int resident = 0;
+    if (resident == 0) {
+      cfg.gridDim = dim3(unsigned(max_units * C::CLUSTER));
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        (void)cudaGetLastError();
+        n = int(max_units);
+      }
+      resident = n;
+    }
+    max_units = std::min<int64_t>(max_units, resident);
+  }
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, max_units))) * C::CLUSTER;
+  cfg.gridDim = dim3(unsigned(grid));
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -91,6 +91,20 @@ namespace gwg {
 #define LIN_CTX_SMEM 1
 #endif
 
+// p % 4 == 0: results leave by direct 256-bit stores from registers (any
+// layout; no staging tiles), and the shared memory that frees holds each
+// tile's S_BR rows, staged by one TMA box per tile from the context warp, and
+// a fourth operand stage
+#ifndef LIN_NOSTAGE
+#define LIN_NOSTAGE 0  // measured at c1: neutral with S_BR per cell and 3 stages, slower otherwise (off)
+#endif
+#ifndef LIN_SBR_TMA  // NOSTAGE: S_BR staged by TMA (1) or loaded per cell as before (0)
+#define LIN_SBR_TMA 1
+#endif
+#ifndef LIN_NOSTAGE_DEEP  // NOSTAGE: one more operand stage
+#define LIN_NOSTAGE_DEEP 1
+#endif
+
 template <int P, int CL = 1>
 struct LinCfg {
   static constexpr int P8 = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : (P + 7) / 8 * 8;
@@ -122,13 +136,24 @@ struct LinCfg {
   // layout): a warp's results are, per trait, 32 SNPs x p contiguous doubles;
   // staged [cell][lane*p + c] and stored as one TMA box {32p, CELLS}
   static constexpr bool STREAM_TMA = 32 * P <= 256 && CELLS * 32 * P * 8 <= 4096;
+  // stream order by direct 256-bit stores from registers (use_tma = 3): a
+  // lane's p results of a cell are p/4 aligned 32-byte pieces, a warp's cell
+  // 32p contiguous doubles — no staging, no proxy fence, no TMA store
+  static constexpr bool STREAM_STG = P % 4 == 0;
   static constexpr int BW = ROW & ~1;                     // doubles per TMA box row
-  static constexpr int OUT_BUFS = TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
+  static constexpr bool NOSTAGE = LIN_NOSTAGE != 0 && LIN_CTX_SMEM != 0 && P % 4 == 0;
+  static constexpr int OUT_BUFS = NOSTAGE ? 0 : TMA_ROW && BW * 8 * 32 > 4096 ? 2 : 1;
   // CL = 4: CTA pairs running one cta_group::2 MMA, half of B per CTA
   // (I8Tile MMA2; 32-row W tiles only)
   static constexpr bool MMA2 = CL == 4;
   static_assert(!MMA2 || RB == 32, "pair MMA on 32-row W tiles");
-  static constexpr int STAGES_0 = MMA2 ? (WIDE ? 5 : 6) : WIDE ? 3 : 4;
+  static constexpr bool DEEP = NOSTAGE && LIN_NOSTAGE_DEEP;
+  static constexpr bool SBR_TMA = NOSTAGE && LIN_SBR_TMA;
+#ifndef LIN_STAGES  // timing override of the operand stages (0 = the default below)
+#define LIN_STAGES 0
+#endif
+  static constexpr int STAGES_0 = LIN_STAGES > 0 ? LIN_STAGES
+                                  : MMA2 ? (WIDE && !DEEP ? 5 : 6) : WIDE && !DEEP ? 3 : 4;
   static constexpr uint32_t STAGE_B = MMA2 ? 128 * 128 + 7 * RB * 64 : 128 * 128 + 8 * RB * 128;
   // shared-memory context staging, per accumulator buffer: the tile's KT trait
   // contexts (CtxLayout, contiguous in global memory) and RB W-row scales,
@@ -137,7 +162,10 @@ struct LinCfg {
   static constexpr int CTX_DOUBLES = KT * CtxLayout<P>::STRIDE;
   static constexpr uint32_t CTX_BYTES = CTX_DOUBLES * 8;
   static constexpr uint32_t SCALE_OFF = ACC * CTX_BYTES;
-  static constexpr uint32_t BAR_OFF = SCALE_OFF + ACC * RB * 8;
+  // NOSTAGE: per accumulator buffer the tile's S_BR box [KT traits][BM SNPs]
+  static constexpr uint32_t SBR_BYTES = SBR_TMA ? KT * 128 * 8 : 0;
+  static constexpr uint32_t SBR_OFF = (SCALE_OFF + ACC * RB * 8 + 127) / 128 * 128;
+  static constexpr uint32_t BAR_OFF = SBR_OFF + ACC * SBR_BYTES;
   static constexpr uint32_t EXTRA = CTX_SMEM ? BAR_OFF + 2 * ACC * 8 : 0;
   static constexpr size_t FIXED_B = size_t(EPI) * OUT_BUFS * 4096 + (EXTRA + 15) / 16 * 16 + 1280;
   static constexpr int STAGES = size_t(STAGES_0) * STAGE_B + FIXED_B <= 227 * 1024 ? STAGES_0
@@ -145,9 +173,10 @@ struct LinCfg {
                                     ? STAGES_0 - 1
                                     : STAGES_0 - 2;
   // CL = 3: CTA pairs along the trait axis sharing (multicasting) the SNP tile
+  // CL = 5: 2 x 2 clusters multicasting halves of both operands
   // warp-collective issue except for the pair MMA (measured, see i8_core.cuh)
-  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL >= 2 ? 2 : 1, CL == 3 ? 1 : 0, EXTRA, MMA2,
-                      LIN_WS != 0 && !MMA2>;
+  using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 5 ? 4 : CL >= 2 ? 2 : 1,
+                      CL == 3 ? 1 : CL == 5 ? 2 : 0, EXTRA, MMA2, LIN_WS != 0 && !MMA2>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = LIN_GMAX > 0 && P <= 4 ? LIN_GMAX
@@ -215,6 +244,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   const int my_tiles = sch.my_tiles;
   double* const ctx_sm = reinterpret_cast<double*>(sm.extra);
   double* const scale_sm = reinterpret_cast<double*>(sm.extra + L::SCALE_OFF);
+  double* const sbr_sm = reinterpret_cast<double*>(sm.extra + L::SBR_OFF);
   uint64_t* const ctx_full = reinterpret_cast<uint64_t*>(sm.extra + L::BAR_OFF);
   uint64_t* const ctx_empty = ctx_full + L::ACC;
   if (L::CTX_SMEM && threadIdx.x == 0) {  // fenced and published by i8_setup
@@ -253,12 +283,17 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
         // last trait: nothing to copy, the phase still completes
         const int nt = tr < a.tiles_r ? min(L::KT, a.t - j0) : 0;
         const uint32_t cbytes = uint32_t(nt) * CX::STRIDE * 8;
-        mbar_arrive_expect_tx(&ctx_full[buf], nt > 0 ? cbytes + C::RB * 8 : 0);
+        mbar_arrive_expect_tx(&ctx_full[buf], nt > 0 ? cbytes + C::RB * 8 + L::SBR_BYTES : 0);
         if (nt > 0) {
           bulk_load(ctx_sm + buf * L::CTX_DOUBLES, a.ctx + int64_t(j0) * CX::STRIDE, cbytes,
                     &ctx_full[buf], pol);
           bulk_load(scale_sm + buf * C::RB, a.scale + int64_t(tr) * C::RB, C::RB * 8,
                     &ctx_full[buf], pol);
+          // S_BR rows [j0, +KT) x SNPs [tm BM, +BM) (tmap_out is the S_BR map
+          // here; zero-filled past either edge, the full box still counts)
+          if (L::SBR_TMA)
+            tma_load_2d(sbr_sm + buf * (L::SBR_BYTES / 8), &tmap_out, tm * C::BM, j0,
+                        &ctx_full[buf], policy_evict_first());
         }
         if (LIN_SBR_L2PF) {  // this tile's S_BR rows [j][tm*BM, +BM) into L2
           const int64_t i_lo = int64_t(tm) * C::BM;
@@ -315,7 +350,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             sbr[cc] = (iv && j < a.t) ? __ldcs(a.sbr + int64_t(j) * a.ld_s + il) : 0.0;
         }
       };
-      if (!SBR_LATE) load_sbr();
+      if (!SBR_LATE && !L::SBR_TMA) load_sbr();
       // without the staged copy, lane r holds the slice scale (sigma 2^-55) of
       // the tile's W row r (RB <= 32), shuffled to the recombination below
       const double sc_lane = !L::CTX_SMEM && lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
@@ -417,7 +452,8 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
           double cell[P + 1];
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
-          cell[P] = sbr[g0 + u];
+          cell[P] = L::SBR_TMA ? sbr_sm[(buf * L::KT + cell0 + g0 + u) * 128 + qd * 32 + lane]
+                               : sbr[g0 + u];
           const double* cx = L::CTX_SMEM ? cx_tile + (cell0 + g0 + u) * CX::STRIDE
                                          : a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
           if (LIN_EXPERIMENT >= 3) {
@@ -448,6 +484,39 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < P; ++c) acc += beta[u][c];
           if (acc == 1.2345e300) a.out[il] = acc;
+        } else if (L::NOSTAGE) {
+          // any layout: a cell's p doubles are p/4 aligned 32-byte pieces
+          // (use_tma = 3) or, for a base not 32-byte aligned, plain stores
+          if (iv) {
+#pragma unroll
+            for (int u = 0; u < L::GROUP; ++u) {
+              const int j = j0 + cell0 + g0 + u;
+              if (j >= a.t) continue;
+              double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
+              if (a.use_tma == 3) {
+#pragma unroll
+                for (int c = 0; c < P; c += 4)
+                  st4_policy(dst + c, beta[u][c], beta[u][c + 1], beta[u][c + 2], beta[u][c + 3],
+                             pol_out);
+              } else {
+#pragma unroll
+                for (int c = 0; c < P; ++c) st_evict_first(dst + c, beta[u][c], pol_out);
+              }
+            }
+          }
+        } else if (L::STREAM_STG && a.use_tma == 3) {
+          if (iv) {
+#pragma unroll
+            for (int u = 0; u < L::GROUP; ++u) {
+              const int j = j0 + cell0 + g0 + u;
+              if (j >= a.t) continue;
+              double* dst = a.out + (il + int64_t(j) * a.out_sj) * P;
+#pragma unroll
+              for (int c = 0; c < P; c += 4)
+                st4_policy(dst + c, beta[u][c], beta[u][c + 1], beta[u][c + 2], beta[u][c + 3],
+                           pol_out);
+            }
+          }
         } else if (L::STREAM_TMA && a.use_tma == 2) {
           if (g0 == 0) {
             if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
@@ -568,9 +637,10 @@ cudaError_t launch_linear_solve(const CUtensorMap& tx, const CUtensorMap& tw,
                                 const CUtensorMap& tout, const LinArgs& a, int sms,
                                 cudaStream_t s, const CUtensorMap& twh) {
   using C = typename LinCfg<P, CL>::Tile;
-  const int64_t units = C::PAIR_AXIS ? int64_t(a.tiles_m) * ((a.tiles_r + 1) / 2)
-                                     : int64_t((a.tiles_m + C::CLUSTER - 1) / C::CLUSTER) *
-                                           a.tiles_r;
+  const int64_t units = C::PAIR_AXIS == 2 ? int64_t((a.tiles_m + 1) / 2) * ((a.tiles_r + 1) / 2)
+                       : C::PAIR_AXIS ? int64_t(a.tiles_m) * ((a.tiles_r + 1) / 2)
+                                      : int64_t((a.tiles_m + C::CLUSTER - 1) / C::CLUSTER) *
+                                            a.tiles_r;
   return i8_launch<C>(linear_solve_kernel<P, CL>, units, sms, s, tx, tw, tout, a, twh);
 }
 
@@ -580,15 +650,19 @@ struct LinOps {
   // [0]: one CTA per tile; [1]: CTA pairs sharing (multicasting) the B tile;
   // [2]: CTA pairs on two B tiles sharing (multicasting) the SNP tile;
   // [3]: CTA pairs running one cta_group::2 MMA (32-row W tiles; else null)
-  cudaError_t (*launch[4])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+  // [4]: 2 x 2 clusters multicasting halves of both operands
+  cudaError_t (*launch[5])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                            const LinArgs&, int, cudaStream_t, const CUtensorMap&) = {
-      nullptr, nullptr, nullptr, nullptr};
-  int b_slices_box[4] = {8, 4, 8, 3};  // slice slots per TMA box (pair MMA: + a half-slot box)
-  int a_box_rows[4] = {128, 128, 64, 128};  // SNP rows per TMA box of the A tile
+      nullptr, nullptr, nullptr, nullptr, nullptr};
+  int b_slices_box[5] = {8, 4, 8, 3, 4};  // slice slots per TMA box (pair MMA: + a half-slot box)
+  int a_box_rows[5] = {128, 128, 64, 128, 64};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
   int cells = 0;         // traits per epilogue warp and tile (LinCfg::CELLS)
   bool stream_tma = false;  // stream-layout results by TMA boxes {32p, cells}
   bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
+  bool stream_stg = false;  // stream-layout results by direct 256-bit stores
+  bool nostage = false;  // direct stores in any layout
+  bool sbr_tma = false;  // tmap_out = the S_BR map
 };
 
 template <int P>
@@ -601,10 +675,14 @@ LinOps make_lin_ops() {
   o.launch[1] = &launch_linear_solve<P, 2>;
   o.launch[2] = &launch_linear_solve<P, 3>;
   if constexpr (LinCfg<P>::RB == 32) o.launch[3] = &launch_linear_solve<P, 4>;
+  o.launch[4] = &launch_linear_solve<P, 5>;
   o.row = LinCfg<P>::BW;
   o.cells = LinCfg<P>::CELLS;
   o.stream_tma = LinCfg<P>::STREAM_TMA;
   o.tma_row = LinCfg<P>::TMA_ROW;
+  o.stream_stg = LinCfg<P>::STREAM_STG;
+  o.nostage = LinCfg<P>::NOSTAGE;
+  o.sbr_tma = LinCfg<P>::SBR_TMA;
   return o;
 }
 

@@ -404,7 +404,8 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const void* x_r_host, double* b_h
 
 int32_t gwg_wait_stream(gwg_engine* e, void* stream, gwg_status* st) {
   clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
+  // no join: the trait side forks from the compute stream after this wait
+  if (int rc = check_engine(e, st, false)) return rc;
   if (!e->ev_wait) GWG_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_wait, cudaEventDisableTiming));
   GWG_CUDA_TRY(cudaEventRecord(e->ev_wait, static_cast<cudaStream_t>(stream)));
   GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_wait, 0));

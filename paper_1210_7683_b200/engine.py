@@ -614,7 +614,8 @@ def device_working_set_bytes(n: int, p: int, t: int, mb: int, snp_coding: str = 
         if t < 256:
             total += lowrank + mb * r * 8                     # E, F, G
         elif p > 1:                                           # factorised covariate columns
-            total += (np_ + n) * r * (p - 1) * 8
+            total += (np_ + n) * r * (p - 1) * 8              # (+ up to 16 split-K partials of U)
+            total += 16 * n * r * (p - 1) * 8
     return total
 
 

@@ -222,17 +222,17 @@ def test_int8_kernel_variants_bitwise_identical(n, p, m, t):
     """Every int8 launch geometry (GWG_OPT_I8_CLUSTER: 1 single CTAs, 2 CTA pairs
     on two SNP tiles multicasting B, 3 CTA pairs on two W tiles multicasting
     the SNP tile, 4 CTA pairs running one cta_group::2 MMA with half of the
-    slice tile each) gives the same bits: the int32 slice products are exact
-    and the recombination order fixed."""
+    slice tile each, 5 2 x 2 clusters multicasting halves of both operands,
+    odd tile counts on both axes included) gives the same bits: the int32
+    slice products are exact and the recombination order fixed."""
     ds = datagen.generate(n, p, m, t, seed=n + p)
     basis, values = gw.eigendecompose(ds["kinship"])
     out = {}
-    for cl in ("1", "2", "3", "4"):
+    for cl in ("1", "2", "3", "4", "5"):
         out[cl] = run(ds, basis, values, "genotypes", options={"i8_cluster": int(cl)})
     assert not np.isnan(out["2"]).any()
-    assert np.array_equal(out["1"], out["2"])
-    assert np.array_equal(out["1"], out["3"])
-    assert np.array_equal(out["1"], out["4"])
+    for cl in ("2", "3", "4", "5"):
+        assert np.array_equal(out["1"], out[cl]), cl
 
 
 def test_auto_coding_picks_the_path_per_slab():
