@@ -309,12 +309,15 @@ int encode_i8(CUtensorMap* tx, const void* x, int64_t kp, int64_t cols, CUtensor
     if (r != CUDA_SUCCESS)
       return set_status(st, GWG_CUDA, -1, -1, "tensor map (int8 slices) failed (%d)", int(r));
     // the half-slot box of the pair MMA (I8Tile MMA2): rb/2 rows of one slice;
-    // otherwise the same map as tb
+    // for CTA pairs / 2 x 2 clusters the odd rank's box: the slots after the
+    // even rank's 4 (3 real slices with I8_SEVEN_SLOTS); otherwise tb itself
     const cuuint32_t hbox[3] = {I8Cfg::BK, cuuint32_t(rb / 2), 1};
+    const cuuint32_t obox[3] = {I8Cfg::BK, cuuint32_t(rb),
+                                cuuint32_t(I8_SEVEN_SLOTS ? I8Cfg::SLICES - 4 : 4)};
     r = tbh == nullptr ? CUDA_SUCCESS
-        : slices_box == 3
+        : slices_box == 3 || slices_box == 4
             ? encode(tbh, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(slices), gdim,
-                     gstride, hbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     gstride, slices_box == 3 ? hbox : obox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
             : (*tbh = *tb, CUDA_SUCCESS);
@@ -371,7 +374,8 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
                                : pair_mma_default(kp) ? 4 : 2;
   CUtensorMap tx, tb, tbh;
   if (int rc = encode_i8(&tx, xi8, kp, cols, &tb, slices, ncols, I8Cfg::RB,
-                         cl == 4 ? 3 : I8Cfg::SLOTS / cl, st, I8Cfg::BM, &tbh))
+                         cl == 4 ? 3 : cl == 1 ? (I8_SEVEN_SLOTS ? 7 : 8) : 4, st, I8Cfg::BM,
+                         &tbh))
     return rc;
   const int pair = cl >= 2 ? 2 : 1;
   const int64_t units = int64_t((a.tiles_m + pair - 1) / pair) * a.tiles_r;

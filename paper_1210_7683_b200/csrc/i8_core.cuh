@@ -21,6 +21,14 @@
 #ifndef I8_NO_TMA  // timing ablation only: stages marked full without loading them
 #define I8_NO_TMA 0
 #endif
+// The B tile's eighth slot is never multiplied (BN <= 7 RB + 8 rows, whose
+// accumulator columns the epilogues do not read): 1 = TMA boxes cover the
+// seven slice slots only (single CTAs and trait pairs one 7-slot box, B pairs
+// and 2 x 2 clusters 4 + 3 slots), so no zero-filled slot is written to shared
+// memory; 0 = whole 8-slot boxes (the eighth zero-filled out of bounds)
+#ifndef I8_SEVEN_SLOTS
+#define I8_SEVEN_SLOTS 1
+#endif
 #ifndef I8_PREFETCH  // stages ahead the producer prefetches into L2 (B not L2-resident)
 #define I8_PREFETCH 0  // measured: 4-16 stages ahead made c2 rotation 44.7 -> 72-78 ms, c4 linear 30.8 -> 41.7 ms
 #endif
@@ -90,6 +98,8 @@ struct I8Tile {
   static_assert(!MMA2 || (CLUSTER == 2 && PAIR_AXIS == 0 && RB == 32),
                 "pair MMA: SNP-tile pairs on 32-row B tiles (112 rows = 14 swizzle atoms per CTA)");
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_SMEM;
+  // bytes TMA lands in one CTA's stage (non-MMA2): the seven slice slots
+  static constexpr uint32_t STAGE_TX = I8_SEVEN_SLOTS ? A_BYTES + SLICES * RB * BK : STAGE_BYTES;
   static constexpr int EPI_WARPS = EPI_WARPS_;  // multiple of 4 (TMEM lane quarters)
   static constexpr int THREADS = (4 + EPI_WARPS) * 32;  // 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
   static constexpr int TMEM_COLS = 512;   // ACC_BUFS accumulator buffers x BN
@@ -787,7 +797,7 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
           if (lane_is_0()) tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, sch.rank * C::B_SLICES_PER_CTA);
         }
       }
-      mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], C::STAGE_BYTES);
+      mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], C::STAGE_TX);
       if constexpr (C::PAIR_AXIS == 2) {
         // 2 x 2: A rows [rb * 64, +64) to both CTAs of this SNP tile (ranks
         // sb, sb + 2), B slots [sb * 4, +4) to both CTAs of this B tile
@@ -797,7 +807,8 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
         tma_load_2d_mc_w<C::WS>(st + rb * (C::A_BYTES / 2), tmap_x, ks * C::BK,
                                 tm * C::BM + rb * (C::BM / 2), &sm.full[s],
                                 uint16_t((1u << sb) | (1u << (sb + 2))), pol_x);
-        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sb * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
+        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sb * C::B_PART, sb ? tmap_bh : tmap_b,
+                                ks * C::BK, tr * C::RB,
                                 sb * C::B_SLICES_PER_CTA, &sm.full[s], uint16_t(3u << (2 * rb)),
                                 pol_b);
         continue;
@@ -812,7 +823,8 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
       }
       tma_load_2d_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
       if (C::CLUSTER > 1)
-        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sch.rank * C::B_PART, tmap_b, ks * C::BK, tr * C::RB,
+        tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sch.rank * C::B_PART,
+                                sch.rank ? tmap_bh : tmap_b, ks * C::BK, tr * C::RB,
                        sch.rank * C::B_SLICES_PER_CTA, &sm.full[s],
                        uint16_t((1u << C::CLUSTER) - 1), pol_b);
       else

@@ -654,7 +654,9 @@ struct LinOps {
   cudaError_t (*launch[5])(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                            const LinArgs&, int, cudaStream_t, const CUtensorMap&) = {
       nullptr, nullptr, nullptr, nullptr, nullptr};
-  int b_slices_box[5] = {8, 4, 8, 3, 4};  // slice slots per TMA box (pair MMA: + a half-slot box)
+  // slice slots per TMA box (pairs / 2 x 2: the even rank's; the odd rank's
+  // box holds the rest, 3 or 4 slots; pair MMA: + a half-slot box)
+  int b_slices_box[5] = {I8_SEVEN_SLOTS ? 7 : 8, 4, I8_SEVEN_SLOTS ? 7 : 8, 3, 4};
   int a_box_rows[5] = {128, 128, 64, 128, 64};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
   int cells = 0;         // traits per epilogue warp and tile (LinCfg::CELLS)
