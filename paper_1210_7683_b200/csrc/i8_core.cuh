@@ -737,7 +737,10 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
   // A (the int8 SNP tile) is re-read by every B tile of its group, so it is
   // NOT evict_first (measured: linear_solve DRAM reads 2.66 -> 1.61 GB, 2.84
   // -> 2.70 ms at c1); the results stream out evict_first (tma_store_2d).
-  const uint64_t pol_x = policy_evict_normal();
+#ifndef I8_X_POLICY  // L2 policy of the SNP-tile loads: 0 evict_normal, 1 evict_last
+#define I8_X_POLICY 0
+#endif
+  const uint64_t pol_x = I8_X_POLICY == 1 ? policy_evict_last() : policy_evict_normal();
   const uint64_t pol_b = b_resident ? policy_evict_last() : policy_evict_normal();
   // B streaming from HBM (large n): prefetch the operand boxes of the stage
   // I8_PREFETCH stages ahead into L2, so the stage ring (4 x 48 KB, ~1,800 MMA

@@ -330,3 +330,46 @@ def test_device_output_solves_are_asynchronous_with_deferred_errors(case):
         got = out.cpu().numpy()  # torch's stream waits for the engine
         eng.synchronize()
     assert np.array_equal(got, base)
+
+
+def test_trait_side_stream_interleavings(case):
+    """On the split path gwg_set_traits queues its work on the engine's side
+    stream and the SNP rotation joins it (set_traits_impl, split_build_ahead):
+    whatever runs in between — a second set_traits, new covariates, an option
+    change, a host run_grid, an error read — sees the traits of the last
+    set_traits, bit for bit what a fresh engine computes."""
+    ds, basis, values, base = case
+    rng = np.random.default_rng(5)
+    y2 = rng.standard_normal(ds["traits"].shape)
+    h2b = rng.uniform(0.1, 0.9, ds["h2"].shape)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    x = dev(ds["snps"])
+    with gw.Engine(ds["kinship"].shape[0], 4) as fresh:
+        fresh.set_spectrum(basis, values)
+        fresh.set_covariates(ds["xl"])
+        fresh.set_snp_coding("genotypes")
+        fresh.set_traits(y2, h2b, ds["sigma2"])
+        ref2 = fresh.run_grid(ds["snps"])
+    with engine(ds, basis, values, coding="genotypes") as eng:
+        first = eng.run_grid(ds["snps"])
+        assert np.array_equal(first, base)
+        # two trait sets back to back on the device: the second wins
+        eng.set_traits(dev(ds["traits"]), dev(ds["h2"]), dev(ds["sigma2"]))
+        eng.set_traits(dev(y2), dev(h2b), dev(ds["sigma2"]))
+        out = torch.empty((ds["snps"].shape[1], 70, 4), dtype=torch.float64, device="cuda")
+        eng.solve_snp_slab(x, out=out)
+        eng.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref2)
+        # device traits, then a host run_grid straight away
+        eng.set_traits(dev(ds["traits"]), dev(ds["h2"]), dev(ds["sigma2"]))
+        assert np.array_equal(eng.run_grid(ds["snps"]), base)
+        # device traits, an option round trip and new (equal) covariates in between
+        eng.set_traits(dev(y2), dev(h2b), dev(ds["sigma2"]))
+        eng.set_option("i8_cluster", 1)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(dev(y2), dev(h2b), dev(ds["sigma2"]))
+        eng.set_option("i8_cluster", 0)
+        out2 = torch.empty_like(out)
+        eng.solve_snp_slab(x, out=out2)
+        got = out2.cpu().numpy()  # torch's stream is ordered after the engine
+        assert np.array_equal(got, ref2)
