@@ -39,6 +39,12 @@
 #ifndef LIN_RASTER
 #define LIN_RASTER 0  // trait tiles fastest: measured 2.49-2.54 vs 2.45-2.46 ms at c1 (off)
 #endif
+#ifndef GWG_B_RESIDENT_MB  // sliced operands up to this size are loaded evict_last
+#define GWG_B_RESIDENT_MB 48
+#endif
+#ifndef GWG_PERSIST_L2_MB  // L2 set-aside for persisting (evict_last) lines, MB (0 = leave)
+#define GWG_PERSIST_L2_MB 0
+#endif
 #ifndef SNP_I8_BLOCKS  // blocks per SM of the code conversion
 #define SNP_I8_BLOCKS 8
 #endif
@@ -360,7 +366,7 @@ int launch_i8(gwg_engine* e, const void* xi8, const void* slices, int64_t cols, 
   a.tiles_m = int32_t(ceil_div(cols, I8Cfg::BM));
   a.tiles_r = int32_t(ceil_div(ncols, I8Cfg::RB));
   a.kstages = int32_t(kp / I8Cfg::BK);
-  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
+  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(GWG_B_RESIDENT_MB) << 20);
   a.gate = gate_word(e);
   a.gate_codes = e->gate_want;
   a.raster = (ROT_RASTER == 2 || (ROT_RASTER == 1 && a.b_resident)) ? 1 : 0;
@@ -529,7 +535,7 @@ void invalidate_derived(gwg_engine* e, bool spectrum) {
 int spectrum_range(gwg_engine* e, gwg_status* st) {
   GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
   double* dx = e->exps.d();
-  gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, nullptr, nullptr, 0,
+  gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), e->n, nullptr, nullptr, 0,
                                                     dx);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
@@ -577,7 +583,7 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
     GWG_CUDA_TRY(cudaEventSynchronize(e->ev_range));
     std::copy(e->range_host, e->range_host + 6, rg);
   } else {  // device-resident inputs: one small reduction and a round trip
-    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(),
+    gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(),
                                                       e->sigma2.d(), int32_t(t), dx);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
@@ -1030,7 +1036,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
   a.tiles_m = int32_t(ceil_div(rows, I8Cfg::BM));
   a.tiles_r = int32_t(tiles_r);
   a.kstages = int32_t(kp / I8Cfg::BK);
-  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(48) << 20);
+  a.b_resident = size_t(I8Cfg::SLICES) * ncols * kp <= (size_t(GWG_B_RESIDENT_MB) << 20);
   a.gate = gate_word(e);
   a.gate_codes = e->gate_want;
   // numpy-order results with L2-resident W slices: trait tiles fastest, so
@@ -1252,7 +1258,7 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
     // device busy while the 48-byte answer travels, so the split grid's
     // build finds it on the host without stalling the device
     GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
-    gwg::expsum_range_kernel<<<1, 1024, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
+    gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
                                                       e->sigma2.d(), int32_t(t), e->exps.d());
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
@@ -1392,6 +1398,18 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
   cudaError_t err;
   if ((err = cudaSetDevice(device)) != cudaSuccess) return bail("cudaSetDevice", err);
   cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device);
+  if (GWG_PERSIST_L2_MB > 0) {
+    // L2 set-aside for the evict_last operands (the W / Z slices the int8
+    // kernels keep resident): without one, evict_last lines compete with the
+    // streamed results like any other
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    const size_t want = std::min<size_t>(size_t(max_persist), size_t(GWG_PERSIST_L2_MB) << 20);
+    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    (void)cudaGetLastError();
+  }
   int cc_major = 0;
   cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
   if (cc_major != 10) {

@@ -671,7 +671,10 @@ __device__ __forceinline__ void i8_acc_release(const I8Smem<C>& sm, int buf) {
 // stay in L2 even when they do not fit whole (n = 10,000: X int8 1 GB, Z
 // slices 0.8 GB, W slices 0.3 GB), and each B tile is fetched from HBM once
 // per group instead of once per SNP tile.
-constexpr int I8_GROUP_M = 16;
+#ifndef I8_GROUP
+#define I8_GROUP 16
+#endif
+constexpr int I8_GROUP_M = I8_GROUP;
 __device__ __forceinline__ void i8_tile_coords(int tile, int tiles_m, int tiles_r, int& tm,
                                                int& tr) {
   const int per_group = I8_GROUP_M * tiles_r;

@@ -104,7 +104,8 @@ __global__ void transpose_kernel(const double* __restrict__ src, double* __restr
 
 // ---- low-rank S_BR (expsum.cpp): D = E F with positive factors ------------------
 
-// Range of the factorisation, one CTA of 1024 threads:
+// Range of the factorisation, one CTA (256 threads: it fits beside the code
+// conversion on a busy SM):
 //   out[0] = min lambda, out[1] = max lambda,
 //   out[2] / out[3] = min / max of gamma_j = (1 - h_j) / h_j over traits with h_j != 0,
 //   out[4] = number of such traits, out[5] = 1 if some trait's scale
