@@ -426,9 +426,8 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   {
     // a few blocks per SM (snp_to_i8_kernel): HBM-bound, leaves room for
     // the trait side running concurrently
-    const int64_t items = cols * (kp / 2);
     const int blocks = int(std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(items, 256 * SNP_I8_ITEMS), int64_t(e->sms) * SNP_I8_BLOCKS)));
+        1, std::min<int64_t>(ceil_div(cols, SNP_I8_ITEMS), int64_t(e->sms) * SNP_I8_BLOCKS)));
     gwg::snp_to_i8_kernel<<<blocks, 256, 0, e->comp>>>(
         src, lds, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
         static_cast<unsigned long long*>(e->err.ptr) + 2);

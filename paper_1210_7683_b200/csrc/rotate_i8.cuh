@@ -142,12 +142,12 @@ __global__ void __launch_bounds__(RotI8Cfg<CL>::THREADS, 1)
 
 // X (n x cols, ld lds, f64 genotype codes) -> int8 [col][kp] with zero padding;
 // flags (*bad = 0) any value that is not an integer in [-127, 127].  HBM-bound
-// (8 bytes in, 1 out per code).  The work is the flat sequence of (column,
-// code pair) items, kp / 2 per column: consecutive threads take consecutive
-// 16-byte pairs (lds is even: 16-byte aligned columns), each thread loads
-// SNP_I8_ITEMS of them before converting any (bytes in flight without a full
-// SM), so a grid of a few blocks per SM saturates HBM and leaves room on every
-// SM for the trait-side kernels that run concurrently (split_build_ahead).
+// (8 bytes in, 1 out per code).  A block takes SNP_I8_ITEMS columns at a time
+// and each thread one 16-byte code pair of every one of them (lds is even:
+// 16-byte aligned columns), all loads issued before any conversion: bytes in
+// flight without a full SM, so a grid of a few blocks per SM saturates HBM and
+// leaves room on every SM for the trait-side kernels that run concurrently
+// (split_build_ahead).
 #ifndef SNP_I8_ITEMS
 #define SNP_I8_ITEMS 4
 #endif
@@ -158,36 +158,32 @@ __global__ void __launch_bounds__(256) snp_to_i8_kernel(const double* __restrict
   constexpr int U = SNP_I8_ITEMS;
   bool ok = true;
   const int pairs = kp >> 1;
-  const int64_t total = int64_t(cols) * pairs;
-  const int64_t step = int64_t(gridDim.x) * blockDim.x * U;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x; base < total;
-       base += step) {
-    double2 v[U];
+  for (int c0 = blockIdx.x * U; c0 < cols; c0 += gridDim.x * U) {
+    for (int k2 = threadIdx.x; k2 < pairs; k2 += blockDim.x) {
+      const int k = 2 * k2;
+      double2 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t it = base + int64_t(u) * blockDim.x;
-      v[u] = make_double2(0.0, 0.0);
-      if (it < total) {
-        const int64_t c = it / pairs;
-        const int k = 2 * int(it - c * pairs);
-        const double* col = x + c * lds;
-        if (k + 1 < n)
-          v[u] = __ldcs(reinterpret_cast<const double2*>(col + k));
-        else if (k < n)
-          v[u].x = col[k];
+      for (int u = 0; u < U; ++u) {
+        v[u] = make_double2(0.0, 0.0);
+        const double* col = x + int64_t(c0 + u) * lds;
+        if (c0 + u < cols) {
+          if (k + 1 < n)
+            v[u] = __ldcs(reinterpret_cast<const double2*>(col + k));
+          else if (k < n)
+            v[u].x = col[k];
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t it = base + int64_t(u) * blockDim.x;
-      if (it >= total) continue;
-      const bool good = (v[u].x == rint(v[u].x)) & (fabs(v[u].x) <= 127.0) &
-                        (v[u].y == rint(v[u].y)) & (fabs(v[u].y) <= 127.0);
-      ok &= good;
-      // item it = pair (it % pairs) of column (it / pairs): byte offset 2 it
-      reinterpret_cast<uint16_t*>(out)[it] =
-          good ? uint16_t((uint32_t(int(v[u].x)) & 0xffu) | ((uint32_t(int(v[u].y)) & 0xffu) << 8))
-               : uint16_t(0);
+      for (int u = 0; u < U; ++u) {
+        if (c0 + u >= cols) continue;
+        const bool good = (v[u].x == rint(v[u].x)) & (fabs(v[u].x) <= 127.0) &
+                          (v[u].y == rint(v[u].y)) & (fabs(v[u].y) <= 127.0);
+        ok &= good;
+        reinterpret_cast<uint16_t*>(out + int64_t(c0 + u) * kp)[k2] =
+            good ? uint16_t((uint32_t(int(v[u].x)) & 0xffu) |
+                            ((uint32_t(int(v[u].y)) & 0xffu) << 8))
+                 : uint16_t(0);
+      }
     }
   }
   if (!ok) *bad = 0;  // error words are reset to all ones
