@@ -1269,9 +1269,23 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
   if (rotated) {
     if (int rc = upload_cols(e, e->y_rot, y, ldy, t, y_where, e->comp, st)) return rc;
   } else {
-    if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st)) return rc;
+    // Y on this device in a TMA-addressable layout (even pitch, 16-byte
+    // aligned) is rotated where it lies — read asynchronously, like every
+    // device operand — instead of through a copy
+    bool in_place = false;
+    if (y_where == GWG_DEVICE && ldy % 2 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+      cudaPointerAttributes pa{};
+      in_place = cudaPointerGetAttributes(&pa, y) == cudaSuccess &&
+                 pa.type == cudaMemoryTypeDevice && pa.device == e->device;
+      (void)cudaGetLastError();
+    }
     GWG_CUDA_TRY(e->y_rot.ensure(size_t(e->np) * t * sizeof(double)));
-    if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
+    if (in_place) {
+      if (int rc = rotate(e, y, t, e->y_rot.d(), st, ldy)) return rc;
+    } else {
+      if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st)) return rc;
+      if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
+    }
   }
   const int64_t tiles_t = ceil_div(t, e->ops.bt);
   const size_t bops_doubles = size_t(tiles_t) * e->np * (e->p + 1) * e->ops.bt;
