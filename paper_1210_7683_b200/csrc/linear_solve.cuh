@@ -37,6 +37,10 @@ namespace gwg {
 #define LIN_EXPERIMENT 0
 #endif
 
+#ifndef LIN_STORE_EXP
+#define LIN_STORE_EXP 0
+#endif
+
 #ifndef LIN_TRACE
 #define LIN_TRACE 0
 #endif
@@ -493,6 +497,12 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
               const int j = j0 + cell0 + g0 + u;
               if (j >= a.t) continue;
               double* dst = a.out + (il * a.out_si + int64_t(j) * a.out_sj) * P;
+              // timing only (LIN_STORE_EXP): 1 = every other cell stored (half the
+              // bytes), 2 = the same stores folded into a 16 MB window (L2-resident,
+              // no DRAM writes)
+              if (LIN_STORE_EXP == 1 && (u & 1)) continue;
+              if (LIN_STORE_EXP == 2)
+                dst = a.out + ((il * a.out_si + int64_t(j) * a.out_sj) * P) % (int64_t(1) << 21);
               if (a.use_tma == 3) {
 #pragma unroll
                 for (int c = 0; c < P; c += 4)
