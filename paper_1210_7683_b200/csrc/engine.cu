@@ -48,6 +48,9 @@
 #ifndef SNP_I8_BLOCKS  // blocks per SM of the code conversion
 #define SNP_I8_BLOCKS 8
 #endif
+#ifndef GWG_COV_STREAM  // W's covariate columns on a helper stream beside the trait column
+#define GWG_COV_STREAM 0  // measured neutral at c1 (the rotation holds the SMs the covariate GEMMs need)
+#endif
 #ifndef GWG_TRAITS_ON_SIDE  // gwg_set_traits' device work on the side stream (split path)
 #define GWG_TRAITS_ON_SIDE 1
 #endif
@@ -717,11 +720,28 @@ int build_split(gwg_engine* e, gwg_status* st) {
     const int64_t r = e->sbr_terms, rc_cols = r * (p - 1), p8 = e->lops.p8;
     if (padded)  // padding rows (c >= p, traits past t) stay zero
       GWG_CUDA_TRY(cudaMemsetAsync(e->wmat.ptr, 0, size_t(np) * ncols * sizeof(double), e->comp));
-    if (int rc = rotate(e, e->vmat.d() + (p - 1) * np, t, e->wmat.d() + (p - 1) * np, st,
-                        p8 * np, nullptr, e->basis_t.d(), p8 * np))
-      return rc;
     GWG_CUDA_TRY(e->xepanel.ensure(size_t(np) * rc_cols * sizeof(double)));
     GWG_CUDA_TRY(e->umat.ensure(size_t(n) * rc_cols * sizeof(double)));
+    // U's split-K partials: n x r(p-1) outputs over K = n are a few dozen
+    // tiles, so K is split until the tiles fill the SMs (summed in a fixed order)
+    int ksplit = 1;
+    {
+      const int64_t kchunks = np / e->sops.bk;
+      const int64_t units = ceil_div(n, e->sops.bm) * ceil_div(rc_cols, e->sops.bt);
+      while (ksplit < 16 && kchunks % (2 * ksplit) == 0 && kchunks / (2 * ksplit) >= 4 &&
+             ceil_div(units * 2 * ksplit, 2) <= e->sms)
+        ksplit *= 2;
+    }
+    if (ksplit > 1)
+      GWG_CUDA_TRY(e->upart.ensure(size_t(ksplit) * n * rc_cols * sizeof(double)));
+    // The covariate columns (below) and the trait column (a rotation) write
+    // disjoint rows of W and share no input but E / F: the covariate chain of
+    // small launches runs on the helper stream while this stream rotates.
+    if (GWG_COV_STREAM) {
+      GWG_CUDA_TRY(cudaEventRecord(e->ev_cov_fork, e->comp));
+      GWG_CUDA_TRY(cudaStreamWaitEvent(e->side2, e->ev_cov_fork, 0));
+      std::swap(e->comp, e->side2);
+    }
     gwg::ExpSumArgs x;
     x.n = n;
     x.np = np;
@@ -739,27 +759,23 @@ int build_split(gwg_engine* e, gwg_status* st) {
     gwg::expsum_e_kernel<<<int(rc_cols), 256, 0, e->comp>>>(x);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
-    // U[k][(c, q)] = sum_l Z[k][l] x_c[l] E[l][q]  (A = Z^T's columns = Z's rows):
-    // n x r(p-1) outputs over K = n — a few dozen tiles, so K is split until
-    // the tiles fill the SMs (partials summed in a fixed order)
-    int ksplit = 1;
-    {
-      const int64_t kchunks = np / e->sops.bk;
-      const int64_t units = ceil_div(n, e->sops.bm) * ceil_div(rc_cols, e->sops.bt);
-      while (ksplit < 16 && kchunks % (2 * ksplit) == 0 && kchunks / (2 * ksplit) >= 4 &&
-             ceil_div(units * 2 * ksplit, 2) <= e->sms)
-        ksplit *= 2;
+    // U[k][(c, q)] = sum_l Z[k][l] x_c[l] E[l][q]  (A = Z^T's columns = Z's rows)
+    int rc = sbr_gemm(e, e->basis_t.d(), n, np, n, e->xepanel.d(), np, rc_cols, e->umat.d(),
+                      rc_cols, true, st, ksplit, ksplit > 1 ? e->upart.d() : nullptr,
+                      n * rc_cols);
+    // W[(j p8 + c) np + k] = sum_q U[k][(c, q)] F[q][j]
+    for (int64_t c = 0; rc == GWG_OK && c + 1 < p; ++c)
+      rc = sbr_gemm(e, e->umat.d() + c * r, r, rc_cols, n, e->fpanel.d(), r, t,
+                    e->wmat.d() + c * np, p8 * np, false, st);
+    if (GWG_COV_STREAM) {
+      std::swap(e->comp, e->side2);
+      GWG_CUDA_TRY(cudaEventRecord(e->ev_cov_join, e->side2));
     }
-    if (ksplit > 1)
-      GWG_CUDA_TRY(e->upart.ensure(size_t(ksplit) * n * rc_cols * sizeof(double)));
-    if (int rc = sbr_gemm(e, e->basis_t.d(), n, np, n, e->xepanel.d(), np, rc_cols,
-                          e->umat.d(), rc_cols, true, st, ksplit,
-                          ksplit > 1 ? e->upart.d() : nullptr, n * rc_cols))
-      return rc;
-    for (int64_t c = 0; c + 1 < p; ++c)  // W[(j p8 + c) np + k] = sum_q U[k][(c, q)] F[q][j]
-      if (int rc = sbr_gemm(e, e->umat.d() + c * r, r, rc_cols, n, e->fpanel.d(), r, t,
-                            e->wmat.d() + c * np, p8 * np, false, st))
-        return rc;
+    if (rc == GWG_OK)
+      rc = rotate(e, e->vmat.d() + (p - 1) * np, t, e->wmat.d() + (p - 1) * np, st, p8 * np,
+                  nullptr, e->basis_t.d(), p8 * np);
+    if (GWG_COV_STREAM) GWG_CUDA_TRY(cudaStreamWaitEvent(e->comp, e->ev_cov_join, 0));
+    if (rc) return rc;
   } else {
     if (int rc = rotate(e, e->vmat.d(), ncols, e->wmat.d(), st, np, nullptr, e->basis_t.d()))
       return rc;
@@ -1447,6 +1463,15 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
                                             GWG_SIDE_PRIORITY ? greatest : least)) != cudaSuccess)
       return bail("stream", err);
   }
+  {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if ((err = cudaStreamCreateWithPriority(&e->side2, cudaStreamNonBlocking,
+                                            GWG_SIDE_PRIORITY ? greatest : least)) != cudaSuccess)
+      return bail("stream", err);
+  }
+  cudaEventCreateWithFlags(&e->ev_cov_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_cov_join, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming);
   for (int b = 0; b < 2; ++b) {
@@ -1480,6 +1505,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->h2d) cudaStreamSynchronize(e->h2d);
   if (e->d2h) cudaStreamSynchronize(e->d2h);
   if (e->side) cudaStreamSynchronize(e->side);
+  if (e->side2) cudaStreamSynchronize(e->side2);
   for (DevBuf* b : {&e->basis, &e->lambda, &e->xl_raw, &e->xl_rot, &e->y_raw, &e->y_rot, &e->h2,
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
@@ -1496,7 +1522,8 @@ void gwg_engine_destroy(gwg_engine* e) {
     if (e->ev_d2h_done[b]) cudaEventDestroy(e->ev_d2h_done[b]);
   }
   for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2],
-                         e->ev_wait, e->ev_signal, e->ev_fork, e->ev_join})
+                         e->ev_wait, e->ev_signal, e->ev_fork, e->ev_join, e->ev_cov_fork,
+                         e->ev_cov_join})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->pipe_events) cudaEventDestroy(ev);
@@ -1509,6 +1536,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   if (e->h2d) cudaStreamDestroy(e->h2d);
   if (e->d2h) cudaStreamDestroy(e->d2h);
   if (e->side) cudaStreamDestroy(e->side);
+  if (e->side2) cudaStreamDestroy(e->side2);
   delete e;
 }
 

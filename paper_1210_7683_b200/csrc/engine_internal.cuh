@@ -97,6 +97,10 @@ struct gwg_engine {
   // side (mark_trait_fork / launch_split): side stream, fork and join events
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // helper stream of the split build (W's covariate columns beside its trait
+  // column) and its fork / join events
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_cov_fork = nullptr, ev_cov_join = nullptr;
   bool fork_pending = false;
   // trait-side device work queued on the side stream and not yet joined into
   // the compute stream (gwg_set_traits on the split path, then the split
