@@ -1015,7 +1015,7 @@ int launch_split(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t i0, 
     } else if (use_tma == 2) {
       const cuuint64_t gdim[2] = {cuuint64_t(rows * p), cuuint64_t(t)};
       const cuuint64_t gstride[1] = {cuuint64_t(out_sj * p * 8)};
-      const cuuint32_t box[2] = {cuuint32_t(32 * p), cuuint32_t(e->lops.cells)};
+      const cuuint32_t box[2] = {cuuint32_t(32 * p), cuuint32_t(e->lops.stream_rows)};
       const cuuint32_t es[2] = {1, 1};
       r = encode(&tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dev_out, gdim, gstride, box, es,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -37,6 +37,9 @@ namespace gwg {
 #define LIN_EXPERIMENT 0
 #endif
 
+#ifndef LIN_STREAM_HALF
+#define LIN_STREAM_HALF 0  // per-group boxes measured slower at c1 (2.37 vs 2.34 ms)
+#endif
 #ifndef LIN_STORE_EXP
 #define LIN_STORE_EXP 0
 #endif
@@ -140,6 +143,8 @@ struct LinCfg {
   // layout): a warp's results are, per trait, 32 SNPs x p contiguous doubles;
   // staged [cell][lane*p + c] and stored as one TMA box {32p, CELLS}
   static constexpr bool STREAM_TMA = 32 * P <= 256 && CELLS * 32 * P * 8 <= 4096;
+  // stream boxes per group of cells (GROUP rows) instead of per tile (CELLS rows)
+  static constexpr bool STREAM_HALF = LIN_STREAM_HALF != 0;
   // stream order by direct 256-bit stores from registers (use_tma = 3): a
   // lane's p results of a cell are p/4 aligned 32-byte pieces, a warp's cell
   // 32p contiguous doubles — no staging, no proxy fence, no TMA store
@@ -527,6 +532,28 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
                            pol_out);
             }
           }
+        } else if (L::STREAM_TMA && a.use_tma == 2 && L::STREAM_HALF) {
+          // one box {32p, GROUP} per group of cells, the staging tile used as
+          // CELLS / GROUP slots in turn: a slot is rewritten only after the
+          // store issued CELLS / GROUP groups earlier has read it, so the wait
+          // is for an older store than the one just issued
+          constexpr int SLOTS = L::CELLS / L::GROUP;
+          if (lane == 0) {
+            if constexpr (SLOTS >= 2)
+              bulk_wait_read1();
+            else
+              bulk_wait_read0();
+          }
+          __syncwarp();
+          double* rowp = reinterpret_cast<double*>(stg) + (g0 / L::GROUP) * (L::GROUP * 32 * P);
+#pragma unroll
+          for (int u = 0; u < L::GROUP; ++u)
+#pragma unroll
+            for (int c = 0; c < P; ++c) rowp[(u * 32 + lane) * P + c] = beta[u][c];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0)
+            tma_store_2d(&tmap_out, rowp, (tm * C::BM + qd * 32) * P, j0 + cell0 + g0);
         } else if (L::STREAM_TMA && a.use_tma == 2) {
           if (g0 == 0) {
             if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
@@ -670,6 +697,7 @@ struct LinOps {
   int a_box_rows[5] = {128, 128, 64, 128, 64};  // SNP rows per TMA box of the A tile
   int row = 0;           // doubles per TMA box row (LinCfg::BW)
   int cells = 0;         // traits per epilogue warp and tile (LinCfg::CELLS)
+  int stream_rows = 0;   // rows (cells) of a stream-layout result box
   bool stream_tma = false;  // stream-layout results by TMA boxes {32p, cells}
   bool tma_row = false;  // results leave by unswizzled TMA boxes {row, 32}
   bool stream_stg = false;  // stream-layout results by direct 256-bit stores
@@ -690,6 +718,7 @@ LinOps make_lin_ops() {
   o.launch[4] = &launch_linear_solve<P, 5>;
   o.row = LinCfg<P>::BW;
   o.cells = LinCfg<P>::CELLS;
+  o.stream_rows = LinCfg<P>::STREAM_HALF ? LinCfg<P>::GROUP : LinCfg<P>::CELLS;
   o.stream_tma = LinCfg<P>::STREAM_TMA;
   o.tma_row = LinCfg<P>::TMA_ROW;
   o.stream_stg = LinCfg<P>::STREAM_STG;
