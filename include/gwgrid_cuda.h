@@ -165,7 +165,12 @@ int32_t gwg_set_covariates(gwg_engine* e, const double* xl, int32_t where, gwg_s
  * (weights d, D = 1/d, D.Y', D.X_L', S_TL, chol(S_TL), z_T) in one kernel.
  * Replaces transform_trait_slab + build_trait_contexts (grid.cpp:135-175) and
  * the per-pass load_pass (grid.cpp:501-517).  Asynchronous: the call queues
- * its work and returns without a host round trip.  A trait whose rotated
+ * its work and returns without a host round trip — on the genotype split path
+ * on the engine's side stream, so it runs under the next slab's upload and
+ * code conversion; the compute stream is ordered after it before anything
+ * reads it (and by gwg_compute_stream, gwg_signal_stream, gwg_synchronize).
+ * Device operands are read asynchronously: keep them unchanged until the next
+ * synchronising call.  A trait whose rotated
  * weights fail the relative floor (gls.cpp:59-75) is reported as
  * GWG_NOT_POSITIVE_DEFINITE, snp_index = -1, trait_index = the first such j,
  * by the next call that synchronises (gwg_solve_snp_slab, gwg_run_grid*,
@@ -358,7 +363,8 @@ void gwg_reset_counters(gwg_engine* e);
 int32_t gwg_synchronize(gwg_engine* e, gwg_status* st);
 
 /* The engine's compute stream (cudaStream_t as void*), so callers can order
- * their own device work (timing events, torch streams) against it. */
+ * their own device work (timing events, torch streams) against it; work still
+ * queued on the engine's side stream (gwg_set_traits) is joined into it first. */
 void* gwg_compute_stream(gwg_engine* e);
 
 /* Positive exponential sum for 1/x on [x_min, x_max] (the low-rank

@@ -1768,6 +1768,10 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
-void* gwg_compute_stream(gwg_engine* e) { return e ? static_cast<void*>(e->comp) : nullptr; }
+void* gwg_compute_stream(gwg_engine* e) {
+  if (!e) return nullptr;
+  if (cudaSetDevice(e->device) == cudaSuccess) (void)join_side(e);  // side work ordered first
+  return static_cast<void*>(e->comp);
+}
 
 }  // extern "C"
