@@ -94,6 +94,10 @@ namespace gwg {
 #define LIN_WS 1
 #endif
 
+#ifndef LIN_WS_MMA2  // warp-collective issue for the pair MMA too (measured slower at c2)
+#define LIN_WS_MMA2 0
+#endif
+
 #ifndef LIN_CTX_SMEM
 #define LIN_CTX_SMEM 1
 #endif
@@ -185,7 +189,8 @@ struct LinCfg {
   // CL = 5: 2 x 2 clusters multicasting halves of both operands
   // warp-collective issue except for the pair MMA (measured, see i8_core.cuh)
   using Tile = I8Tile<RB, STAGES, OUT_BUFS, EPI, CL == 5 ? 4 : CL >= 2 ? 2 : 1,
-                      CL == 3 ? 1 : CL == 5 ? 2 : 0, EXTRA, MMA2, LIN_WS != 0 && !MMA2>;
+                      CL == 3 ? 1 : CL == 5 ? 2 : 0, EXTRA, MMA2,
+                      LIN_WS != 0 && (!MMA2 || LIN_WS_MMA2 != 0)>;
   static_assert(Tile::ACC_BUFS == ACC && Tile::OUT_Q == CHUNK, "tile geometry");
   // cells solved together (independent chains; KT is a power of two or 1)
   static constexpr int GMAX = LIN_GMAX > 0 && P <= 4 ? LIN_GMAX
