@@ -183,6 +183,12 @@ int run_pipeline(gwg_engine* e, const PipeSpec& sp, PipeStats* stats, gwg_status
       if (i8) {
         GWG_CUDA_TRY(cudaMemcpyAsync(e->raw8[bd].ptr, src, size_t(n) * rows, cudaMemcpyHostToDevice,
                                      up));
+      } else if (raw_ld(e) == n) {
+        // contiguous on both sides: one flat copy (a pitched copy of 8n-byte
+        // rows measured 41 vs 55 GB/s over PCIe, and its longer H2D window
+        // slowed the concurrent result D2H: c1 e2e 67 -> see DESIGN)
+        GWG_CUDA_TRY(cudaMemcpyAsync(e->raw[bd].ptr, src, size_t(n) * rows * 8,
+                                     cudaMemcpyHostToDevice, up));
       } else {
         GWG_CUDA_TRY(cudaMemcpy2DAsync(e->raw[bd].ptr, raw_ld(e) * 8, src, n * 8, n * 8, rows,
                                        cudaMemcpyHostToDevice, up));
