@@ -1282,8 +1282,11 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
     GWG_CUDA_TRY(cudaEventRecord(e->ev_range, e->comp));
     e->range_pending = true;
   }
+  bool uploads_done = false;  // ev_traits_in follows every host upload of this call
   if (rotated) {
     if (int rc = upload_cols(e, e->y_rot, y, ldy, t, y_where, e->comp, st)) return rc;
+    GWG_CUDA_TRY(cudaEventRecord(e->ev_traits_in, e->comp));
+    uploads_done = true;
   } else {
     // Y on this device in a TMA-addressable layout (even pitch, 16-byte
     // aligned) is rotated where it lies — read asynchronously, like every
@@ -1300,6 +1303,8 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
       if (int rc = rotate(e, y, t, e->y_rot.d(), st, ldy)) return rc;
     } else {
       if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st)) return rc;
+      GWG_CUDA_TRY(cudaEventRecord(e->ev_traits_in, e->comp));
+    uploads_done = true;
       if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
     }
   }
@@ -1341,7 +1346,14 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
   // host operands are consumed before the call returns (the caller owns and
   // may reuse them, like the reference's synchronous load_pass); device
   // operands stay asynchronous
-  if (y_where == GWG_HOST || s_where == GWG_HOST) GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  // (the uploads, not the context build: the caller may reuse its buffers, the
+  // device work continues asynchronously)
+  if (y_where == GWG_HOST || s_where == GWG_HOST) {
+    if (uploads_done)
+      GWG_CUDA_TRY(cudaEventSynchronize(e->ev_traits_in));  // after every upload
+    else
+      GWG_CUDA_TRY(cudaStreamSynchronize(e->comp));
+  }
   e->t = t;
   e->have_traits = true;
   return GWG_OK;
@@ -1471,6 +1483,7 @@ gwg_engine* gwg_engine_create(int32_t device, int64_t n, int64_t p, gwg_status* 
       return bail("stream", err);
   }
   cudaEventCreateWithFlags(&e->ev_cov_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_traits_in, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_cov_join, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming);
@@ -1523,7 +1536,7 @@ void gwg_engine_destroy(gwg_engine* e) {
   }
   for (cudaEvent_t ev : {e->ev_k0, e->ev_k1, e->ev_r0, e->ev_r1, e->ev_s[0], e->ev_s[1], e->ev_s[2],
                          e->ev_wait, e->ev_signal, e->ev_fork, e->ev_join, e->ev_cov_fork,
-                         e->ev_cov_join})
+                         e->ev_cov_join, e->ev_traits_in})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->slab_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->pipe_events) cudaEventDestroy(ev);

@@ -100,6 +100,7 @@ struct gwg_engine {
   // helper stream of the split build (W's covariate columns beside its trait
   // column) and its fork / join events
   cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_traits_in = nullptr;  // gwg_set_traits' host uploads done
   cudaEvent_t ev_cov_fork = nullptr, ev_cov_join = nullptr;
   bool fork_pending = false;
   // trait-side device work queued on the side stream and not yet joined into

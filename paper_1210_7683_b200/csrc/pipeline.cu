@@ -404,7 +404,9 @@ int32_t gwg_run_grid(gwg_engine* e, int64_t m, const void* x_r_host, double* b_h
                      const gwg_run_options* opts, gwg_counters* counters, gwg_status* st) {
   NvtxRange nvtx_("gwg_run_grid");
   clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
+  // no join here: the pipeline joins trait work still on the side stream right
+  // before the first slab's rotation, so the first uploads overlap it
+  if (int rc = check_engine(e, st, false)) return rc;
   return run_grid_impl(e, m, x_r_host, b_host, opts, counters, st);
 }
 

@@ -219,7 +219,7 @@ int32_t gwg_run_grid_files(gwg_engine* e, const char* snps_path, int32_t snps_ro
                            gwg_counters* counters, gwg_status* st) {
   NvtxRange nvtx_("gwg_run_grid_files");
   clear_status(st);
-  if (int rc = check_engine(e, st)) return rc;
+  if (int rc = check_engine(e, st, false)) return rc;  // joined before the first rotation
   if (!e->have_traits)
     return set_status(st, GWG_DIMENSION, -1, -1, "traits must be installed first");
   Fd in;

@@ -50,6 +50,14 @@ def step():
 for _ in range(2):
     step()
 torch.cuda.synchronize()
+import time as _t
+for _ in range(3):
+    a = _t.perf_counter()
+    eng.set_traits(y, h2, s2)
+    b_ = _t.perf_counter()
+    eng.run_grid(x, out=b, layout="numpy", mb=args.mb)
+    c = _t.perf_counter()
+    print(f"host: set_traits {1e3 * (b_ - a):.3f} ms, run_grid {1e3 * (c - b_):.3f} ms")
 import time
 t0 = time.perf_counter()
 step()
