@@ -1302,10 +1302,13 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
     if (in_place) {
       if (int rc = rotate(e, y, t, e->y_rot.d(), st, ldy)) return rc;
     } else {
-      if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st)) return rc;
+      // pitch n when TMA can address it (n even): one flat copy for a
+      // contiguous Y instead of a pitched one
+      const int64_t ldr = raw_ld(e);
+      if (int rc = upload_cols(e, e->y_raw, y, ldy, t, y_where, e->comp, st, ldr)) return rc;
       GWG_CUDA_TRY(cudaEventRecord(e->ev_traits_in, e->comp));
-    uploads_done = true;
-      if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st)) return rc;
+      uploads_done = true;
+      if (int rc = rotate(e, e->y_raw.d(), t, e->y_rot.d(), st, ldr)) return rc;
     }
   }
   const int64_t tiles_t = ceil_div(t, e->ops.bt);
