@@ -18,6 +18,9 @@
 #ifndef I8_NO_MMA
 #define I8_NO_MMA 0
 #endif
+#ifndef I8_MMA_NOWAIT  // timing ablation only: the MMA issuer does not wait for operands
+#define I8_MMA_NOWAIT 0
+#endif
 #ifndef I8_NO_TMA  // timing ablation only: stages marked full without loading them
 #define I8_NO_TMA 0
 #endif
@@ -907,7 +910,7 @@ __device__ __forceinline__ void i8_mma(const I8Smem<C>& sm, uint32_t tmem_base, 
 #if I8_PROFILE
       long long tf = clock64();
 #endif
-      mbar_wait_w<C::WS>(&sm.full[s], (g / C::STAGES) & 1);
+      if (!I8_MMA_NOWAIT) mbar_wait_w<C::WS>(&sm.full[s], (g / C::STAGES) & 1);
 #if I8_PROFILE
       t_full += clock64() - tf;
 #endif

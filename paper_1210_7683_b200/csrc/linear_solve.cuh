@@ -101,6 +101,9 @@ namespace gwg {
 #ifndef LIN_CTX_SMEM
 #define LIN_CTX_SMEM 1
 #endif
+#ifndef LIN_CTX_SLOTS  // context staging slots (>= the 2 accumulator buffers)
+#define LIN_CTX_SLOTS 4
+#endif
 
 // p % 4 == 0: results leave by direct 256-bit stores from registers (any
 // layout; no staging tiles), and the shared memory that frees holds each
@@ -174,12 +177,17 @@ struct LinCfg {
   static constexpr bool CTX_SMEM = LIN_CTX_SMEM != 0;
   static constexpr int CTX_DOUBLES = KT * CtxLayout<P>::STRIDE;
   static constexpr uint32_t CTX_BYTES = CTX_DOUBLES * 8;
-  static constexpr uint32_t SCALE_OFF = ACC * CTX_BYTES;
+  // context slots: tile lt uses slot lt % NCTX; with NCTX > ACC the context
+  // warp loads a tile's contexts NCTX - ACC tiles ahead of its epilogue
+  // instead of right after the same warps finished the tile before it
+  static constexpr int NCTX = LIN_CTX_SLOTS > ACC ? LIN_CTX_SLOTS : ACC;
+  static_assert(NCTX % ACC == 0, "a warp's tiles cycle through the slots in order");
+  static constexpr uint32_t SCALE_OFF = NCTX * CTX_BYTES;
   // NOSTAGE: per accumulator buffer the tile's S_BR box [KT traits][BM SNPs]
   static constexpr uint32_t SBR_BYTES = SBR_TMA ? KT * 128 * 8 : 0;
-  static constexpr uint32_t SBR_OFF = (SCALE_OFF + ACC * RB * 8 + 127) / 128 * 128;
-  static constexpr uint32_t BAR_OFF = SBR_OFF + ACC * SBR_BYTES;
-  static constexpr uint32_t EXTRA = CTX_SMEM ? BAR_OFF + 2 * ACC * 8 : 0;
+  static constexpr uint32_t SBR_OFF = (SCALE_OFF + NCTX * RB * 8 + 127) / 128 * 128;
+  static constexpr uint32_t BAR_OFF = SBR_OFF + NCTX * SBR_BYTES;
+  static constexpr uint32_t EXTRA = CTX_SMEM ? BAR_OFF + 2 * NCTX * 8 : 0;
   static constexpr size_t FIXED_B = size_t(EPI) * OUT_BUFS * 4096 + (EXTRA + 15) / 16 * 16 + 1280;
   static constexpr int STAGES = size_t(STAGES_0) * STAGE_B + FIXED_B <= 227 * 1024 ? STAGES_0
                                 : size_t(STAGES_0 - 1) * STAGE_B + FIXED_B <= 227 * 1024
@@ -260,9 +268,9 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
   double* const scale_sm = reinterpret_cast<double*>(sm.extra + L::SCALE_OFF);
   double* const sbr_sm = reinterpret_cast<double*>(sm.extra + L::SBR_OFF);
   uint64_t* const ctx_full = reinterpret_cast<uint64_t*>(sm.extra + L::BAR_OFF);
-  uint64_t* const ctx_empty = ctx_full + L::ACC;
+  uint64_t* const ctx_empty = ctx_full + L::NCTX;
   if (L::CTX_SMEM && threadIdx.x == 0) {  // fenced and published by i8_setup
-    for (int b = 0; b < L::ACC; ++b) {
+    for (int b = 0; b < L::NCTX; ++b) {
       mbar_init(&ctx_full[b], 1);
       mbar_init(&ctx_empty[b], 4 * L::HMAX);
     }
@@ -288,8 +296,8 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     if (L::CTX_SMEM && lane == 0) {
       const uint64_t pol = policy_evict_last();
       for (int lt = 0; lt < my_tiles; ++lt) {
-        const int buf = lt % L::ACC;
-        if (lt >= L::ACC) mbar_wait(&ctx_empty[buf], uint32_t((lt / L::ACC) - 1) & 1);
+        const int buf = lt % L::NCTX;
+        if (lt >= L::NCTX) mbar_wait(&ctx_empty[buf], uint32_t((lt / L::NCTX) - 1) & 1);
         int tm, tr;
         sch.coords(lt, tm, tr);
         const int j0 = tr * L::KT;
@@ -337,6 +345,8 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
     for (int lt = h; lt < my_tiles; lt += L::ACC) {
       const int buf = lt % L::ACC;
       const uint32_t par = uint32_t(lt / L::ACC) & 1;
+      const int cslot = lt % L::NCTX;                         // context slot
+      const uint32_t cpar = uint32_t(lt / L::NCTX) & 1;
       int tm, tr;
       sch.coords(lt, tm, tr);
       const int64_t il = int64_t(tm) * C::BM + qd * 32 + lane;
@@ -344,11 +354,11 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       const int j0 = tr * L::KT;  // first trait of the tile
       if (!active) {  // KT = 1 under WIDE: nothing to do but keep the buffer protocol
         mbar_wait(&sm.acc_full[buf], par);
-        if (L::CTX_SMEM) mbar_wait(&ctx_full[buf], par);
+        if (L::CTX_SMEM) mbar_wait(&ctx_full[cslot], cpar);
         __syncwarp();
         if (lane == 0) {
           i8_acc_release<C>(sm, buf);
-          if (L::CTX_SMEM) mbar_arrive(&ctx_empty[buf]);
+          if (L::CTX_SMEM) mbar_arrive(&ctx_empty[cslot]);
         }
         continue;
       }
@@ -368,15 +378,15 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       // without the staged copy, lane r holds the slice scale (sigma 2^-55) of
       // the tile's W row r (RB <= 32), shuffled to the recombination below
       const double sc_lane = !L::CTX_SMEM && lane < C::RB ? __ldg(a.scale + tr * C::RB + lane) : 0.0;
-      const double* const cx_tile = ctx_sm + buf * L::CTX_DOUBLES;
-      const double* const sc_tile = scale_sm + buf * C::RB;
+      const double* const cx_tile = ctx_sm + cslot * L::CTX_DOUBLES;
+      const double* const sc_tile = scale_sm + cslot * C::RB;
 #if LIN_TRACE
       const int tix = (lt - h) / L::ACC;
       const bool tr_on = blockIdx.x == 0 && lane == 0 && tix < 48;
       if (tr_on) g_lin_trace[ew][tix][0] = clock64();
 #endif
       mbar_wait(&sm.acc_full[buf], par);
-      if (L::CTX_SMEM) mbar_wait(&ctx_full[buf], par);
+      if (L::CTX_SMEM) mbar_wait(&ctx_full[cslot], cpar);
 #if LIN_TRACE
       if (tr_on) g_lin_trace[ew][tix][1] = clock64();
 #endif
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
           double cell[P + 1];
 #pragma unroll
           for (int c = 0; c < P; ++c) cell[c] = lin[u][c];
-          cell[P] = L::SBR_TMA ? sbr_sm[(buf * L::KT + cell0 + g0 + u) * 128 + qd * 32 + lane]
+          cell[P] = L::SBR_TMA ? sbr_sm[(cslot * L::KT + cell0 + g0 + u) * 128 + qd * 32 + lane]
                                : sbr[g0 + u];
           const double* cx = L::CTX_SMEM ? cx_tile + (cell0 + g0 + u) * CX::STRIDE
                                          : a.ctx + size_t(cv ? j : 0) * CX::STRIDE;
@@ -654,7 +664,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
       }
       if (L::CTX_SMEM) {  // this warp is done with the tile's contexts and scales
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctx_empty[buf]);
+        if (lane == 0) mbar_arrive(&ctx_empty[cslot]);
       }
       if (tma) nchunk += L::ROW / L::CHUNK;
 #if LIN_TRACE
