@@ -18,6 +18,9 @@
 #ifndef I8_NO_MMA
 #define I8_NO_MMA 0
 #endif
+#ifndef I8_EXP_A_ONCE
+#define I8_EXP_A_ONCE 0
+#endif
 #ifndef I8_MMA_NOWAIT  // timing ablation only: the MMA issuer does not wait for operands
 #define I8_MMA_NOWAIT 0
 #endif
@@ -806,7 +809,17 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
           if (lane_is_0()) tma_prefetch_3d(tmap_b, ksf * C::BK, trf * C::RB, sch.rank * C::B_SLICES_PER_CTA);
         }
       }
-      mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], C::STAGE_TX);
+      // timing probe only (I8_EXP_A_ONCE): the A box of the first K stage
+      // only, the rest left stale — how much the kernel gains without the
+      // per-stage SNP-tile ingress
+      const bool a_skip = I8_EXP_A_ONCE == 1 && C::PAIR_AXIS == 0 && (g % C::STAGES) != 0;
+      const bool b_skip = I8_EXP_A_ONCE == 2 && C::PAIR_AXIS == 0 && (g % C::STAGES) != 0;
+      mbar_arrive_expect_tx_w<C::WS>(&sm.full[s], a_skip ? C::STAGE_TX - C::A_BYTES
+                                                  : b_skip ? C::A_BYTES : C::STAGE_TX);
+      if (b_skip) {
+        tma_load_2d_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
+        continue;
+      }
       if constexpr (C::PAIR_AXIS == 2) {
         // 2 x 2: A rows [rb * 64, +64) to both CTAs of this SNP tile (ranks
         // sb, sb + 2), B slots [sb * 4, +4) to both CTAs of this B tile
@@ -830,7 +843,7 @@ __device__ __forceinline__ void i8_produce(const I8Smem<C>& sm, const CUtensorMa
         tma_load_3d_w<C::WS>(st + C::A_BYTES, tmap_b, ks * C::BK, tr * C::RB, 0, &sm.full[s], pol_b);
         continue;
       }
-      tma_load_2d_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
+      if (!a_skip) tma_load_2d_w<C::WS>(st, tmap_x, ks * C::BK, tm * C::BM, &sm.full[s], pol_x);
       if (C::CLUSTER > 1)
         tma_load_3d_mc_w<C::WS>(st + C::A_BYTES + sch.rank * C::B_PART,
                                 sch.rank ? tmap_bh : tmap_b, ks * C::BK, tr * C::RB,
