@@ -40,6 +40,9 @@ namespace gwg {
 #ifndef LIN_STREAM_HALF
 #define LIN_STREAM_HALF 0  // per-group boxes measured slower at c1 (2.37 vs 2.34 ms)
 #endif
+#ifndef LIN_STG_RECOMPUTE
+#define LIN_STG_RECOMPUTE 0
+#endif
 #ifndef LIN_STORE_EXP
 #define LIN_STORE_EXP 0
 #endif
@@ -574,7 +577,13 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             if (lane == 0) bulk_wait_read0();  // the previous tile's store has read it
             __syncwarp();
           }
-          double* rowp = reinterpret_cast<double*>(stg);
+          unsigned char* stg_now = stg;
+          if (LIN_STG_RECOMPUTE) {  // recomputed here instead of kept live (ptxas spilled it)
+            uint32_t tid;
+            asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+            stg_now = sm.staging + ((tid >> 5) - 4) * C::OUT_BYTES;
+          }
+          double* rowp = reinterpret_cast<double*>(stg_now);
 #pragma unroll
           for (int u = 0; u < L::GROUP; ++u)
 #pragma unroll
@@ -583,7 +592,7 @@ __global__ void __launch_bounds__(LinCfg<P, CL>::Tile::THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0)
-              tma_store_2d(&tmap_out, stg, (tm * C::BM + qd * 32) * P, j0 + cell0);
+              tma_store_2d(&tmap_out, stg_now, (tm * C::BM + qd * 32) * P, j0 + cell0);
           }
         } else if (tma) {
           // flat index f = (g0+u)*P + c of this row; 128-byte chunks of 16
