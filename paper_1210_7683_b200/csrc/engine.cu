@@ -48,6 +48,9 @@
 #ifndef SNP_I8_BLOCKS  // blocks per SM of the code conversion
 #define SNP_I8_BLOCKS 8
 #endif
+#ifndef SNP_I8_BLOCKS_BESIDE  // the same with the trait side running beside it
+#define SNP_I8_BLOCKS_BESIDE 8    // 2 (+ GWG_SMEM_CARVEOUT): measured neutral, off (below)
+#endif
 #ifndef GWG_COV_STREAM  // W's covariate columns on a helper stream beside the trait column
 #define GWG_COV_STREAM 0  // measured neutral at c1 (the rotation holds the SMs the covariate GEMMs need)
 #endif
@@ -418,6 +421,7 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   if (!e->slices_valid) {
     GWG_CUDA_TRY(e->zslices.ensure(size_t(I8Cfg::SLICES) * n * kp));
     GWG_CUDA_TRY(e->zscale.ensure(size_t(n) * sizeof(double)));
+    gwg::prefer_max_smem(gwg::slice_basis_kernel);
     gwg::slice_basis_kernel<<<int(n), 256, 0, e->comp>>>(
         e->basis.d(), e->np, int32_t(n), int32_t(n), int32_t(kp),
         static_cast<int8_t*>(e->zslices.ptr), e->zscale.d());
@@ -427,10 +431,23 @@ int rotate_snps(gwg_engine* e, const double* src, int64_t lds, int64_t cols, gwg
   }
   GWG_CUDA_TRY(e->xi8.ensure(size_t(cols) * kp));
   {
-    // a few blocks per SM (snp_to_i8_kernel): HBM-bound, leaves room for
-    // the trait side running concurrently
+    // HBM-bound, all blocks resident.  Measured and not kept: two blocks per
+    // SM plus the max-shared carveout (SNP_I8_BLOCKS_BESIDE = 2,
+    // GWG_SMEM_CARVEOUT = 1) whenever the trait side runs beside it — its
+    // 200 KB-CTA rotations then co-reside from the start instead of waiting
+    // for the conversion to drain (c1 "other" 0.31 -> 0.19 ms), but the
+    // conversion slows by the same 0.12 ms (step 4.23-4.27 vs 4.23-4.24 ms).
+    const bool beside = e->side_pending || (e->fork_pending && !e->split_valid);
+    const int per_sm = beside ? SNP_I8_BLOCKS_BESIDE : SNP_I8_BLOCKS;
     const int blocks = int(std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(cols, SNP_I8_ITEMS), int64_t(e->sms) * SNP_I8_BLOCKS)));
+        1, std::min<int64_t>(ceil_div(cols, SNP_I8_ITEMS), int64_t(e->sms) * per_sm)));
+    if (GWG_SMEM_CARVEOUT) {
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(gwg::snp_to_i8_kernel),
+                           cudaFuncAttributePreferredSharedMemoryCarveout,
+                           beside ? int(cudaSharedmemCarveoutMaxShared)
+                                  : int(cudaSharedmemCarveoutDefault));
+      (void)cudaGetLastError();
+    }
     gwg::snp_to_i8_kernel<<<blocks, 256, 0, e->comp>>>(
         src, lds, int32_t(n), int32_t(cols), int32_t(kp), static_cast<int8_t*>(e->xi8.ptr),
         static_cast<unsigned long long*>(e->err.ptr) + 2);
@@ -481,6 +498,7 @@ int rotate_snps_i8(gwg_engine* e, const int8_t* src, int64_t cols, gwg_status* s
   if (!e->slices_valid) {
     GWG_CUDA_TRY(e->zslices.ensure(size_t(I8Cfg::SLICES) * n * kp));
     GWG_CUDA_TRY(e->zscale.ensure(size_t(n) * sizeof(double)));
+    gwg::prefer_max_smem(gwg::slice_basis_kernel);
     gwg::slice_basis_kernel<<<int(n), 256, 0, e->comp>>>(
         e->basis.d(), e->np, int32_t(n), int32_t(n), int32_t(kp),
         static_cast<int8_t*>(e->zslices.ptr), e->zscale.d());
@@ -537,6 +555,7 @@ void invalidate_derived(gwg_engine* e, bool spectrum) {
 int spectrum_range(gwg_engine* e, gwg_status* st) {
   GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
   double* dx = e->exps.d();
+  gwg::prefer_max_smem(gwg::expsum_range_kernel);
   gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), e->n, nullptr, nullptr, 0,
                                                     dx);
   GWG_CUDA_TRY(cudaGetLastError());
@@ -585,6 +604,7 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
     GWG_CUDA_TRY(cudaEventSynchronize(e->ev_range));
     std::copy(e->range_host, e->range_host + 6, rg);
   } else {  // device-resident inputs: one small reduction and a round trip
+    gwg::prefer_max_smem(gwg::expsum_range_kernel);
     gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), n, e->h2.d(),
                                                       e->sigma2.d(), int32_t(t), dx);
     GWG_CUDA_TRY(cudaGetLastError());
@@ -635,8 +655,10 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   e->ex_lam0 = rg[0];
   a.epanel = e->epanel.d();
   a.fpanel = e->fpanel.d();
+  gwg::prefer_max_smem(gwg::expsum_e_kernel);
   gwg::expsum_e_kernel<<<r, 256, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
+  gwg::prefer_max_smem(gwg::expsum_f_kernel);
   gwg::expsum_f_kernel<<<int(t), 128, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 2;
@@ -706,6 +728,7 @@ int build_split(gwg_engine* e, gwg_status* st) {
   a.dpanel = e->dpanel.d();
   a.v = e->vmat.d();
   a.y_only = fact ? 1 : 0;
+  gwg::prefer_max_smem(gwg::split_prep_kernel);
   gwg::split_prep_kernel<<<int(t), 256, 0, e->comp>>>(a);
   GWG_CUDA_TRY(cudaGetLastError());
   e->counters.kernel_launches += 1;
@@ -756,6 +779,7 @@ int build_split(gwg_engine* e, gwg_status* st) {
     x.ldx = np;
     x.ncx = int32_t(p - 1);
     x.panel_out = e->xepanel.d();
+    gwg::prefer_max_smem(gwg::expsum_e_kernel);
     gwg::expsum_e_kernel<<<int(rc_cols), 256, 0, e->comp>>>(x);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
@@ -796,12 +820,14 @@ int build_split(gwg_engine* e, gwg_status* st) {
     f.z = co.z;
     f.flag = co.flag;
     f.linv = co.linv;
+    gwg::prefer_max_smem(gwg::fold_w_kernel);
     gwg::fold_w_kernel<<<int(t), 256, 0, e->comp>>>(f);
     GWG_CUDA_TRY(cudaGetLastError());
     e->counters.kernel_launches += 1;
   }
   GWG_CUDA_TRY(e->wslices.ensure(size_t(I8Cfg::SLICES) * ncols * kp));
   GWG_CUDA_TRY(e->wscale.ensure(size_t(ncols) * sizeof(double)));
+  gwg::prefer_max_smem(gwg::slice_basis_kernel);
   gwg::slice_basis_kernel<<<int(ncols), 256, 0, e->comp>>>(e->wmat.d(), np, int32_t(n),
                                                           int32_t(ncols), int32_t(kp),
                                                           static_cast<int8_t*>(e->wslices.ptr),
@@ -852,6 +878,7 @@ int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64
   GWG_CUDA_TRY(so.launch(map, q, int(std::min<int64_t>(supers, e->sms)), e->comp));
   e->counters.kernel_launches += 1;
   if (ksplit > 1) {  // dense dst (ldd = cols, rowmajor) = the partials in order
+    gwg::prefer_max_smem(gwg::sum_partials_kernel);
     gwg::sum_partials_kernel<<<int(std::min<int64_t>(ceil_div(split_stride, 256), 4 * e->sms)),
                                256, 0, e->comp>>>(partials, split_stride, ksplit, split_stride,
                                                   dst);
@@ -1273,6 +1300,7 @@ int set_traits_body(gwg_engine* e, int64_t t, const double* y, int64_t ldy, int 
     // device busy while the 48-byte answer travels, so the split grid's
     // build finds it on the host without stalling the device
     GWG_CUDA_TRY(e->exps.ensure(size_t(8 + 2 * 512) * sizeof(double)));
+    gwg::prefer_max_smem(gwg::expsum_range_kernel);
     gwg::expsum_range_kernel<<<1, 256, 0, e->comp>>>(e->lambda.d(), e->n, e->h2.d(),
                                                       e->sigma2.d(), int32_t(t), e->exps.d());
     GWG_CUDA_TRY(cudaGetLastError());

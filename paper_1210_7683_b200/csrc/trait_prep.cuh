@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(256) trait_prep_kernel(const PrepArgs a) {
 // trait side.  Launch helper.
 template <int P, int BT>
 inline cudaError_t launch_trait_prep(const PrepArgs& a, cudaStream_t s) {
+  prefer_max_smem(trait_prep_kernel<P, BT>);
   trait_prep_kernel<P, BT><<<a.t, 256, 0, s>>>(a);
   return cudaGetLastError();
 }

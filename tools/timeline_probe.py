@@ -26,6 +26,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--m", type=int, default=100_000)
 ap.add_argument("--option", action="append", default=[])
+ap.add_argument("--host", action="store_true", help="also list host runtime API calls")
 args = ap.parse_args()
 
 n, p, m, t, seed = 1000, 4, args.m, 1000, 20261019
@@ -71,12 +72,14 @@ for e in prof.events():
 for e in prof.profiler.function_events:
     if e.device_type == torch.autograd.DeviceType.CUDA:
         evs.append((e.time_range.start, e.time_range.end, getattr(e, "device_resource_id", 0) or e.thread, e.name))
+    elif args.host and e.name.startswith("cuda"):
+        evs.append((e.time_range.start, e.time_range.end, "H", e.name))
 evs.sort()
 if not evs:
     print("no device events captured")
     sys.exit(1)
 # split into steps at each trait_prep launch (one per set_traits)
-starts = [i for i, ev in enumerate(evs) if "trait_prep" in ev[3]]
+starts = [i for i, ev in enumerate(evs) if "trait_prep" in ev[3] and ev[2] != "H"]
 print(f"{len(evs)} device events, {len(starts)} steps")
 for si in range(len(starts)):
     lo = starts[si]
