@@ -1,0 +1,99 @@
+"""The device path against outputs of the REFERENCE ITSELF (-m gpu).
+
+* tests/golden/ref_grids.npz: grids the reference's own sources produced in
+  the build container (tests/golden/make_ref_golden.py; /root/reference does
+  not exist on the GPU box).  Inputs regenerate bit-identically from the
+  counter-based generator, so only seeds and outputs are stored.
+* when the prebuilt reference library travelled with the repo
+  (oracle/_ref/libgwgrid_ref.so: gwgrid's gls.cpp / grid.cpp / stream.cpp ...
+  compiled against our Eigen stand-in), the reference's streamed CT engine is
+  also run live on the box's host cores at n = 1000, p = 4 and compared with
+  the device on every cell, and its GWG1 reader decodes the result stream our
+  engine's file leg wrote.
+
+Tolerances as in tests/test_gpu_parity.py: norm-wise <= 1e-10 per cell,
+components within 1e-8 floored at 1e-6 of the cell norm (typical 1e-14).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1210_7683_b200 as gw  # noqa: E402
+from oracle import ref  # noqa: E402
+from oracle.parity import parity_metrics  # noqa: E402
+from paper_1210_7683_b200 import datagen, gwg1  # noqa: E402
+from tests.golden import make_ref_golden as golden  # noqa: E402
+from tests.test_gpu_parity import assert_parity  # noqa: E402
+
+have_ref_build = pytest.mark.skipif(not os.path.exists(ref.LIB_PATH),
+                                    reason="prebuilt reference library did not travel")
+
+
+def codings(kind):
+    # genotype codes run the default (auto -> exact int8 split grid), the
+    # explicit genotype coding and the all-FP64 path; real values only the latter
+    return ("auto", "genotypes", "real") if kind == "codes" else ("auto", "real")
+
+
+@pytest.mark.parametrize("name", sorted(golden.CASES))
+def test_device_matches_reference_goldens(name):
+    want = golden.load()[name]
+    ds = golden.inputs(name)
+    kind = golden.CASES[name][5]
+    for coding in codings(kind):
+        res = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                            ds["sigma2"], snp_coding=coding)
+        assert res["b"].shape == want["b"].shape
+        assert_parity(res["b"], want["b"])
+        ci, cj = golden.cholesky_cells(name)
+        rel = np.linalg.norm(res["b"][ci, cj] - want["chol"], axis=1) / np.linalg.norm(
+            want["chol"], axis=1)
+        assert rel.max() <= 1e-9, (coding, rel.max())
+
+
+@have_ref_build
+@pytest.mark.parametrize("coding", ["auto", "real"])
+def test_device_matches_live_reference_every_cell(coding):
+    """configs[0]/[1]'s n and p, 3,000 SNPs x 300 traits (9e5 cells): the
+    reference's streamed CT engine on the host against the device."""
+    ds = datagen.generate(1000, 4, 3000, 300, seed=77)
+    want = ref.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                          ds["sigma2"], workers=min(16, os.cpu_count() or 1))
+    got = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"], ds["sigma2"],
+                        snp_coding=coding)["b"]
+    pm = parity_metrics(got, want)
+    print(f"device ({coding}) vs live reference build, 9e5 cells:", pm)
+    assert pm["normwise_max"] <= 1e-10, pm
+    assert pm["floored5_componentwise_max"] <= 1e-8, pm
+    assert pm["n_floored_over_1e-8"] <= 1, pm
+
+
+@have_ref_build
+@pytest.mark.parametrize("coding", ["genotypes", "real"])
+def test_reference_reader_decodes_engine_result_stream(tmp_path, coding):
+    """stream.cpp:414-445 / 83-200: the result stream written by
+    gwg_run_grid_files is a valid, complete kind-3 stream for the reference's
+    reader, cell for cell; the reference's engine over the same input files
+    agrees with it."""
+    ds = datagen.generate(120, 3, 257, 19, seed=13)
+    snp_path, trait_path = str(tmp_path / "snps.gwg"), str(tmp_path / "traits.gwg")
+    out_path, ref_out = str(tmp_path / "b.gwg"), str(tmp_path / "b_ref.gwg")
+    gwg1.write_snp_stream(snp_path, ds["snps"])
+    gwg1.write_trait_stream(trait_path, ds["traits"], ds["h2"], ds["sigma2"])
+    with gw.Engine(120, 3) as eng:
+        eng.set_spectrum(*gw.eigendecompose(ds["kinship"]))
+        eng.set_covariates(ds["xl"])
+        eng.set_snp_coding(coding)
+        eng.set_traits_file(trait_path)
+        eng.run_grid_files(snp_path, out_path, mb=100)
+    decoded = ref.read_result(out_path)
+    assert np.array_equal(decoded, gwg1.read_result(out_path))
+    ref.run_grid_files(ds["kinship"], ds["xl"], snp_path, trait_path, ref_out, workers=2)
+    assert_parity(decoded, ref.read_result(ref_out))
