@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
             "ref_run_grid_files": [I64, I64, P, P, C, C, C, C, I32, I32, I64, I64, I64, I64, I64,
                                    I32, P, S],
             "ref_read_result": [C, P, P, I64, S],
+            "ref_compute_grid": [I64, I64, I64, I64, P, P, P, P, P, P, P, I32, I64, I64, I64, P, S],
         }.items():
             fn = getattr(lib, name)
             fn.argtypes = args
@@ -237,4 +238,24 @@ def read_result(path):
     out = np.empty(tuple(int(d) for d in dims))
     _check(load().ref_read_result(str(path).encode(), dims.ctypes.data, _ptr(out), out.size,
                                   ctypes.byref(st)), st)
+    return out
+
+
+def compute_grid(basis, values, xl, snps, traits, h2, sigma2, workers=1, mb=8192, mbb=0, tbb=0):
+    """run_grid's in-core traversal (grid.cpp:495-556) without the file legs,
+    from UNROTATED operands and a given eigensystem: rotate X_L and the trait
+    slab, build_trait_contexts, then per slab of mb variant columns
+    transform_snp_slab + compute_tile (CT blocks, `workers` pool threads; the
+    rotation's dgemm uses OpenBLAS's own threads).  b as (m, t, p)."""
+    basis, values, snps, traits = _f(basis), _f(values), _f(snps), _f(traits)
+    n = basis.shape[0]
+    xl = _f(xl).reshape(n, -1, order="F")
+    p = xl.shape[1] + 1
+    m, t = snps.shape[1], traits.shape[1]
+    h2, sigma2 = _f(h2), _f(sigma2)
+    out = np.empty((m, t, p))
+    st = _Status()
+    _check(load().ref_compute_grid(n, p, m, t, _ptr(basis), _ptr(values), _ptr(xl), _ptr(snps),
+                                   _ptr(traits), _ptr(h2), _ptr(sigma2), workers, min(mb, m), mbb,
+                                   tbb, _ptr(out), ctypes.byref(st)), st)
     return out

@@ -19,6 +19,7 @@
 
 #include "gwgrid/gls.hpp"
 #include "gwgrid/grid.hpp"
+#include "gwgrid/pool.hpp"
 #include "gwgrid/stream.hpp"
 #include "gwgrid/types.hpp"
 
@@ -298,6 +299,58 @@ int ref_read_result(const char* path, std::int64_t* dims, double* b, std::int64_
     for (std::int64_t j = 0; j < t; ++j)
       for (std::int64_t i = 0; i < m; ++i)
         results.read_result_cell(i, j, b + (static_cast<std::size_t>(i) * t + j) * p);
+  });
+}
+
+// The in-core traversal of run_grid (grid.cpp:495-556) without the file
+// legs: rotate the covariates and the trait slab, build the contexts once,
+// then per slab of mb variant columns transform_snp_slab + compute_tile (CT
+// blocks on a WorkerPool).  Used as the timed CPU path of the reference
+// build (bench.py --impl reference) and for in-memory pins.  b is (m, t, p).
+int ref_compute_grid(std::int64_t n, std::int64_t p, std::int64_t m, std::int64_t t,
+                     const double* basis, const double* values, const double* xl,
+                     const double* snps, const double* traits, const double* h2,
+                     const double* sigma2, int workers, std::int64_t mb, std::int64_t mbb,
+                     std::int64_t tbb, double* b, ref_status* st) {
+  return guarded(st, [&] {
+    GridPrecompute pre;
+    pre.spectrum = spectrum_of(n, basis, values);
+    const Eigen::MatrixXd xlm = mat(xl, n, p - 1);
+    pre.xl_rot.resize(n, p - 1);
+    if (p > 1) rotate_columns(pre.spectrum.basis, xlm, pre.xl_rot);
+    Eigen::MatrixXd trait_slab = mat(traits, n, t);
+    transform_trait_slab(pre, trait_slab, nullptr);
+    std::vector<TraitScalars> scalars(static_cast<std::size_t>(t));
+    for (std::int64_t j = 0; j < t; ++j) {
+      scalars[static_cast<std::size_t>(j)].h2 = h2[j];
+      scalars[static_cast<std::size_t>(j)].sigma2 = sigma2[j];
+    }
+    const std::vector<TraitContext> contexts =
+        build_trait_contexts(pre, trait_slab, scalars, 0, nullptr);
+    ProblemDims dims;
+    dims.n = n;
+    dims.p = p;
+    dims.m = m;
+    dims.t = t;
+    TileParams flags;
+    flags.mb = mb;
+    flags.mbb = mbb;
+    flags.tbb = tbb;
+    const TileParams params = flags.resolved(dims);
+    WorkerPool pool(workers);
+    Eigen::MatrixXd raw(n, params.mb), rot(n, params.mb);
+    ResultTile tile;
+    for (std::int64_t i0 = 0; i0 < m; i0 += params.mb) {
+      const std::int64_t rows = std::min(params.mb, m - i0);
+      std::memcpy(raw.data(), snps + i0 * n, sizeof(double) * static_cast<std::size_t>(rows * n));
+      transform_snp_slab(pre, raw.leftCols(rows), rot.leftCols(rows), nullptr);
+      tile.reset(i0, 0, rows, t, p);
+      compute_tile(contexts, rot.leftCols(rows), params, tile, &pool, nullptr);
+      for (std::int64_t jl = 0; jl < t; ++jl)
+        for (std::int64_t il = 0; il < rows; ++il)
+          std::memcpy(b + (static_cast<std::size_t>(i0 + il) * t + jl) * p, tile.cell(il, jl),
+                      sizeof(double) * static_cast<std::size_t>(p));
+    }
   });
 }
 
