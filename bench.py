@@ -384,8 +384,10 @@ def run_ours(args):
 
         cpu, ref = cpu_baseline(args, shared, x_host)
         got = b_dev.cpu().numpy()
-        parity = parity_metrics(got if args.layout == "numpy" else got.transpose(1, 0, 2), ref)
+        got = got if args.layout == "numpy" else got.transpose(1, 0, 2)
+        parity = parity_metrics(got, ref)
         del ref
+        parity["vs_reference_build"] = parity_vs_reference_build(args, shared, x_host, got)
 
     if rank == 0:
         line = {
@@ -525,6 +527,28 @@ def run_reference(args):
                 "inputs from the oracle library's copy of the generator (no engine code loaded)",
     }
     print(json.dumps(line), flush=True)
+
+
+def parity_vs_reference_build(args, shared, x_host, got, sample=10_000):
+    """The timed device grid against the REFERENCE'S OWN sources
+    (oracle/_ref/libgwgrid_ref.so, gwgrid compiled in place against the Eigen
+    stand-in) on the first `sample` SNPs x all traits, when the prebuilt
+    library is present (test infrastructure; never on the product path)."""
+    from oracle import ref
+    from oracle.parity import parity_metrics
+
+    if not os.path.exists(ref.LIB_PATH):
+        return {"unavailable": "oracle/_ref/libgwgrid_ref.so not present"}
+    ms = min(sample, x_host.shape[1])
+    h2 = shared["h2"].cpu().numpy()
+    want = ref.compute_grid(shared["basis"].cpu().numpy(), shared["values"].cpu().numpy(),
+                            shared["xl"].cpu().numpy(), np.asfortranarray(x_host[:, :ms]),
+                            shared["y"].cpu().numpy(), h2, np.ones(len(h2)),
+                            workers=os.cpu_count() or 1)
+    pm = parity_metrics(np.ascontiguousarray(got[:ms]), want)
+    pm["reference"] = ("gwgrid's own rotate_columns + build_trait_contexts + compute_tile "
+                       f"(oracle/_ref), first {ms} SNPs x {len(h2)} traits")
+    return pm
 
 
 def reference_build_sample(basis, values, xl, y, h2, xs, workers, sample=10_000):
