@@ -97,3 +97,31 @@ def test_reference_reader_decodes_engine_result_stream(tmp_path, coding):
     assert np.array_equal(decoded, gwg1.read_result(out_path))
     ref.run_grid_files(ds["kinship"], ds["xl"], snp_path, trait_path, ref_out, workers=2)
     assert_parity(decoded, ref.read_result(ref_out))
+
+
+DROPIN = os.path.join(os.path.dirname(ref.LIB_PATH), "dropin_run_grid")
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="prebuilt drop-in program did not travel")
+@pytest.mark.parametrize("shape", [
+    "96 4 300 50 128 20 7 real",        # ragged slabs, 3 trait passes
+    "200 4 500 300 256 300 8 codes",    # raw genotype codes -> exact int8 path, t >= 256
+    "120 1 64 9 64 4 9 real",           # p = 1
+    "1000 4 2000 100 512 100 10 real",  # configs 0/1's n and p
+    "150 12 90 40 90 16 11 codes",      # p = 12, trait passes
+])
+def test_dropin_inside_reference_run_grid(tmp_path, shape):
+    """INTEGRATION.md section 1 as a program (oracle/refbuild/dropin_run_grid.cpp):
+    the reference's own run_grid traversal (its generator, GWG1 streams,
+    TileParams, ResultTile, result writer, compiled from its sources) with
+    load_pass -> gwg_set_traits and compute_tile -> gwg_solve_snp_slab, against
+    the reference's run_grid on the CPU: every cell norm-wise <= 1e-10, the same
+    NotPositiveDefiniteError coordinates for a zero variant column, and no
+    readable output after the failure."""
+    import subprocess
+
+    run = subprocess.run([DROPIN, str(tmp_path)] + shape.split(), capture_output=True, text=True,
+                         timeout=600)
+    print(run.stdout)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "status=ok" in run.stdout
