@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--snp-coding", default="genotypes", choices=["genotypes", "real"],
                     help="BASELINE X_R are genotype codes {0,1,2}: exact int8 tcgen05 rotation")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise torch.distributed (NCCL) and run the broadcast / barrier / "
+                         "max-over-ranks code even at world size 1 (exercises the multi-GPU "
+                         "plumbing on a one-GPU box; needs the torchrun environment)")
     ap.add_argument("--no-alt-coding", dest="alt_coding", action="store_false",
                     help="skip timing the other SNP coding on the same data")
     ap.add_argument("--no-cpu", action="store_true",
@@ -171,7 +175,8 @@ def run_ours(args):
     from paper_1210_7683_b200 import multi
 
     world, rank, local = multi.dist_env()
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -197,14 +202,14 @@ def run_ours(args):
         eng.solve_snp_slab(x_dev, out=b_dev, i0=i0, layout=args.layout)
 
     def barrier():
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
 
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
+        if not use_dist:
             return v
         import torch.distributed as dist
 
@@ -422,7 +427,7 @@ def run_ours(args):
             line["config"]["engine_options"] = args.option
         print(json.dumps(line), flush=True)
     eng.close()
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
 
         dist.destroy_process_group()

@@ -76,7 +76,7 @@ def broadcast_shared(shared: dict | None, n: int, p: int, t: int, device=None,
             buf = torch.from_numpy(a).to(device) if device is not None else torch.from_numpy(a)
         else:
             buf = torch.empty(shapes[key], dtype=torch.float64, device=device)
-        if dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.is_initialized():  # (a no-op at world size 1, kept to exercise the call)
             dist.broadcast(buf, src=src)
         out[key] = buf.t() if buf.dim() == 2 else buf
     return out
