@@ -58,18 +58,33 @@ def test_device_matches_reference_goldens(name):
         assert rel.max() <= 1e-9, (coding, rel.max())
 
 
+LIVE_SHAPES = {
+    # configs[0]/[1]'s n and p
+    "c0_c1": (1000, 4, 3000, 300, 77),
+    # configs[3]: many traits per SNP slab (t >> m)
+    "c3": (1000, 4, 256, 4096, 78),
+    # configs[4]: n = 2000, p = 20 (one trait per int8 tile, precomputed L^-1 solve)
+    "c4": (2000, 20, 600, 256, 79),
+}
+
+
 @have_ref_build
 @pytest.mark.parametrize("coding", ["auto", "real"])
-def test_device_matches_live_reference_every_cell(coding):
-    """configs[0]/[1]'s n and p, 3,000 SNPs x 300 traits (9e5 cells): the
-    reference's streamed CT engine on the host against the device."""
-    ds = datagen.generate(1000, 4, 3000, 300, seed=77)
+@pytest.mark.parametrize("shape", sorted(LIVE_SHAPES))
+def test_device_matches_live_reference_every_cell(shape, coding):
+    """The reference's streamed CT engine (its own sources, built in the
+    container) run live on the box's host cores against the device, every
+    cell, at the n / p / t regimes of BASELINE's configs."""
+    n, p, m, t, seed = LIVE_SHAPES[shape]
+    ds = datagen.generate(n, p, m, t, seed=seed)
     want = ref.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
                           ds["sigma2"], workers=min(16, os.cpu_count() or 1))
     got = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"], ds["sigma2"],
                         snp_coding=coding)["b"]
     pm = parity_metrics(got, want)
-    print(f"device ({coding}) vs live reference build, 9e5 cells:", pm)
+    print(f"device ({coding}) vs live reference build, {shape} {m * t} cells: "
+          f"normwise {pm['normwise_max']:.3e} floored {pm['floored_componentwise_max']:.3e} "
+          f"raw {pm['raw_componentwise_max']:.3e}")
     assert pm["normwise_max"] <= 1e-10, pm
     assert pm["floored5_componentwise_max"] <= 1e-8, pm
     assert pm["n_floored_over_1e-8"] <= 1, pm
