@@ -77,6 +77,8 @@ def load() -> ctypes.CDLL:
             "ref_run_grid_files": [I64, I64, P, P, C, C, C, C, I32, I32, I64, I64, I64, I64, I64,
                                    I32, P, S],
             "ref_read_result": [C, P, P, I64, S],
+            "ref_generate_dataset": [C, I64, I64, I64, I64, ctypes.c_uint64, D, S],
+            "ref_load_dataset": [C, P, P, S],
             "ref_compute_grid": [I64, I64, I64, I64, P, P, P, P, P, P, P, I32, I64, I64, I64, P, S],
         }.items():
             fn = getattr(lib, name)
@@ -259,3 +261,24 @@ def compute_grid(basis, values, xl, snps, traits, h2, sigma2, workers=1, mb=8192
                                    _ptr(traits), _ptr(h2), _ptr(sigma2), workers, min(mb, m), mbb,
                                    tbb, _ptr(out), ctypes.byref(st)), st)
     return out
+
+
+def generate_dataset(directory, n, p, m, t, seed=1, condition=100.0):
+    """gwgrid::generate_dataset (datagen.cpp:263-315): a gwgrid-dataset-1
+    directory (manifest.txt + four GWG1 streams) from the reference's own
+    generator."""
+    st = _Status()
+    _check(load().ref_generate_dataset(str(directory).encode(), n, p, m, t, seed, condition,
+                                       ctypes.byref(st)), st)
+
+
+def load_dataset(manifest_path):
+    """gwgrid::load_manifest + read_dense on a dataset somebody else wrote:
+    ((n, p, m, t), sums of the kinship / xl / snps / traits / h2 / sigma2
+    payloads as the reference read them)."""
+    dims = np.zeros(4, dtype=np.int64)
+    sums = np.zeros(6)
+    st = _Status()
+    _check(load().ref_load_dataset(str(manifest_path).encode(), dims.ctypes.data, sums.ctypes.data,
+                                   ctypes.byref(st)), st)
+    return tuple(int(d) for d in dims), sums

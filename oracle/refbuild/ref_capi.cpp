@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "gwgrid/datagen.hpp"
 #include "gwgrid/gls.hpp"
 #include "gwgrid/grid.hpp"
 #include "gwgrid/pool.hpp"
@@ -351,6 +352,46 @@ int ref_compute_grid(std::int64_t n, std::int64_t p, std::int64_t m, std::int64_
           std::memcpy(b + (static_cast<std::size_t>(i0 + il) * t + jl) * p, tile.cell(il, jl),
                       sizeof(double) * static_cast<std::size_t>(p));
     }
+  });
+}
+
+// A gwgrid-dataset-1 directory written by the reference's own generator
+// (datagen.cpp:263-315: manifest.txt + kinship / xl / snps / traits streams).
+int ref_generate_dataset(const char* dir, std::int64_t n, std::int64_t p, std::int64_t m,
+                         std::int64_t t, std::uint64_t seed, double condition, ref_status* st) {
+  return guarded(st, [&] {
+    GenSpec spec;
+    spec.dims.n = n;
+    spec.dims.p = p;
+    spec.dims.m = m;
+    spec.dims.t = t;
+    spec.seed = seed;
+    spec.condition = condition;
+    generate_dataset(spec, dir);
+  });
+}
+
+// A dataset directory somebody else wrote (our CLI's generate), parsed by the
+// reference's load_manifest (datagen.cpp:317-396) and read by its stream
+// reader: dims[4] = n, p, m, t from the manifest; sums[6] = plain sums of the
+// kinship, xl, snps, traits, h2 and sigma2 payloads as the reference read them.
+int ref_load_dataset(const char* manifest_path, std::int64_t* dims, double* sums, ref_status* st) {
+  return guarded(st, [&] {
+    const DatasetManifest man = load_manifest(manifest_path);
+    dims[0] = man.spec.dims.n;
+    dims[1] = man.spec.dims.p;
+    dims[2] = man.spec.dims.m;
+    dims[3] = man.spec.dims.t;
+    sums[0] = read_dense(man.paths.kinship, StreamKind::operand).sum();
+    sums[1] = man.spec.dims.p > 1 ? read_dense(man.paths.xl, StreamKind::operand).sum() : 0.0;
+    sums[2] = read_dense(man.paths.snps, StreamKind::snp).sum();
+    sums[3] = read_dense(man.paths.traits, StreamKind::trait).sum();
+    const InputStream traits = InputStream::open(man.paths.traits, StreamKind::trait);
+    std::vector<double> h2(static_cast<std::size_t>(traits.count())), s2(h2.size());
+    traits.read_scalars(0, traits.count(), h2.data(), s2.data());
+    sums[4] = sums[5] = 0.0;
+    for (double v : h2) sums[4] += v;
+    for (double v : s2) sums[5] += v;
   });
 }
 

@@ -140,3 +140,35 @@ def test_dropin_inside_reference_run_grid(tmp_path, shape):
     print(run.stdout)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "status=ok" in run.stdout
+
+
+@have_ref_build
+def test_cli_solves_a_reference_generated_dataset(tmp_path):
+    """A gwgrid-dataset-1 directory written by the reference's own
+    generate_dataset (datagen.cpp:263-315) goes through our CLI's solve and
+    verify; the result stream equals the reference engine's over the same
+    files to rounding."""
+    import subprocess
+    import sys
+
+    from paper_1210_7683_b200 import cli
+
+    d = tmp_path / "ds"
+    ref.generate_dataset(d, 150, 4, 400, 30, seed=21)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(*args):
+        r = subprocess.run([sys.executable, "-m", "paper_1210_7683_b200", *args], cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        return r.returncode, dict(ln.split("=", 1) for ln in r.stdout.splitlines() if "=" in ln), r
+
+    rc, kv, r = run("solve", "--data", str(d))
+    assert rc == 0 and kv["status"] == "ok", r.stderr
+    rc, kv2, r = run("verify", "--data", str(d), "--sample", "300")
+    assert rc == 0 and kv2["status"] == "ok" and float(kv2["max_rel_err"]) < 1e-10, r.stdout
+    man = cli.load_manifest(str(d))
+    kin = gwg1.read_columns(man["kinship"], gwg1.KIND_OPERAND)
+    xl = gwg1.read_columns(man["xl"], gwg1.KIND_OPERAND)
+    ref_out = str(tmp_path / "b_ref.gwg")
+    ref.run_grid_files(kin, xl, man["snps"], man["traits"], ref_out, workers=4)
+    assert_parity(ref.read_result(kv["out"]), ref.read_result(ref_out))

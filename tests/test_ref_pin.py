@@ -299,6 +299,43 @@ def test_compute_grid_in_core_matches_streamed_reference():
 
 
 @live
+def test_dataset_directories_interoperate_with_reference(tmp_path):
+    """gwgrid-dataset-1 (datagen.cpp:241-396) both ways: a directory written by
+    the reference's generate_dataset is read by our manifest parser and codec;
+    a directory written by our CLI's generate is accepted by the reference's
+    load_manifest and read by its stream reader to the same payload sums."""
+    from paper_1210_7683_b200 import cli
+
+    theirs = tmp_path / "theirs"
+    ref.generate_dataset(theirs, 40, 3, 25, 7, seed=5)
+    man = cli.load_manifest(str(theirs))
+    assert (man["n"], man["p"], man["m"], man["t"]) == (40, 3, 25, 7)
+    kin = gwg1.read_columns(man["kinship"], gwg1.KIND_OPERAND)
+    xl = gwg1.read_columns(man["xl"], gwg1.KIND_OPERAND)
+    snps = gwg1.read_columns(man["snps"], gwg1.KIND_SNP)
+    assert kin.shape == (40, 40) and xl.shape == (40, 2) and snps.shape == (40, 25)
+    assert np.array_equal(kin, kin.T)
+    dims, sums = ref.load_dataset(theirs / "manifest.txt")
+    assert dims == (40, 3, 25, 7)
+    assert np.isclose(sums[0], kin.sum(), rtol=1e-13) and np.isclose(sums[2], snps.sum(), rtol=1e-13)
+    # the reference's engine over its own dataset == the oracle on what our codec read
+    raw = np.fromfile(man["traits"], dtype="<f8", offset=gwg1.HEADER)
+    traits, h2, s2 = raw[:40 * 7].reshape((40, 7), order="F"), raw[280:287], raw[287:294]
+    out = str(tmp_path / "b.gwg")
+    ref.run_grid_files(kin, xl, man["snps"], man["traits"], out)
+    got = orc.solve_grid(kin, xl, snps, traits, h2, s2)
+    assert normwise(got, ref.read_result(out)) <= 1e-12
+
+    ours = str(tmp_path / "ours")
+    ds = cli.write_dataset(ours, 36, 4, 20, 6, seed=9)
+    dims, sums = ref.load_dataset(os.path.join(ours, "manifest.txt"))
+    assert dims == (36, 4, 20, 6)
+    want = [ds["kinship"].sum(), ds["xl"].sum(), ds["snps"].sum(), ds["traits"].sum(),
+            ds["h2"].sum(), ds["sigma2"].sum()]
+    assert np.allclose(sums, want, rtol=1e-12, atol=1e-12)
+
+
+@live
 def test_config0_every_cell_matches_reference():
     """BASELINE configs[0] (n=1000, p=4, m=10,000, t=100), all 1e6 cells:
     oracle vs the reference's streamed CT engine."""
