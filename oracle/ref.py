@@ -5,6 +5,9 @@ grid.cpp, stream.cpp, pool.cpp, pipeline.cpp, types.cpp) compiled where they
 lie under /root/reference by oracle/refbuild/Makefile, against our stand-in for
 <Eigen/Dense> (Eigen3 is absent from the image; see the stand-in's header for
 what that carries over), behind the small C face oracle/refbuild/ref_capi.cpp.
+The same Makefile builds the reference's acceptance program, its seven doctest
+suites (doctest stand-in) and its command-line tool (CLI11 stand-in) into
+oracle/_ref/ for tests/test_ref_pin.py and tests/test_gpu_ref_golden.py.
 It is used to pin oracle/gls_oracle.cpp (tests/test_ref_pin.py) and to write
 the golden vectors tests/golden/ref_*.npz (tests/golden/make_ref_golden.py).
 Only tests/ may import this module.  /root/reference does not exist on the

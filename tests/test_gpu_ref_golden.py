@@ -172,3 +172,60 @@ def test_cli_solves_a_reference_generated_dataset(tmp_path):
     ref_out = str(tmp_path / "b_ref.gwg")
     ref.run_grid_files(kin, xl, man["snps"], man["traits"], ref_out, workers=4)
     assert_parity(ref.read_result(kv["out"]), ref.read_result(ref_out))
+
+
+REF_TOOL = os.path.join(os.path.dirname(ref.LIB_PATH), "gwgrid")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="prebuilt reference CLI did not travel")
+@pytest.mark.parametrize("coding", ["auto", "real"])
+def test_reference_cli_verifies_device_results(tmp_path, coding):
+    """The reference's OWN command-line tool (proj/tools/gwgrid_main.cpp built
+    against the stand-ins) generates a dataset; our CLI solves it on the
+    device; the reference's `verify --exhaustive` (its CholeskyOracle over
+    every cell, gwgrid_main.cpp:300-404) accepts the device's result stream.
+    The other way round, our `verify` accepts the result stream the
+    reference's `solve` wrote."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = str(tmp_path / "ds")
+
+    def kv(stdout):
+        return dict(ln.split("=", 1) for ln in stdout.splitlines() if "=" in ln)
+
+    def theirs(*args):
+        r = subprocess.run([REF_TOOL, *args], capture_output=True, text=True, timeout=600)
+        return r.returncode, kv(r.stdout), r
+
+    def ours(*args):
+        r = subprocess.run([sys.executable, "-m", "paper_1210_7683_b200", *args], cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        return r.returncode, kv(r.stdout), r
+
+    rc, out, r = theirs("generate", "--n", "96", "--p", "4", "--m", "220", "--t", "24", "--seed", "3",
+                        "--out", d)
+    assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
+    dev_out, cpu_out = str(tmp_path / "b_dev.gwg"), str(tmp_path / "b_cpu.gwg")
+    rc, out, r = ours("solve", "--data", d, "--out", dev_out, "--snp-coding", coding)
+    assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
+    rc, out, r = theirs("verify", "--data", d, "--results", dev_out, "--exhaustive")
+    print("reference verify of the device results:", out)
+    assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
+    assert float(out["max_rel_err"]) < 1e-10
+
+    rc, out, r = theirs("solve", "--data", d, "--out", cpu_out, "--workers", "2")
+    assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
+    rc, out, r = ours("verify", "--data", d, "--results", cpu_out, "--sample", "400")
+    assert rc == 0 and out["status"] == "ok" and float(out["max_rel_err"]) < 1e-10, r.stdout
+    assert_parity(gwg1.read_result(dev_out), gwg1.read_result(cpu_out))
+    # a corrupted cell is caught by the reference's verifier with exit code 3
+    raw = np.fromfile(dev_out, dtype=np.uint8)
+    cell = np.frombuffer(raw[gwg1.HEADER + 8 * 40:gwg1.HEADER + 8 * 41].tobytes(), dtype="<f8")[0]
+    raw[gwg1.HEADER + 8 * 40:gwg1.HEADER + 8 * 41] = np.frombuffer(
+        np.array([cell * 1.001 + 1e-3], dtype="<f8").tobytes(), dtype=np.uint8)
+    bad = str(tmp_path / "b_bad.gwg")
+    raw.tofile(bad)
+    rc, out, r = theirs("verify", "--data", d, "--results", bad, "--exhaustive")
+    assert rc == 3, r.stdout
