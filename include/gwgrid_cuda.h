@@ -367,6 +367,13 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st);
  * queued on the engine's side stream (gwg_set_traits) is joined into it first. */
 void* gwg_compute_stream(gwg_engine* e);
 
+/* The SNP-slab width gwg_run_grid / gwg_run_grid_files use for an m-column run
+ * when gwg_run_options.mb is 0, for the traits currently installed (whole
+ * tile waves near a 96 MB result slab): the resolved `mb` that the reference's
+ * solve report prints (TileParams::resolved, grid.cpp:37-62).  0 if no traits
+ * are installed. */
+int64_t gwg_default_slab_snps(gwg_engine* e, int64_t m);
+
 /* Positive exponential sum for 1/x on [x_min, x_max] (the low-rank
  * factorisation of the GLS weights behind the genotype grid's S_BR term, see
  * csrc/expsum.cpp):  1/x ~= sum_r w[r] exp(-s[r] x),  s[0] = 0, all w > 0,

@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "gwg_reset_counters",
     "gwg_synchronize",
     "gwg_compute_stream",
+    "gwg_default_slab_snps",
     "gwg_verify_grid",
     "gwg_stream_info",
     "gwg_set_traits_file",
@@ -173,6 +174,7 @@ def load() -> ctypes.CDLL:
         "gwg_reset_counters": (None, [P]),
         "gwg_synchronize": (I32, [P, S]),
         "gwg_compute_stream": (P, [P]),
+        "gwg_default_slab_snps": (I64, [P, I64]),
         "gwg_gen_genotypes": (None, [U64, I32, I64, I64, I64, I32, P, I64]),
         "gwg_gen_normals": (None, [U64, I32, I64, I64, I64, P, I64]),
         "gwg_gen_uniform": (None, [U64, I32, I64, D, D, P]),

@@ -125,16 +125,29 @@ def cmd_solve(a) -> int:
     eng = _engine_for(man, a.device_eig, a.snp_coding)
     t1 = time.perf_counter()
     try:
+        mb = int(a.mb) if a.mb else eng.default_slab_snps(man["m"])
         c = eng.run_grid_files(man["snps"], out, mb=a.mb)
     finally:
         eng.close()
     t2 = time.perf_counter()
+    # every key of the reference's solve report (gwgrid_main.cpp:233-298), in
+    # its order, plus the device's own (snp_coding, grid_flops, kernel_launches,
+    # grid_kernel_seconds).  The device tiling: one trait pass (tb = t), SNP
+    # slabs of mb columns that are also the transfer unit (nb = mb), no host
+    # cache blocks (mbb = mb, tbb = t), rotation on the device (no transformed
+    # stream is written).
+    mb = min(mb, man["m"])
+    stall = float(c.get("io_stall_ms", 0.0)) * 1e-3
+    loops = t2 - t1
     print(f"scheduler=gpu\nsnp_coding={a.snp_coding}\nn={man['n']}\np={man['p']}\nm={man['m']}\nt={man['t']}")
+    print(f"workers=1\nnb={mb}\nmb={mb}\ntb={man['t']}\nmbb={mb}\ntbb={man['t']}\ntransformed=")
     for k in ("preloop_flops", "loop_flops", "grid_flops", "context_builds", "bytes_loaded",
               "bytes_stored", "kernel_launches"):
         print(f"{k}={c[k]}")
     print(f"loop_transform_flops=0\ngrid_kernel_seconds={fmt(c['grid_kernel_ms'] * 1e-3)}\n"
-          f"loops_wall_seconds={fmt(t2 - t1)}\npreloop_wall_seconds={fmt(t1 - t0)}\n"
+          f"io_stall_seconds={fmt(stall)}\n"
+          f"loops_wall_seconds={fmt(loops)}\npreloop_wall_seconds={fmt(t1 - t0)}\n"
+          f"stall_fraction={fmt(stall / loops if loops > 0 else 0.0)}\nwall_time_s={fmt(loops)}\n"
           f"total_wall_seconds={fmt(t2 - t0)}\nout={out}\nstatus=ok")
     return OK
 

@@ -1812,6 +1812,11 @@ int32_t gwg_synchronize(gwg_engine* e, gwg_status* st) {
   return GWG_OK;
 }
 
+int64_t gwg_default_slab_snps(gwg_engine* e, int64_t m) {
+  if (!e || e->t <= 0 || m <= 0) return 0;
+  return default_slab(e, m);
+}
+
 void* gwg_compute_stream(gwg_engine* e) {
   if (!e) return nullptr;
   if (cudaSetDevice(e->device) == cudaSuccess) (void)join_side(e);  // side work ordered first

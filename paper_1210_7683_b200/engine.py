@@ -429,6 +429,10 @@ class Engine:
         handle = getattr(stream, "cuda_stream", stream)
         self._call(self._lib.gwg_wait_stream, int(handle))
 
+    def default_slab_snps(self, m: int) -> int:
+        """The slab width run_grid uses for m SNP columns when mb = 0."""
+        return int(self._lib.gwg_default_slab_snps(self._h, int(m)))
+
     @property
     def compute_stream(self) -> int:
         return int(self._lib.gwg_compute_stream(self._h) or 0)

@@ -215,8 +215,16 @@ def test_reference_cli_verifies_device_results(tmp_path, coding):
     assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
     assert float(out["max_rel_err"]) < 1e-10
 
+    their_verify_keys = set(out)
     rc, out, r = theirs("solve", "--data", d, "--out", cpu_out, "--workers", "2")
     assert rc == 0 and out["status"] == "ok", r.stdout + r.stderr
+    # our reports carry every key of the reference tool's (a script parsing
+    # the reference's key=value lines keeps working)
+    rc, mine, r = ours("solve", "--data", d, "--out", dev_out, "--snp-coding", coding)
+    assert rc == 0 and set(out) <= set(mine), sorted(set(out) - set(mine))
+    assert int(mine["mb"]) >= 1 and int(mine["tb"]) == 24 and float(mine["stall_fraction"]) >= 0.0
+    rc, mine, r = ours("verify", "--data", d, "--results", dev_out, "--exhaustive")
+    assert rc == 0 and their_verify_keys <= set(mine), sorted(their_verify_keys - set(mine))
     rc, out, r = ours("verify", "--data", d, "--results", cpu_out, "--sample", "400")
     assert rc == 0 and out["status"] == "ok" and float(out["max_rel_err"]) < 1e-10, r.stdout
     assert_parity(gwg1.read_result(dev_out), gwg1.read_result(cpu_out))
