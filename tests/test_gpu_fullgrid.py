@@ -112,3 +112,39 @@ def test_every_cell_of_a_full_n_p_t_slab(name, n, p, m, t, s):
     print(f"\n{name}: " + json.dumps({k: v for k, v in res.items() if k != "reference"}))
     assert res["normwise_max"] <= 1e-10, res
     assert res["floored5_componentwise_max"] <= 1e-8, res
+
+
+def test_config1_full_size_device_vs_live_reference_every_cell():
+    """BASELINE configs[1] at full size (1e8 cells) against the REFERENCE'S OWN
+    sources (oracle/_ref/libgwgrid_ref.so: gwgrid's rotate_columns +
+    build_trait_contexts + compute_tile CT, built in the container against the
+    Eigen stand-in) run live on the box's host cores, in slabs of 20,000 SNPs
+    (2e7 cells each) so that only one reference slab is resident."""
+    from oracle import ref as refbuild
+
+    if not os.path.exists(refbuild.LIB_PATH):
+        pytest.skip("prebuilt reference library did not travel")
+    n, p, m, t = CONFIGS["c1"]
+    ds = datagen.generate(n, p, m, t, seed=20260816)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    with gw.Engine(n, p) as eng:
+        eng.set_spectrum(basis, values)
+        eng.set_covariates(ds["xl"])
+        eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+        b = eng.run_grid(ds["snps"])
+    workers = os.cpu_count() or 1
+    worst = {"normwise_max": 0.0, "floored_componentwise_max": 0.0, "floored5_componentwise_max": 0.0,
+             "raw_componentwise_max": 0.0, "n_floored_over_1e-8": 0, "n_raw_over_1e-8": 0}
+    step = 20_000
+    for i0 in range(0, m, step):
+        want = refbuild.compute_grid(basis, values, ds["xl"],
+                                     np.asfortranarray(ds["snps"][:, i0:i0 + step]), ds["traits"],
+                                     ds["h2"], ds["sigma2"], workers=workers)
+        pm = parity_metrics(np.ascontiguousarray(b[i0:i0 + step]), want)
+        for k in worst:
+            worst[k] = worst[k] + pm[k] if k.startswith("n_") else max(worst[k], pm[k])
+        del want
+    print("c1 full size (1e8 cells), device vs live reference build:", json.dumps(worst))
+    assert worst["normwise_max"] <= 1e-10, worst
+    assert worst["floored5_componentwise_max"] <= 1e-8, worst
+    assert worst["n_floored_over_1e-8"] <= 4e8 * 1e-6, worst

@@ -237,3 +237,21 @@ def test_reference_cli_verifies_device_results(tmp_path, coding):
     raw.tofile(bad)
     rc, out, r = theirs("verify", "--data", d, "--results", bad, "--exhaustive")
     assert rc == 3, r.stdout
+
+
+@have_ref_build
+def test_config0_full_size_device_vs_live_reference_every_cell():
+    """BASELINE configs[0] at full size (n=1000, p=4, m=10,000, t=100: the
+    reference's own CPU-runnable case), all 1e6 cells: the reference's streamed
+    CT engine run live on the host against the device's default path."""
+    ds = datagen.generate(1000, 4, 10_000, 100, seed=20260816)
+    want = ref.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"],
+                          ds["sigma2"], workers=min(16, os.cpu_count() or 1))
+    got = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"], ds["sigma2"])["b"]
+    pm = parity_metrics(got, want)
+    print(f"c0 full size, device vs live reference build: normwise {pm['normwise_max']:.3e} "
+          f"floored {pm['floored_componentwise_max']:.3e} raw {pm['raw_componentwise_max']:.3e} "
+          f"({pm['n_raw_over_1e-8']} raw components over 1e-8 of {pm['components']})")
+    assert pm["normwise_max"] <= 1e-10, pm
+    assert pm["floored5_componentwise_max"] <= 1e-8, pm
+    assert pm["n_floored_over_1e-8"] <= 4, pm
