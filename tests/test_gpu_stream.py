@@ -7,6 +7,9 @@ in-memory run.  References: run_grid / pipeline_run
 (proj/src/grid.cpp:454-641, proj/include/gwgrid/pipeline.hpp:78-137),
 write_result_cells (proj/src/stream.cpp:414-445), sampled verification
 (proj/tools/gwgrid_main.cpp:336-353)."""
+import os
+import queue
+
 import numpy as np
 import pytest
 
@@ -373,3 +376,67 @@ def test_trait_side_stream_interleavings(case):
         eng.solve_snp_slab(x, out=out2)
         got = out2.cpu().numpy()  # torch's stream is ordered after the engine
         assert np.array_equal(got, ref2)
+
+
+def _nccl_rank_worker(port, q):
+    """One torch.distributed rank on cuda:0 with the NCCL backend (a one-GPU
+    box can host a world of one): multi.solve_sharded with the device engine
+    as the per-rank solve — the code path of every rank of bench.py --gpus N."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1210_7683_b200 import multi
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1",
+                      LOCAL_RANK="0")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    n, p, m, t = 200, 4, 700, 40
+
+    def make_shared():
+        ds = datagen.generate(n, p, 1, t, seed=12)
+        z, lam = gw.eigendecompose(ds["kinship"])
+        return {"basis": z, "values": lam, "xl": ds["xl"], "y": ds["traits"], "h2": ds["h2"],
+                "sigma2": ds["sigma2"]}
+
+    def load_shard(i0, i1):
+        return datagen.genotypes(12, datagen.M_SNPS, n, i0, i1 - i0)
+
+    res = multi.solve_sharded(n, p, m, t, make_shared, load_shard, multi.engine_compute(0),
+                              device=torch.device("cuda", 0))
+    q.put((res["i0"], res["i1"], np.asarray(res["b"]), res["checksum"]))
+    dist.destroy_process_group()
+
+
+def test_solve_sharded_with_the_engine_under_nccl():
+    """multi.solve_sharded + multi.engine_compute under an NCCL process group
+    on the GPU (world size 1): NCCL broadcasts of the shared operands into
+    HBM, the engine fed from those device tensors, the checksum all-gather —
+    equal, bit for bit, to the single-engine grid and its checksum."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_rank_worker, args=(port, q))
+    pr.start()
+    got = None
+    for _ in range(300):  # a crashed worker fails the test at once, not after the timeout
+        try:
+            got = q.get(timeout=1)
+            break
+        except queue.Empty:
+            if not pr.is_alive():
+                break
+    pr.join(timeout=120)
+    assert got is not None and pr.exitcode == 0, f"worker exit code {pr.exitcode}"
+    i0, i1, b, checksum = got
+    assert (i0, i1) == (0, 700)
+    ds = datagen.generate(200, 4, 700, 40, seed=12)
+    whole = gw.solve_grid(ds["kinship"], ds["xl"], ds["snps"], ds["traits"], ds["h2"], ds["sigma2"],
+                          checksum=True)
+    assert np.array_equal(b, whole["b"])
+    assert checksum == whole["counters"]["checksum"] == gw.grid_checksum(whole["b"])
