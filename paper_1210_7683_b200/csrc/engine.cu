@@ -635,7 +635,15 @@ int build_expsum(gwg_engine* e, gwg_status* st) {
   }
   const int64_t bt = e->sops.bt;
   const int64_t t_pad = round_up(t, bt);
-  GWG_CUDA_TRY(e->epanel.ensure(size_t(r) * np * sizeof(double)));
+  // (+ slack: the split-K G GEMM may read up to 7 K-chunks past the last
+  // trait tile's panel; they meet zero-filled SNP-side tiles, so they only
+  // have to be finite: zeroed)
+  {
+    const size_t panel = size_t(r) * np * sizeof(double);
+    const size_t slack = size_t(8) * e->sops.bk * e->sops.bt * sizeof(double);
+    GWG_CUDA_TRY(e->epanel.ensure(panel + slack));
+    GWG_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(e->epanel.ptr) + panel, 0, slack, e->comp));
+  }
   GWG_CUDA_TRY(e->fpanel.ensure(size_t(t_pad) * r * sizeof(double)));
   if (t_pad != t)  // padded traits of the last tile contribute zeros
     GWG_CUDA_TRY(cudaMemsetAsync(e->fpanel.d() + size_t(t_pad - bt) * r, 0,
@@ -852,7 +860,7 @@ int build_split(gwg_engine* e, gwg_status* st) {
 int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
              const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
              bool rowmajor, gwg_status* st, int ksplit, double* partials,
-             int64_t split_stride) {
+             int64_t split_stride, int64_t pad_chunks) {
   const gwg::SbrOps& so = e->sops;
   CUtensorMap map;
   if (int rc = encode_kmajor(&map, a_op, kext, rows, lda, so.bm, st)) return rc;
@@ -864,7 +872,7 @@ int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64
   q.t = int32_t(cols);
   q.tiles_m = int32_t(ceil_div(rows, so.bm));
   q.tiles_t = int32_t(ceil_div(cols, so.bt));
-  q.kchunks = int32_t(pk / so.bk);
+  q.kchunks = int32_t(pk / so.bk + pad_chunks);  // padded chunks: A out of bounds = zeros
   q.np = pk;
   q.rowmajor = rowmajor ? 1 : 0;
   q.gate = gate_word(e);
@@ -902,8 +910,24 @@ int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t 
                                          : uint64_t(e->n) * uint64_t(t));
   if (const int64_t r = e->sbr_terms) {
     GWG_CUDA_TRY(e->gmat.ensure(size_t(rows) * r * sizeof(double)));
-    if (int rc = gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true))
+    // G = (X'.X')^T E has only r = 64..512 columns: a slab of a few thousand
+    // SNPs is a few dozen tiles (config 2's default 3,000-SNP slab: 24 CTAs,
+    // 0.65 ms per slab, a quarter of the streamed run's grid time).  From
+    // K >= 2048 on, K is split into up to 8 parts of >= 32 chunks, summed in a
+    // fixed order.  The split depends on n alone, never on the slab, so results
+    // stay bitwise independent of the slab width; below 2048 nothing changes.
+    int ksplit = 1;
+    const int64_t kchunks = e->np / e->sops.bk;
+    while (ksplit < 8 && ceil_div(kchunks, int64_t(2 * ksplit)) >= 32) ksplit *= 2;
+    if (ksplit > 1) {
+      const int64_t kc_per = ceil_div(kchunks, int64_t(ksplit));
+      GWG_CUDA_TRY(e->gpart.ensure(size_t(ksplit) * rows * r * sizeof(double)));
+      if (int rc = sbr_gemm(e, rot_sq, e->n, e->np, rows, e->epanel.d(), e->np, r, e->gmat.d(), r,
+                            true, st, ksplit, e->gpart.d(), rows * r, kc_per * ksplit - kchunks))
+        return rc;
+    } else if (int rc = gemm(rot_sq, e->n, e->np, e->epanel.d(), e->np, r, e->gmat.d(), r, true)) {
       return rc;
+    }
     return gemm(e->gmat.d(), r, r, e->fpanel.d(), r, t, e->sbr.d(), ld_s, false);
   }
   return gemm(rot_sq, e->n, e->np, e->dpanel.d(), e->np, t, e->sbr.d(), ld_s, false);
@@ -1554,7 +1578,7 @@ void gwg_engine_destroy(gwg_engine* e) {
                     &e->sigma2, &e->bops, &e->ctx, &e->raw[0], &e->raw[1], &e->rot, &e->rot_sq, &e->out[0],
                     &e->out[1], &e->stage, &e->err, &e->zslices, &e->zscale, &e->xi8, &e->basis_t, &e->vmat, &e->wmat,
                     &e->wslices, &e->wscale, &e->dpanel, &e->sbr, &e->epanel, &e->fpanel,
-                    &e->gmat, &e->exps, &e->xepanel, &e->umat, &e->upart, &e->raw8[0], &e->raw8[1], &e->csum})
+                    &e->gmat, &e->gpart, &e->exps, &e->xepanel, &e->umat, &e->upart, &e->raw8[0], &e->raw8[1], &e->csum})
     b->release();
   if (e->err_host) cudaFreeHost(e->err_host);
   if (e->range_host) cudaFreeHost(e->range_host);

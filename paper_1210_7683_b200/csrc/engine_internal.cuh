@@ -163,7 +163,7 @@ struct gwg_engine {
   // FP64 path: S_BR from the factorised GEMMs and the grid kernel without the
   // D column (GWG_OPT_REAL_SPLIT = 0 keeps the fused S_BR)
   bool real_split = true;
-  gwg_host::DevBuf epanel, fpanel, gmat, exps;
+  gwg_host::DevBuf epanel, fpanel, gmat, gpart, exps;
   gwg_host::DevBuf xepanel, umat, upart;  // upart: split-K partials of U  // W build through the factorisation: diag(X_L'_c) E, Z diag(X_L'_c) E
   // host copies of lambda / h2 / sigma2 when they were passed from the host:
   // the factorisation's range is then found without a device round trip
@@ -246,7 +246,7 @@ int prepare_expsum(gwg_engine* e, gwg_status* st);
 int sbr_gemm(gwg_engine* e, const double* a_op, int64_t kext, int64_t lda, int64_t rows,
              const double* panel, int64_t pk, int64_t cols, double* dst, int64_t ldd,
              bool rowmajor, gwg_status* st, int ksplit = 1, double* partials = nullptr,
-             int64_t split_stride = 0);
+             int64_t split_stride = 0, int64_t pad_chunks = 0);
 int launch_sbr_stage(gwg_engine* e, const double* rot_sq, int64_t rows, int64_t ld_s,
                      gwg_status* st);
 int launch_fused(gwg_engine* e, const double* rot, const double* rot_sq, int64_t rows, int64_t i0,

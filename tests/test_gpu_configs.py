@@ -68,3 +68,29 @@ def test_config3_many_traits(coding):
 @pytest.mark.parametrize("coding", ["real", "genotypes"])
 def test_config4_many_covariates(coding):
     print(run_config(2000, 20, 2000, 2000, 700, 200, 200, 4, device_eig=False, coding=coding))
+
+
+def test_split_k_g_gemm_is_slab_invariant_and_matches_oracle():
+    """From K >= 2048 the S_BR stage's G = (X'.X')^T E GEMM splits K by n alone
+    (launch_sbr_stage); n = 2080 gives 65 K-chunks -> two parts of 33 with one
+    zero-padded chunk.  Results: bitwise independent of the slab width (the
+    split never depends on the slab) and equal to the oracle to rounding, on
+    both codings (the FP64 path factorises S_BR too for t >= 256)."""
+    from oracle import oracle as orc
+    from tests.test_gpu_parity import assert_parity
+
+    n, p, m, t = 2080, 3, 700, 260
+    ds = datagen.generate(n, p, m, t, seed=41)
+    basis, values = gw.eigendecompose(ds["kinship"])
+    ref = orc.compute_grid(values, orc.rotate(basis, ds["xl"]), orc.rotate(basis, ds["snps"]),
+                           orc.rotate(basis, ds["traits"]), ds["h2"], ds["sigma2"], workers=8)
+    for coding in ("genotypes", "real"):
+        with gw.Engine(n, p) as eng:
+            eng.set_spectrum(basis, values)
+            eng.set_covariates(ds["xl"])
+            eng.set_snp_coding(coding)
+            eng.set_traits(ds["traits"], ds["h2"], ds["sigma2"])
+            whole = eng.run_grid(ds["snps"], mb=700)
+            for mb in (100, 333):
+                assert np.array_equal(eng.run_grid(ds["snps"], mb=mb), whole), (coding, mb)
+        assert_parity(whole, ref)
