@@ -53,7 +53,7 @@ def link_bandwidth(nbytes: int = 1 << 30, reps: int = 3) -> dict:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c3", choices=["c2", "c3"])
+    ap.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3", "c4"])
     ap.add_argument("--m", type=int, default=0, help="SNPs (default: the config's m)")
     ap.add_argument("--mb", type=int, default=0)
     ap.add_argument("--ring", type=int, default=3)
